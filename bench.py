@@ -1,0 +1,437 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 gpu module.
+
+Workload (BASELINE.json configs[1], "cfg2"): int16 [4096,4096] viewed
+transposed with a reversed axis (strides (-8192, 2)) plus a float32 [1,4096]
+row broadcast, `add(V, R)` -> float32 [4096,4096].  One step = one pass of
+the hot path over that batch; algorithmic bytes = 2 (int16 read) + 4 (f32
+write) per element + the 16 KiB row = 100,679,680 B.  The gpu module fuses
+the int16->float32 conversion into the add (one kernel).  L2 is flushed
+(256 MiB memset) between timed steps.
+
+`--impl reference` times the reference CPU implementation of the same
+path (the C restatement in oracle/, all host threads) on a bounded sample.
+
+Prints ONE JSON line.  Multi-GPU: run under torchrun; every rank runs its
+own cfg2 instance (weak scaling), times are max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "elementwise/reduce HBM GB/s vs ~8 TB/s; gemm TFLOP/s; at 1/2/4/8 B200"
+N = 4096
+CFG2_BYTES = N * N * (2 + 4) + N * 4
+FLUSH_BYTES = 256 << 20
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (torch.distributed gloo: barrier + max over ranks)
+# ---------------------------------------------------------------------------
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+            self.dist = dist
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled while the benchmark runs
+# ---------------------------------------------------------------------------
+REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x2: "applications_clocks_setting"}
+
+
+class Clocks:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 4:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), float(parts[2]),
+                                         int(parts[3], 16)))
+                except ValueError:
+                    pass
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        load = [s for s in self.samples if s[2] > 0] or self.samples
+        if not load:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        reasons = set()
+        for s in load:
+            for bit, name in REASONS.items():
+                if s[3] & bit:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[0] for s in load),
+                "sm_max_mhz": max(s[1] for s in load), "reasons": sorted(reasons),
+                "samples": len(load)}
+
+
+# ---------------------------------------------------------------------------
+# timing helpers over the C ABI
+# ---------------------------------------------------------------------------
+class Timer:
+    def __init__(self, L, stream):
+        self.L, self.stream = L, stream
+
+    def event(self):
+        e = C.c_void_p()
+        self.L.tpg_event_create(C.byref(e))
+        return e.value
+
+    def elapsed(self, a, b):
+        ms = C.c_float()
+        self.L.tpg_event_elapsed(a, b, C.byref(ms))
+        return ms.value
+
+
+def timed_steps(L, stream, step, steps, flush=None, gate=True):
+    """Run `steps` steps with events around each; optional L2 flush before
+    each step (outside the events).  Returns per-step device ms."""
+    from paper_1810_08723_b200 import _native
+    t = Timer(L, stream.handle)
+    evs = [(t.event(), t.event()) for _ in range(steps)]
+    if gate:
+        _native.check(L.tpg_gate_arm(stream.handle))
+    for s, e in evs:
+        if flush:
+            flush()
+        L.tpg_event_record(s, stream.handle)
+        step()
+        L.tpg_event_record(e, stream.handle)
+    if gate:
+        L.tpg_gate_release()
+    stream.sync()
+    out = [t.elapsed(s, e) for s, e in evs]
+    for s, e in evs:
+        L.tpg_event_destroy(s)
+        L.tpg_event_destroy(e)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+def cfg2_inputs(tp, dev):
+    rng3, rng4 = np.random.default_rng(3), np.random.default_rng(4)
+    x16 = np.asfortranarray(rng3.integers(-1000, 1000, (N, N), endpoint=True).astype(np.int16))
+    r = np.asfortranarray(rng4.standard_normal((1, N)).astype(np.float32))
+    X = tp.from_numpy(x16, dev)
+    R = tp.from_numpy(r, dev)
+    V = tp.apply_index(tp.transpose(X), (slice(None, None, -1), slice(None)))
+    assert V.strides == (-8192, 2), V.strides
+    return x16, r, X, R, V
+
+
+def bench_cfg2(tp, dev, steps, warmup, L):
+    x16, r, X, R, V = cfg2_inputs(tp, dev)
+    out = tp.tensor_create((N, N), tp.float, dev)
+    stream = dev.default_stream()
+    flush_buf = dev.allocate(FLUSH_BYTES)
+    it = [0]
+
+    def flush():
+        it[0] += 1
+        L.tpg_memset(flush_buf, it[0] & 0xFF, FLUSH_BYTES, stream.handle)
+
+    def step():
+        tp.add(V, R, dest=out)
+
+    for _ in range(warmup):
+        flush()
+        step()
+    stream.sync()
+    ms = timed_steps(L, stream, step, steps, flush)
+    # end to end through the public API with host buffers: H2D of the
+    # step's inputs from pinned memory, the op, D2H of the result
+    hx = C.c_void_p()
+    hr = C.c_void_p()
+    ho = C.c_void_p()
+    L.tpg_host_alloc(x16.nbytes, C.byref(hx))
+    L.tpg_host_alloc(r.nbytes, C.byref(hr))
+    L.tpg_host_alloc(N * N * 4, C.byref(ho))
+    C.memmove(hx.value, x16.ctypes.data, x16.nbytes)
+    C.memmove(hr.value, r.ctypes.data, r.nbytes)
+
+    def e2e_step():
+        L.tpg_memcpy_h2d(X.storage.ptr, hx.value, x16.nbytes, stream.handle)
+        L.tpg_memcpy_h2d(R.storage.ptr, hr.value, r.nbytes, stream.handle)
+        tp.add(V, R, dest=out)
+        L.tpg_memcpy_d2h(ho.value, out.storage.ptr, N * N * 4, stream.handle)
+
+    for _ in range(2):
+        e2e_step()
+    stream.sync()
+    e2e_steps = max(3, steps // 4)
+    t0 = time.perf_counter()
+    e2e_ms = timed_steps(L, stream, e2e_step, e2e_steps, None, gate=False)
+    wall = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    # correctness spot check against the host result of the same bytes
+    got = np.frombuffer((C.c_char * (N * N * 4)).from_address(ho.value), dtype=np.float32)
+    want = (x16.T[::-1, :].astype(np.float64) + r.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(got.reshape((N, N), order="F"), want), "cfg2 e2e result mismatch"
+    for h in (hx, hr, ho):
+        L.tpg_host_free(h.value)
+    dev.release(flush_buf, stream)
+    return ms, e2e_ms, wall, x16.nbytes + r.nbytes, N * N * 4
+
+
+def extras(tp, dev, L, warmup=3, steps=5):
+    """Kernel-level numbers for the other configs, rank 0."""
+    res = {}
+    stream = dev.default_stream()
+    flush_buf = dev.allocate(FLUSH_BYTES)
+
+    def flush():
+        L.tpg_memset(flush_buf, 0, FLUSH_BYTES, stream.handle)
+
+    def run(name, step, nbytes=None, flops=None, fl=True, st=steps):
+        for _ in range(warmup):
+            step()
+        stream.sync()
+        ms = timed_steps(L, stream, step, st, flush if fl else None)
+        m = statistics.median(ms)
+        rec = {"ms": round(m, 4)}
+        if nbytes:
+            rec["GB/s"] = round(nbytes / m / 1e6, 1)
+        if flops:
+            rec["TFLOP/s"] = round(flops / m / 1e9, 1)
+        res[name] = rec
+
+    rng = np.random.default_rng(1)
+    a = tp.from_numpy(rng.standard_normal(1 << 20).astype(np.float32), dev)
+    b = tp.from_numpy(rng.standard_normal(1 << 20).astype(np.float32), dev)
+    o = tp.tensor_create((1 << 20,), tp.float, dev)
+    run("cfg1_add_f32_2^20", lambda: tp.add(a, b, dest=o), nbytes=12 << 20)
+    del a, b, o
+
+    X = tp.from_numpy(np.asfortranarray(np.random.default_rng(5).random((8192, 8192))), dev)
+    nb = 8192 * 8192 * 8
+    for op in ("sum", "maximum", "norm"):
+        for axes, tag in (((0,), "axis0"), ((1,), "axis1"), (None, "full")):
+            run(f"cfg3_{op}_{tag}_f64_8192^2", lambda op=op, axes=axes: tp.reduce(op, X, axes=axes),
+                nbytes=nb)
+    del X
+
+    n5 = 1 << 28  # a quarter of cfg5's 2^30 per step keeps extras short
+    s = np.random.default_rng(8).uniform(-1e3, 1e3, n5).astype(">f8")
+    S = tp.from_numpy(s, dev)
+    Y = tp.tensor_create((n5,), tp.float, dev)
+    run("cfg5_cast_f64BE_to_f32_2^28", lambda: tp.copy(S, Y), nbytes=12 * n5, fl=False)
+    Z = tp.tensor_create((n5,), tp.float, dev)
+    k15, km2 = tp.Scalar(1.5, tp.float), tp.Scalar(-2.0, tp.float)
+    run("cfg5_multiply_scalar_f32_2^28", lambda: tp.multiply(Y, k15, dest=Z), nbytes=8 * n5,
+        fl=False)
+    run("cfg5_add_scalar_f32_2^28", lambda: tp.add(Z, km2, dest=Y), nbytes=8 * n5, fl=False)
+    del S, Y, Z
+    s16 = tp.from_numpy(np.random.default_rng(9).integers(-3000, 3000, n5).astype(">i2"), dev)
+    h16 = tp.tensor_create((n5,), tp.half, dev)
+    run("cfg5_cast_i16BE_to_f16_2^28", lambda: tp.copy(s16, h16), nbytes=4 * n5, fl=False)
+    del s16, h16
+
+    for dname, dt in (("f16", tp.half), ("bf16", tp.bfloat16), ("f32", tp.float)):
+        m = 4096
+        base = np.random.default_rng(6).uniform(-1, 1, (m, m)).astype(np.float32)
+        if dt is tp.bfloat16:
+            raw = (base.view(np.uint32) >> 16).astype(np.uint16)
+            A = tp.from_numpy(np.asfortranarray(raw), dev, dtype=tp.bfloat16)
+            B = tp.from_numpy(np.asfortranarray(raw), dev, dtype=tp.bfloat16)
+        else:
+            npd = np.float16 if dt is tp.half else np.float32
+            A = tp.from_numpy(np.asfortranarray(base.astype(npd)), dev)
+            B = tp.from_numpy(np.asfortranarray(base.astype(npd)), dev)
+        At = tp.transpose(A)  # K-major A, as SURVEY cfg4
+        Cm = tp.tensor_create((m, m), dt, dev)
+        run(f"cfg4_gemm_{dname}_{m}^3", lambda: tp.matmul(At, B, dest=Cm), flops=2 * m ** 3,
+            fl=False, st=3)
+    dev.release(flush_buf, stream)
+    return res
+
+
+def cpu_baseline(steps: int = 3):
+    """Reference CPU implementation (oracle/tp_oracle.c, all host threads)
+    on a bounded cfg2 sample: 512 of the 4096 columns (2,097,152 elements)."""
+    from oracle import oracle
+    from paper_1810_08723_b200 import abi
+    L = oracle.lib()
+    cols = 512
+    x16 = np.asfortranarray(np.random.default_rng(3).integers(-1000, 1000, (N, N),
+                                                              endpoint=True).astype(np.int16))
+    r = np.asfortranarray(np.random.default_rng(4).standard_normal((1, N)).astype(np.float32))
+    out = np.zeros((N, cols), dtype=np.float32, order="F")
+    # V = reversed transpose of x16: element (i, j) at x16[j, N-1-i]
+    plan = abi.make_plan([N, cols], [[4, 4 * N], [-2 * N, 2], [0, 4]])
+    d = abi.make_operand(out.ctypes.data, 0, 10, False)
+    a = abi.make_operand(x16.ctypes.data, (N - 1) * 2 * N, 3, False)
+    b = abi.make_operand(r.ctypes.data, 0, 10, False)
+    st = C.c_uint32(0)
+    times = []
+    for _ in range(steps + 1):
+        t0 = time.perf_counter()
+        L.tpo_binary(0, C.byref(plan), C.byref(d), C.byref(a), C.byref(b), 10, 0, C.byref(st))
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times[1:])
+    elems = N * cols
+    want = (x16.T[::-1, :cols].astype(np.float64) + r[:, :cols].astype(np.float64)).astype(np.float32)
+    assert np.array_equal(out, want)
+    return {"value": round(elems * 6 / t / 1e9, 3), "unit": "GB/s", "cores": oracle.threads(),
+            "kind": "port", "sample": f"cfg2 columns 0..{cols - 1} ({elems} elements), "
+            "oracle/tp_oracle.c tpo_binary with fused int16->f32 load, OpenMP"}, t
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extras", action="store_true")
+    args = ap.parse_args()
+    dist = Dist()
+    hbm_peak, tc_peak, peak_kind = peaks()
+    config = {"workload": "cfg2: int16[4096,4096] transposed reversed view (strides -8192,2) "
+                          "+ float32[1,4096] broadcast -> float32 add",
+              "elements": N * N, "algorithmic_bytes_per_step": CFG2_BYTES,
+              "l2": "flushed between timed steps (256 MiB memset)", "parallelism": f"dp{dist.world}"}
+
+    if args.impl == "reference":
+        if dist.rank != 0:
+            dist.close()
+            return
+        base, t = cpu_baseline(max(args.steps // 10, 3))
+        line = {"metric": METRIC, "value": base["value"], "unit": "GB/s", "n_gpus": args.gpus,
+                "steps": max(args.steps // 10, 3), "warmup": 1, "ms_per_step": round(t * 1e3, 3),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": config, "impl": "reference", "cpu_baseline": base,
+                "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        dist.close()
+        return
+
+    import paper_1810_08723_b200 as tp
+    from paper_1810_08723_b200 import _native
+    L = _native.lib()
+    devs = tp.list_devices()
+    if not devs:
+        raise SystemExit("no CUDA device visible")
+    dev = devs[dist.local % len(devs)]
+    clocks = Clocks(dev.index)
+    clocks.start()
+    dist.barrier()
+    ms, e2e_ms, e2e_wall, h2d, d2h = bench_cfg2(tp, dev, args.steps, args.warmup, L)
+    dist.barrier()
+    total = dist.max(sum(ms))
+    e2e_total = dist.max(sum(e2e_ms))
+    per_step = total / args.steps
+    value = dist.world * CFG2_BYTES / (per_step / 1e3) / 1e9
+    achieved = CFG2_BYTES / (statistics.mean(ms) / 1e3) / 1e9
+    e2e_val = dist.world * CFG2_BYTES / (e2e_total / len(e2e_ms) / 1e3) / 1e9
+    work = {}
+    if dist.rank == 0 and dist.world == 1 and not args.no_extras:
+        work = extras(tp, dev, L)
+    clk = clocks.stop()
+    if dist.rank == 0:
+        traffic = None
+        tf = ROOT / "profiles" / "ncu_traffic.json"
+        if tf.exists():
+            traffic = json.loads(tf.read_text()).get("cfg2_add_kernel_bytes")
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": dist.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(per_step, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded numpy)", "config": config,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
+                         "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                         "peak_kind": peak_kind, "traffic": traffic,
+                         "kernel": "tpg::k_tile<Ew<OC_BINARY,add,f32<-i16,f32>> (fused)"},
+            "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_total / len(e2e_ms), 3),
+                    "wall_ms_per_step": round(e2e_wall, 3)},
+            "gpu_launches": args.steps + 1 + len(e2e_ms),
+            "clocks": clk,
+        }
+        if dist.world == 1:
+            try:
+                base, _ = cpu_baseline()
+                line["cpu_baseline"] = base
+            except Exception as exc:  # pragma: no cover
+                line["cpu_baseline"] = {"error": repr(exc)}
+        if work:
+            line["workloads"] = work
+        print(json.dumps(line), flush=True)
+    dist.close()
+
+
+if __name__ == "__main__":
+    main()

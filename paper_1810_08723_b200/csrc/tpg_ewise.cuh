@@ -1,0 +1,596 @@
+// tpg_ewise.cuh — the strided elementwise / copy-cast engine (shared by the
+// tpg_ewise_*.cu translation units).
+//
+// Replaces the reference loops kernels.binary_elementwise (kernels.py:213-248),
+// kernels.unary_elementwise (275-302, also the `copy` entry via ops.py:681),
+// kernels.fill (343-352), kernels.arange_fill (377-381),
+// kernels.byteswap_inplace (355-357) and kernels.gather (360-363).  The plan
+// is the reference IterPlan after canonicalize (tensors.py:570-604): axis 0
+// is the destination's fastest axis.
+//
+// Traversals (picked per call on the host, see choose_traversal):
+//   contig  1-D plans whose views are unit-stride (or broadcast): each
+//           thread moves 8 elements per operand with 128-bit loads/stores;
+//           compile-time-typed fast set (Tier A) only.
+//   tile    an input whose fastest axis is not the destination's (a
+//           transposed / reversed view, SURVEY cfg2) is staged through a
+//           64x64 shared-memory tile so both its loads and the destination
+//           stores are coalesced.
+//   rows    axis 0 inner, remaining axes decomposed once per block-row.
+//   flat    per-element index decomposition (short axis 0).
+// Element semantics (decode, compute, cast-on-store) are in tpg_common.cuh.
+// Tier A kernels fix op and dtypes at compile time (inlined, small); Tier B
+// (dtype -1) calls one out-of-line element function that switches on the
+// runtime dtypes (warp-uniform), covering all 15x15 pairs, both byte orders
+// and every op with one kernel per (op class, compute kind, traversal).
+#pragma once
+#include <cuda_runtime.h>
+#include <thrust/complex.h>
+
+#include <algorithm>
+
+#include "tpg_common.cuh"
+#include "tpg_internal.h"
+
+namespace tpg {
+
+enum OpClass { OC_BINARY = 0, OC_UNARY = 1, OC_COPY = 2, OC_FILL = 3, OC_ARANGE = 4,
+               OC_BSWAP = 5, OC_RAW = 6 };
+
+struct EwParams {
+  int ndim;
+  int nin;
+  int64_t ext[TPG_MAX_DIMS];
+  int64_t str[3][TPG_MAX_DIMS];
+  char* base[3];
+  R16 imm[3];
+  int dt[3];
+  int swap[3];
+  int aligned[3];
+  int isimm[3];
+  int op;
+  int track;
+  int dry;
+  int force_complex;
+  uint32_t* flags;
+};
+
+// the per-element descriptor handed (by value) to the out-of-line op
+struct EwDesc {
+  int dtd, dta, dtb;
+  int sd, sa, sb;
+  int op, track, fc;
+};
+
+// ------------------------------------------------------------ unary math
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
+
+// UNARY_TABLE real branch + unary_scalar_fn domain flag (kernels.py:121-158)
+__device__ __forceinline__ double un_flt(int op, double v, uint32_t& st) {
+  switch (op) {
+    case TPG_NEGATE: return -v;
+    case TPG_ABSOLUTE: return fabs(v);
+    case TPG_SQRT:
+      if (v < 0.0) { st |= TPG_FLAG_DOMAIN; return qnan(); }
+      return isnan(v) ? qnan() : sqrt(v);
+    case TPG_EXP: return isnan(v) ? qnan() : exp(v);
+    case TPG_LOG:
+      if (v < 0.0) { st |= TPG_FLAG_DOMAIN; return qnan(); }
+      if (isnan(v)) return qnan();
+      if (v == 0.0) return -INFINITY;
+      return log(v);
+    case TPG_SIN: return isnan(v) ? qnan() : sin(v);
+    case TPG_COS: return isnan(v) ? qnan() : cos(v);
+    case TPG_ASIN:
+      if (fabs(v) > 1.0) { st |= TPG_FLAG_DOMAIN; return qnan(); }
+      return isnan(v) ? qnan() : asin(v);
+    case TPG_ACOS:
+      if (fabs(v) > 1.0) { st |= TPG_FLAG_DOMAIN; return qnan(); }
+      return isnan(v) ? qnan() : acos(v);
+    default: return v;  // conjugate / identity
+  }
+}
+
+__device__ __forceinline__ int64_t un_int(int op, int64_t v, bool uns) {
+  switch (op) {
+    case TPG_NEGATE: return (int64_t)(0ull - (uint64_t)v);
+    case TPG_ABSOLUTE: return (!uns && v < 0) ? (int64_t)(0ull - (uint64_t)v) : v;
+    default: return v;
+  }
+}
+
+// complex branch (cmath); results are tolerance-level vs CPython's cmath
+static __device__ __noinline__ double2 un_cpx(int op, double2 z) {
+  typedef thrust::complex<double> C;
+  C c(z.x, z.y), r;
+  switch (op) {
+    case TPG_NEGATE: return make_double2(-z.x, -z.y);
+    case TPG_ABSOLUTE: return make_double2(hypot(z.x, z.y), 0.0);
+    case TPG_SQRT: r = thrust::sqrt(c); break;
+    case TPG_EXP: r = thrust::exp(c); break;
+    case TPG_LOG:
+      if (z.x == 0.0 && z.y == 0.0) return make_double2(-INFINITY, 0.0);
+      r = thrust::log(c);
+      break;
+    case TPG_SIN: r = thrust::sin(c); break;
+    case TPG_COS: r = thrust::cos(c); break;
+    case TPG_ASIN: r = thrust::asin(c); break;
+    case TPG_ACOS: r = thrust::acos(c); break;
+    case TPG_CONJ: return make_double2(z.x, -z.y);
+    default: return z;
+  }
+  return make_double2(r.real(), r.imag());
+}
+
+// ------------------------------------------------------------ element op
+template <int OC, int KIND>
+__device__ __forceinline__ R16 ew_body(const EwDesc& e, R16 ra, R16 rb, int64_t lin, uint32_t& st) {
+  const int d_t = e.dtd, a_t = e.dta, b_t = e.dtb, op = e.op;
+  uint32_t* fl = e.track ? &st : nullptr;
+  R16 out{0, 0};
+  if (OC == OC_RAW) return ra;
+  if (OC == OC_BSWAP) return swap_raw(d_t, ra);
+  if (OC == OC_ARANGE) {
+    out = enc_from_int(d_t, lin, false, fl);
+  } else if (OC == OC_BINARY) {
+    if (e.sa) ra = swap_raw(a_t, ra);
+    if (e.sb) rb = swap_raw(b_t, rb);
+    if (KIND == K_INT) {
+      out = enc_from_int(d_t, bin_int(op, dec_int(a_t, ra), dec_int(b_t, rb), &st), false, fl);
+    } else if (KIND == K_UINT) {
+      out = enc_from_int(
+          d_t, (int64_t)bin_uint(op, (uint64_t)dec_int(a_t, ra), (uint64_t)dec_int(b_t, rb), &st),
+          true, fl);
+    } else if (KIND == K_FLT) {
+      out = enc_from_flt(d_t, bin_flt(op, dec_flt(a_t, ra), dec_flt(b_t, rb)), fl);
+    } else {
+      double2 r = bin_cpx(op, dec_cpx(a_t, ra), dec_cpx(b_t, rb));
+      out = enc_from_cpx(d_t, r.x, r.y, fl);
+    }
+  } else if (OC == OC_UNARY) {
+    if (e.sa) ra = swap_raw(a_t, ra);
+    if (KIND == K_CPX || (KIND == K_FLT && e.fc)) {
+      double2 r = un_cpx(op, dec_cpx(a_t, ra));
+      out = (op == TPG_ABSOLUTE) ? enc_from_flt(d_t, r.x, fl) : enc_from_cpx(d_t, r.x, r.y, fl);
+    } else if (KIND == K_FLT) {
+      out = enc_from_flt(d_t, un_flt(op, dec_flt(a_t, ra), st), fl);
+    } else {
+      out = enc_from_int(d_t, un_int(op, dec_int(a_t, ra), KIND == K_UINT), KIND == K_UINT, fl);
+    }
+  } else {  // OC_COPY: value copy with cast-on-store (ops._run_copy)
+    if (e.sa) ra = swap_raw(a_t, ra);
+    if (a_t == d_t && a_t != TPG_BOOL) {
+      out = ra;  // same dtype: the value round-trips exactly
+    } else if (KIND == K_CPX) {
+      double2 v = dec_cpx(a_t, ra);
+      out = enc_from_cpx(d_t, v.x, v.y, fl);
+    } else if (KIND == K_FLT) {
+      out = enc_from_flt(d_t, dec_flt(a_t, ra), fl);
+    } else {
+      out = enc_from_int(d_t, dec_int(a_t, ra), KIND == K_UINT, fl);
+    }
+  }
+  if (e.sd) out = swap_raw(d_t, out);
+  return out;
+}
+
+// Tier B: one out-of-line copy of the body per (op class, kind)
+struct R16S {
+  R16 r;
+  uint32_t st;
+};
+template <int OC, int KIND>
+__device__ __noinline__ R16S ew_body_gen(EwDesc e, R16 ra, R16 rb, int64_t lin) {
+  uint32_t st = 0;
+  R16 r = ew_body<OC, KIND>(e, ra, rb, lin, st);
+  return R16S{r, st};
+}
+
+template <int OC, int NIN, int OP, int KIND, int DTD, int DTA, int DTB>
+struct Ew {
+  static constexpr bool typed = DTD >= 0 && (DTA >= 0 || NIN < 1) && (DTB >= 0 || NIN < 2);
+  static __device__ __forceinline__ int dtd(const EwParams& p) { return DTD >= 0 ? DTD : p.dt[0]; }
+  static __device__ __forceinline__ int dta(const EwParams& p) { return DTA >= 0 ? DTA : p.dt[1]; }
+  static __device__ __forceinline__ int dtb(const EwParams& p) { return DTB >= 0 ? DTB : p.dt[2]; }
+
+  static __device__ __forceinline__ R16 apply(const EwParams& p, R16 ra, R16 rb, int64_t lin,
+                                              uint32_t& st) {
+    if (OC == OC_FILL) return p.imm[1];
+    EwDesc e;
+    e.dtd = dtd(p); e.dta = dta(p); e.dtb = dtb(p);
+    e.sd = p.swap[0]; e.sa = p.swap[1]; e.sb = p.swap[2];
+    e.op = OP >= 0 ? OP : p.op;
+    e.track = p.track;
+    e.fc = p.force_complex;
+    if (typed || OC == OC_RAW || OC == OC_BSWAP || OC == OC_ARANGE)
+      return ew_body<OC, KIND>(e, ra, rb, lin, st);
+    R16S x = ew_body_gen<OC, KIND>(e, ra, rb, lin);
+    st |= x.st;
+    return x.r;
+  }
+};
+
+// load operand V (1 or 2) at byte offset off
+template <class F, int V>
+__device__ __forceinline__ R16 ld_op(const EwParams& p, int64_t off) {
+  if (p.isimm[V]) return p.imm[V];
+  const int dt = V == 1 ? F::dta(p) : F::dtb(p);
+  return load_raw(dt, p.base[V] + off, p.aligned[V]);
+}
+
+// ------------------------------------------------------------ traversals
+// rows: axis 0 inner.  Work item = (tile of axis 0, row over axes 1..).
+template <class F, int NIN, int U>
+__global__ void __launch_bounds__(256) k_rows(EwParams p, int64_t rows, int64_t ntile) {
+  const int64_t e0 = p.ext[0];
+  uint32_t st = 0;
+  const int dtd = F::dtd(p);
+  for (int64_t w = blockIdx.x; w < rows * ntile; w += gridDim.x) {
+    const int64_t row = w / ntile, tile = w - row * ntile;
+    int64_t od = 0, oa = 0, ob = 0, r = row;
+    for (int k = 1; k < p.ndim; ++k) {
+      const int64_t e = p.ext[k];
+      const int64_t c = r % e;
+      r /= e;
+      od += c * p.str[0][k];
+      if (NIN >= 1) oa += c * p.str[1][k];
+      if (NIN >= 2) ob += c * p.str[2][k];
+    }
+    const int64_t i_base = tile * (256 * U) + threadIdx.x;
+    R16 ra[U], rb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i0 = i_base + u * 256;
+      ra[u] = rb[u] = R16{0, 0};
+      if (i0 < e0) {
+        if (NIN >= 1) ra[u] = ld_op<F, 1>(p, oa + i0 * p.str[1][0]);
+        if (NIN >= 2) rb[u] = ld_op<F, 2>(p, ob + i0 * p.str[2][0]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i0 = i_base + u * 256;
+      if (i0 < e0) {
+        R16 o = F::apply(p, ra[u], rb[u], row * e0 + i0, st);
+        if (!p.dry) store_raw(dtd, p.base[0] + od + i0 * p.str[0][0], o, p.aligned[0]);
+      }
+    }
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+// flat: full index decomposition per element
+template <class F, int NIN>
+__global__ void __launch_bounds__(256) k_flat(EwParams p, int64_t total) {
+  uint32_t st = 0;
+  const int dtd = F::dtd(p);
+  const int64_t nthreads = (int64_t)gridDim.x * 256;
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < total; i += nthreads) {
+    int64_t r = i, d = 0, a = 0, b = 0;
+    for (int k = 0; k < p.ndim; ++k) {
+      const int64_t e = p.ext[k];
+      const int64_t c = r % e;
+      r /= e;
+      d += c * p.str[0][k];
+      if (NIN >= 1) a += c * p.str[1][k];
+      if (NIN >= 2) b += c * p.str[2][k];
+    }
+    R16 ra{0, 0}, rb{0, 0};
+    if (NIN >= 1) ra = ld_op<F, 1>(p, a);
+    if (NIN >= 2) rb = ld_op<F, 2>(p, b);
+    R16 o = F::apply(p, ra, rb, i, st);
+    if (!p.dry) store_raw(dtd, p.base[0] + d, o, p.aligned[0]);
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+// tile: operand X (1 or 2) is coalesced along axis q != 0; stage 64x64
+// tiles of it in shared memory, then sweep the tile along axis 0 so the
+// destination (and any axis-0-coalesced operand) is written coalesced.
+constexpr int TT = 64;
+
+template <class F, int NIN, int X>
+__global__ void __launch_bounds__(256) k_tile(EwParams p, int q, int64_t nt0, int64_t ntq,
+                                              int64_t nrest) {
+  __shared__ uint64_t tile[TT][TT + 1];
+  const int64_t e0 = p.ext[0], eq = p.ext[q];
+  const int dtd = F::dtd(p);
+  const int dtx = X == 1 ? F::dta(p) : F::dtb(p);
+  uint32_t st = 0;
+  const int64_t nwork = nt0 * ntq * nrest;
+  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int64_t t0 = w % nt0;
+    const int64_t tq = (w / nt0) % ntq;
+    int64_t rr = w / (nt0 * ntq);
+    int64_t off[3] = {0, 0, 0};
+    for (int k = 1; k < p.ndim; ++k) {
+      if (k == q) continue;
+      const int64_t e = p.ext[k];
+      const int64_t c = rr % e;
+      rr /= e;
+#pragma unroll
+      for (int v = 0; v < 3; ++v) off[v] += c * p.str[v][k];
+    }
+    // phase 1: coalesced along q
+    {
+      constexpr int U = 4;
+      for (int idx0 = threadIdx.x; idx0 < TT * TT; idx0 += 256 * U) {
+        uint64_t v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = idx0 + u * 256;
+          const int iq = idx % TT, i0 = idx / TT;
+          const int64_t g0 = t0 * TT + i0, gq = tq * TT + iq;
+          v[u] = 0;
+          if (g0 < e0 && gq < eq)
+            v[u] = load_raw(dtx, p.base[X] + off[X] + g0 * p.str[X][0] + gq * p.str[X][q],
+                            p.aligned[X]).lo;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = idx0 + u * 256;
+          tile[idx / TT][idx % TT] = v[u];
+        }
+      }
+    }
+    __syncthreads();
+    // phase 2: coalesced along axis 0
+    {
+      constexpr int U = 4;
+      constexpr int Y = 3 - X;
+      for (int idx0 = threadIdx.x; idx0 < TT * TT; idx0 += 256 * U) {
+        R16 ry[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = idx0 + u * 256;
+          const int i0 = idx % TT, iq = idx / TT;
+          const int64_t g0 = t0 * TT + i0, gq = tq * TT + iq;
+          ry[u] = R16{0, 0};
+          if (NIN >= 2 && g0 < e0 && gq < eq)
+            ry[u] = ld_op<F, Y>(p, off[Y] + g0 * p.str[Y][0] + gq * p.str[Y][q]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = idx0 + u * 256;
+          const int i0 = idx % TT, iq = idx / TT;
+          const int64_t g0 = t0 * TT + i0, gq = tq * TT + iq;
+          if (g0 < e0 && gq < eq) {
+            const R16 rx{tile[i0][iq], 0};
+            R16 o = (X == 1) ? F::apply(p, rx, ry[u], 0, st) : F::apply(p, ry[u], rx, 0, st);
+            if (!p.dry)
+              store_raw(dtd, p.base[0] + off[0] + g0 * p.str[0][0] + gq * p.str[0][q], o,
+                        p.aligned[0]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+// contig: 1-D unit-stride views, compile-time element sizes; 8 elements per
+// thread per operand moved with the widest aligned vector accesses.
+constexpr int CV = 8;
+
+template <int S>
+__device__ __forceinline__ void load_vec(const char* ptr, R16 (&o)[CV]) {
+  constexpr int B = S * CV;
+  if constexpr (B >= 16) {
+    uint32_t w[B / 4];
+#pragma unroll
+    for (int i = 0; i < B / 16; ++i) {
+      uint4 v = __ldcs((const uint4*)ptr + i);  // streaming: read once
+      w[4 * i] = v.x; w[4 * i + 1] = v.y; w[4 * i + 2] = v.z; w[4 * i + 3] = v.w;
+    }
+#pragma unroll
+    for (int j = 0; j < CV; ++j) {
+      if constexpr (S == 16) {
+        o[j].lo = w[4 * j] | ((uint64_t)w[4 * j + 1] << 32);
+        o[j].hi = w[4 * j + 2] | ((uint64_t)w[4 * j + 3] << 32);
+      } else if constexpr (S == 8) {
+        o[j].lo = w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
+        o[j].hi = 0;
+      } else if constexpr (S == 4) {
+        o[j].lo = w[j];
+        o[j].hi = 0;
+      } else {  // S == 2
+        o[j].lo = (w[j / 2] >> (16 * (j % 2))) & 0xffffu;
+        o[j].hi = 0;
+      }
+    }
+  } else {  // S == 1: 8 bytes
+    uint2 v = __ldcs((const uint2*)ptr);
+#pragma unroll
+    for (int j = 0; j < CV; ++j) {
+      o[j].lo = ((j < 4 ? v.x : v.y) >> (8 * (j % 4))) & 0xffu;
+      o[j].hi = 0;
+    }
+  }
+}
+
+template <int S>
+__device__ __forceinline__ void store_vec(char* ptr, const R16 (&o)[CV]) {
+  constexpr int B = S * CV;
+  if constexpr (B >= 16) {
+    uint32_t w[B / 4];
+#pragma unroll
+    for (int j = 0; j < CV; ++j) {
+      if constexpr (S == 16) {
+        w[4 * j] = (uint32_t)o[j].lo; w[4 * j + 1] = (uint32_t)(o[j].lo >> 32);
+        w[4 * j + 2] = (uint32_t)o[j].hi; w[4 * j + 3] = (uint32_t)(o[j].hi >> 32);
+      } else if constexpr (S == 8) {
+        w[2 * j] = (uint32_t)o[j].lo; w[2 * j + 1] = (uint32_t)(o[j].lo >> 32);
+      } else if constexpr (S == 4) {
+        w[j] = (uint32_t)o[j].lo;
+      } else {  // S == 2
+        if (j % 2 == 0) w[j / 2] = (uint32_t)o[j].lo & 0xffffu;
+        else w[j / 2] |= ((uint32_t)o[j].lo & 0xffffu) << 16;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < B / 16; ++i)
+      __stcs((uint4*)ptr + i, make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]));
+  } else {
+    uint32_t x = 0, y = 0;
+#pragma unroll
+    for (int j = 0; j < CV; ++j) {
+      uint32_t b = (uint32_t)o[j].lo & 0xffu;
+      if (j < 4) x |= b << (8 * j); else y |= b << (8 * (j - 4));
+    }
+    __stcs((uint2*)ptr, make_uint2(x, y));
+  }
+}
+
+template <class F, int NIN, int SD, int SA, int SB>
+__global__ void __launch_bounds__(256) k_contig(EwParams p, int64_t n) {
+  uint32_t st = 0;
+  const int64_t nchunk = n / CV;
+  const int64_t tid = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * 256;
+  const bool bca = NIN >= 1 && (p.isimm[1] || p.str[1][0] == 0);
+  const bool bcb = NIN >= 2 && (p.isimm[2] || p.str[2][0] == 0);
+  R16 sa{0, 0}, sb{0, 0};
+  if (NIN >= 1 && bca) sa = ld_op<F, 1>(p, 0);
+  if (NIN >= 2 && bcb) sb = ld_op<F, 2>(p, 0);
+  for (int64_t c = tid; c < nchunk; c += nthreads) {
+    R16 a[CV], b[CV], o[CV];
+    if (NIN >= 1) {
+      if (bca) {
+#pragma unroll
+        for (int j = 0; j < CV; ++j) a[j] = sa;
+      } else {
+        load_vec<SA>(p.base[1] + c * (CV * SA), a);
+      }
+    }
+    if (NIN >= 2) {
+      if (bcb) {
+#pragma unroll
+        for (int j = 0; j < CV; ++j) b[j] = sb;
+      } else {
+        load_vec<SB>(p.base[2] + c * (CV * SB), b);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CV; ++j)
+      o[j] = F::apply(p, NIN >= 1 ? a[j] : sa, NIN >= 2 ? b[j] : sb, c * CV + j, st);
+    if (!p.dry) store_vec<SD>(p.base[0] + c * (CV * SD), o);
+  }
+  // tail
+  for (int64_t i = nchunk * CV + tid; i < n; i += nthreads) {
+    R16 a{0, 0}, b{0, 0};
+    if (NIN >= 1) a = bca ? sa : load_raw(F::dta(p), p.base[1] + i * SA, true);
+    if (NIN >= 2) b = bcb ? sb : load_raw(F::dtb(p), p.base[2] + i * SB, true);
+    R16 o = F::apply(p, a, b, i, st);
+    if (!p.dry) store_raw(F::dtd(p), p.base[0] + i * SD, o, true);
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+// ------------------------------------------------------------ host side
+struct Choice {
+  int kind;  // 0 contig, 1 tile, 2 rows, 3 flat
+  int x, q;
+};
+
+inline int64_t plan_total(const EwParams& p) {
+  int64_t t = 1;
+  for (int k = 0; k < p.ndim; ++k) t *= p.ext[k];
+  return t;
+}
+
+inline Choice choose_traversal(const EwParams& p, bool typed, int oc) {
+  const int nin = p.nin;
+  if (typed && p.ndim == 1) {
+    bool ok = true;
+    for (int v = 0; v <= nin; ++v) {
+      if (v > 0 && (p.isimm[v] || p.str[v][0] == 0)) continue;
+      const int s = dt_size(p.dt[v]);
+      const int al = std::min(16, s * CV);
+      if (p.str[v][0] != s || ((uintptr_t)p.base[v] % al) != 0) ok = false;
+    }
+    if (ok) return Choice{0, 0, 0};
+  }
+  if (oc == OC_BINARY || oc == OC_UNARY || oc == OC_COPY || oc == OC_RAW) {
+    for (int x = 1; x <= nin; ++x) {
+      if (p.isimm[x]) continue;
+      const int s = dt_size(p.dt[x]);
+      if (s > 8) continue;
+      const int64_t s0 = p.str[x][0] < 0 ? -p.str[x][0] : p.str[x][0];
+      if (s0 <= 2 * s || p.ext[0] < 16) continue;
+      int best = -1;
+      int64_t bs = 0;
+      for (int k = 1; k < p.ndim; ++k) {
+        if (p.ext[k] < 16) continue;
+        const int64_t sk = p.str[x][k] < 0 ? -p.str[x][k] : p.str[x][k];
+        if (sk == 0) continue;
+        if (best < 0 || sk < bs) { best = k; bs = sk; }
+      }
+      if (best > 0 && bs <= 2 * s && bs < s0) return Choice{1, x, best};
+    }
+  }
+  if (p.ext[0] >= 128 || p.ndim <= 1) return Choice{2, 0, 0};
+  return Choice{3, 0, 0};
+}
+
+inline int grid_for(int64_t work, int dev, int per_sm) {
+  int64_t cap = (int64_t)sm_count(dev) * per_sm;
+  int64_t g = work < cap ? work : cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// Launch one (op class, op, kind, dtypes) configuration.  Typed (Tier A)
+// instantiations compile contig/tile/rows; the flat traversal (short axis
+// 0, rare) always goes through the Tier B kernel of the same class/kind.
+template <int OC, int NIN, int OP, int KIND, int DTD, int DTA, int DTB>
+int launch_ew(EwParams& p, Stream* st) {
+  typedef Ew<OC, NIN, OP, KIND, DTD, DTA, DTB> F;
+  constexpr bool typed = F::typed;
+  const int64_t total = plan_total(p);
+  if (total == 0) return TPG_OK;
+  Choice c = choose_traversal(p, typed, OC);
+  const int dev = st->device;
+  if (c.kind == 0) {
+    if constexpr (typed) {
+      constexpr int SD = dt_size(DTD);
+      constexpr int SA = DTA >= 0 ? dt_size(DTA) : 1;
+      constexpr int SB = DTB >= 0 ? dt_size(DTB) : 1;
+      const int64_t n = p.ext[0];
+      const int g = grid_for((n / CV + 255) / 256, dev, 16);
+      k_contig<F, NIN, SD, SA, SB><<<g, 256, 0, st->s>>>(p, n);
+    }
+  } else if (c.kind == 1) {
+    if constexpr (NIN >= 1) {
+      const int64_t nt0 = (p.ext[0] + TT - 1) / TT, ntq = (p.ext[c.q] + TT - 1) / TT;
+      const int64_t nrest = total / (p.ext[0] * p.ext[c.q]);
+      const int g = grid_for(nt0 * ntq * nrest, dev, 8);
+      if (c.x == 1) {
+        k_tile<F, NIN, 1><<<g, 256, 0, st->s>>>(p, c.q, nt0, ntq, nrest);
+      } else {
+        if constexpr (NIN >= 2) k_tile<F, NIN, 2><<<g, 256, 0, st->s>>>(p, c.q, nt0, ntq, nrest);
+      }
+    }
+  } else if (c.kind == 2) {
+    constexpr int U = 4;
+    const int64_t rows = total / p.ext[0];
+    const int64_t ntile = (p.ext[0] + 256 * U - 1) / (256 * U);
+    const int g = grid_for(rows * ntile, dev, 16);
+    k_rows<F, NIN, U><<<g, 256, 0, st->s>>>(p, rows, ntile);
+  } else {
+    typedef Ew<OC, NIN, -1, KIND, -1, -1, -1> G;
+    if (OP >= 0) p.op = OP;  // generic kernels read op from params
+    const int g = grid_for((total + 255) / 256, dev, 16);
+    k_flat<G, NIN><<<g, 256, 0, st->s>>>(p, total);
+  }
+  TPG_LAUNCH_CHECK("elementwise launch");
+  return TPG_OK;
+}
+
+// entry points implemented in the tpg_ewise_*.cu units
+int ew_dispatch_fast(int oc, int op, int kind, EwParams& p, Stream* st, bool* done);
+int ew_dispatch_generic_binary(int kind, EwParams& p, Stream* st);
+int ew_dispatch_generic_unary(int kind, EwParams& p, Stream* st);
+int ew_dispatch_generic_copy(int kind, EwParams& p, Stream* st);
+int ew_dispatch_misc(int oc, EwParams& p, Stream* st);
+
+}  // namespace tpg

@@ -1,0 +1,39 @@
+// tpg_internal.h — shared host-side plumbing for the C ABI implementation.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/tidepool_gpu.h"
+
+namespace tpg {
+
+struct Stream {
+  int device;
+  cudaStream_t s;
+};
+
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+int arg_fail(const std::string& msg);
+
+// Resolve a tpg_stream (NULL = default stream of the current device) and
+// make its device current.
+Stream* resolve_stream(tpg_stream s);
+int sm_count(int device);
+uint32_t* device_flags(int device);  // device-resident sticky status word
+
+#define TPG_CUDA_CHECK(expr)                                 \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) return ::tpg::cuda_fail(_e, #expr); \
+  } while (0)
+
+#define TPG_LAUNCH_CHECK(what)                                 \
+  do {                                                         \
+    cudaError_t _e = cudaGetLastError();                       \
+    if (_e != cudaSuccess) return ::tpg::cuda_fail(_e, what);  \
+  } while (0)
+
+}  // namespace tpg

@@ -1,0 +1,355 @@
+// tpg_runtime.cu — devices, stream-ordered caching allocator, streams,
+// events, transfers and the sticky status word.
+//
+// Reference counterparts: devices.Device / Stream (pkg/src/tidepool/
+// devices.py:47-192), storage_alloc (storage.py:91-97) and the sticky
+// status set ops._status (ops.py:27-38).  The reference frees buffers when
+// the Python object dies (storage.py:59-67); on the GPU a free must not
+// overtake in-flight kernels, so frees are stream-ordered (cudaFreeAsync
+// into the device's memory pool, whose release threshold keeps freed
+// blocks cached for reuse: a caching allocator with stream semantics).
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "tpg_internal.h"
+
+namespace tpg {
+
+static thread_local std::string g_err;
+static std::mutex g_mu;
+static bool g_inited = false;
+static int g_ndev = 0;
+static std::vector<Stream*> g_default;
+static std::vector<int> g_sms;
+static std::vector<uint32_t*> g_flags;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? TPG_E_ALLOC : TPG_E_CUDA;
+}
+
+int arg_fail(const std::string& msg) {
+  set_error(msg);
+  return TPG_E_ARG;
+}
+
+static int init_locked() {
+  if (g_inited) return TPG_OK;
+  cudaError_t e = cudaGetDeviceCount(&g_ndev);
+  if (e != cudaSuccess) {
+    g_ndev = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  g_default.assign(g_ndev, nullptr);
+  g_sms.assign(g_ndev, 0);
+  g_flags.assign(g_ndev, nullptr);
+  for (int d = 0; d < g_ndev; ++d) {
+    TPG_CUDA_CHECK(cudaSetDevice(d));
+    cudaDeviceProp prop;
+    TPG_CUDA_CHECK(cudaGetDeviceProperties(&prop, d));
+    g_sms[d] = prop.multiProcessorCount;
+    Stream* st = new Stream{d, nullptr};
+    TPG_CUDA_CHECK(cudaStreamCreateWithFlags(&st->s, cudaStreamNonBlocking));
+    g_default[d] = st;
+    // keep freed blocks cached in the pool (no release back to the OS)
+    cudaMemPool_t pool;
+    TPG_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, d));
+    uint64_t thresh = UINT64_MAX;
+    TPG_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    uint32_t* f = nullptr;
+    TPG_CUDA_CHECK(cudaMalloc(&f, 64));
+    TPG_CUDA_CHECK(cudaMemset(f, 0, 64));
+    g_flags[d] = f;
+  }
+  if (g_ndev > 0) TPG_CUDA_CHECK(cudaSetDevice(0));
+  g_inited = true;
+  return TPG_OK;
+}
+
+Stream* resolve_stream(tpg_stream s) {
+  Stream* st = (Stream*)s;
+  if (st == nullptr) {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d < 0 || d >= (int)g_default.size()) return nullptr;
+    st = g_default[d];
+  }
+  cudaSetDevice(st->device);
+  return st;
+}
+
+int sm_count(int device) {
+  if (device < 0 || device >= (int)g_sms.size()) return 148;
+  return g_sms[device];
+}
+
+uint32_t* device_flags(int device) {
+  if (device < 0 || device >= (int)g_flags.size()) return nullptr;
+  return g_flags[device];
+}
+
+}  // namespace tpg
+
+using namespace tpg;
+
+extern "C" {
+
+const char* tpg_last_error(void) { return g_err.c_str(); }
+
+const char* tpg_version(void) { return "tidepool_gpu 0.1 (sm_100a)"; }
+
+int tpg_init(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return init_locked();
+}
+
+int tpg_device_count(int* count) {
+  int rc = tpg_init();
+  *count = g_ndev;
+  return rc;
+}
+
+int tpg_device_props_get(int device, tpg_device_props* p) {
+  if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
+  cudaDeviceProp prop;
+  TPG_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+  TPG_CUDA_CHECK(cudaSetDevice(device));
+  size_t fr = 0, tot = 0;
+  TPG_CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
+  p->sm_count = prop.multiProcessorCount;
+  p->cc_major = prop.major;
+  p->cc_minor = prop.minor;
+  p->total_mem = (int64_t)tot;
+  p->free_mem = (int64_t)fr;
+  p->l2_bytes = prop.l2CacheSize;
+  strncpy(p->name, prop.name, sizeof(p->name) - 1);
+  p->name[sizeof(p->name) - 1] = 0;
+  return TPG_OK;
+}
+
+int tpg_malloc(int device, size_t nbytes, void** ptr) {
+  if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
+  TPG_CUDA_CHECK(cudaSetDevice(device));
+  if (nbytes == 0) nbytes = 1;
+  // round to 256 B so vectorized paths see aligned bases
+  nbytes = (nbytes + 255) & ~(size_t)255;
+  cudaError_t e = cudaMallocAsync(ptr, nbytes, g_default[device]->s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  return TPG_OK;
+}
+
+int tpg_free(int device, void* ptr, tpg_stream stream) {
+  if (ptr == nullptr) return TPG_OK;
+  if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
+  TPG_CUDA_CHECK(cudaSetDevice(device));
+  Stream* st = stream ? (Stream*)stream : g_default[device];
+  TPG_CUDA_CHECK(cudaFreeAsync(ptr, st->s));
+  return TPG_OK;
+}
+
+int tpg_host_alloc(size_t nbytes, void** ptr) {
+  TPG_CUDA_CHECK(cudaHostAlloc(ptr, nbytes ? nbytes : 1, cudaHostAllocPortable));
+  return TPG_OK;
+}
+
+int tpg_host_free(void* ptr) {
+  TPG_CUDA_CHECK(cudaFreeHost(ptr));
+  return TPG_OK;
+}
+
+int tpg_mem_stats(int device, int64_t* in_use, int64_t* cached, int64_t* n_alloc) {
+  if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
+  cudaMemPool_t pool;
+  TPG_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t used = 0, reserved = 0;
+  TPG_CUDA_CHECK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  TPG_CUDA_CHECK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+  *in_use = (int64_t)used;
+  *cached = (int64_t)(reserved - used);
+  *n_alloc = 0;
+  return TPG_OK;
+}
+
+int tpg_empty_cache(int device) {
+  if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
+  TPG_CUDA_CHECK(cudaSetDevice(device));
+  TPG_CUDA_CHECK(cudaDeviceSynchronize());
+  cudaMemPool_t pool;
+  TPG_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+  TPG_CUDA_CHECK(cudaMemPoolTrimTo(pool, 0));
+  return TPG_OK;
+}
+
+int tpg_default_stream(int device, tpg_stream* stream) {
+  if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
+  *stream = g_default[device];
+  return TPG_OK;
+}
+
+int tpg_stream_create(int device, tpg_stream* stream) {
+  if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
+  TPG_CUDA_CHECK(cudaSetDevice(device));
+  Stream* st = new Stream{device, nullptr};
+  cudaError_t e = cudaStreamCreateWithFlags(&st->s, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete st;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  *stream = st;
+  return TPG_OK;
+}
+
+int tpg_stream_destroy(tpg_stream stream) {
+  Stream* st = (Stream*)stream;
+  if (!st) return TPG_OK;
+  for (Stream* d : g_default)
+    if (d == st) return arg_fail("cannot destroy a default stream");
+  TPG_CUDA_CHECK(cudaSetDevice(st->device));
+  TPG_CUDA_CHECK(cudaStreamDestroy(st->s));
+  delete st;
+  return TPG_OK;
+}
+
+int tpg_stream_sync(tpg_stream stream) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  TPG_CUDA_CHECK(cudaStreamSynchronize(st->s));
+  return TPG_OK;
+}
+
+int tpg_stream_wait(tpg_stream waiter, tpg_stream signaller) {
+  Stream* w = (Stream*)waiter;
+  Stream* s = (Stream*)signaller;
+  if (!w || !s) return arg_fail("null stream");
+  TPG_CUDA_CHECK(cudaSetDevice(s->device));
+  cudaEvent_t ev;
+  TPG_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  TPG_CUDA_CHECK(cudaEventRecord(ev, s->s));
+  TPG_CUDA_CHECK(cudaSetDevice(w->device));
+  TPG_CUDA_CHECK(cudaStreamWaitEvent(w->s, ev, 0));
+  TPG_CUDA_CHECK(cudaEventDestroy(ev));
+  return TPG_OK;
+}
+
+int tpg_event_create(tpg_event* ev) {
+  cudaEvent_t e;
+  TPG_CUDA_CHECK(cudaEventCreate(&e));
+  *ev = (tpg_event)e;
+  return TPG_OK;
+}
+
+int tpg_event_destroy(tpg_event ev) {
+  TPG_CUDA_CHECK(cudaEventDestroy((cudaEvent_t)ev));
+  return TPG_OK;
+}
+
+int tpg_event_record(tpg_event ev, tpg_stream stream) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  TPG_CUDA_CHECK(cudaEventRecord((cudaEvent_t)ev, st->s));
+  return TPG_OK;
+}
+
+int tpg_event_sync(tpg_event ev) {
+  TPG_CUDA_CHECK(cudaEventSynchronize((cudaEvent_t)ev));
+  return TPG_OK;
+}
+
+int tpg_event_elapsed(tpg_event start, tpg_event stop, float* ms) {
+  TPG_CUDA_CHECK(cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)stop));
+  return TPG_OK;
+}
+
+int tpg_memcpy_h2d(void* dst, const void* src, size_t n, tpg_stream stream) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  if (n == 0) return TPG_OK;
+  TPG_CUDA_CHECK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st->s));
+  return TPG_OK;
+}
+
+int tpg_memcpy_d2h(void* dst, const void* src, size_t n, tpg_stream stream) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  if (n == 0) return TPG_OK;
+  TPG_CUDA_CHECK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st->s));
+  return TPG_OK;
+}
+
+int tpg_memcpy_d2d(void* dst, const void* src, size_t n, tpg_stream stream) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  if (n == 0) return TPG_OK;
+  TPG_CUDA_CHECK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, st->s));
+  return TPG_OK;
+}
+
+int tpg_memset(void* dst, int value, size_t n, tpg_stream stream) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  if (n == 0) return TPG_OK;
+  TPG_CUDA_CHECK(cudaMemsetAsync(dst, value, n, st->s));
+  return TPG_OK;
+}
+
+// ---- launch gate (measurement helper): hold a stream until the host has
+// enqueued a whole batch of timed steps, so host-side enqueue latency never
+// shows up between the CUDA events of a step.
+static volatile uint32_t* g_gate = nullptr;
+static uint32_t* g_gate_dev = nullptr;
+
+__global__ void k_gate(volatile uint32_t* flag) {
+  const long long t0 = clock64();
+  while (*flag == 0) {
+    __nanosleep(2000);
+    if (clock64() - t0 > 40000000000ll) break;  // ~20 s safety valve
+  }
+}
+
+int tpg_gate_arm(tpg_stream stream) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  if (!g_gate) {
+    void* h = nullptr;
+    TPG_CUDA_CHECK(cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    g_gate = (volatile uint32_t*)h;
+    TPG_CUDA_CHECK(cudaHostGetDevicePointer((void**)&g_gate_dev, h, 0));
+  }
+  *g_gate = 0;
+  __sync_synchronize();
+  k_gate<<<1, 1, 0, st->s>>>(g_gate_dev);
+  TPG_LAUNCH_CHECK("gate");
+  return TPG_OK;
+}
+
+int tpg_gate_release(void) {
+  if (g_gate) {
+    __sync_synchronize();
+    *g_gate = 1;
+    __sync_synchronize();
+  }
+  return TPG_OK;
+}
+
+int tpg_flags_get(int device, uint32_t* flags) {
+  if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
+  TPG_CUDA_CHECK(cudaSetDevice(device));
+  TPG_CUDA_CHECK(cudaMemcpy(flags, g_flags[device], sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return TPG_OK;
+}
+
+int tpg_flags_clear(int device) {
+  if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
+  TPG_CUDA_CHECK(cudaSetDevice(device));
+  TPG_CUDA_CHECK(cudaMemset(g_flags[device], 0, sizeof(uint32_t)));
+  return TPG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,578 @@
+"""Storage, strided tensor views and host interop for gpu tensors.
+
+Tensor semantics follow the reference object layer
+(pkg/src/tidepool/tensors.py): a tensor is a storage reference, a byte
+offset, up to 8 extents with signed byte strides, a dtype and a byte-order
+flag; fresh tensors are column-major (first axis fastest, tensors.py:62-68);
+broadcasting aligns leading axes (411-451); self-overlapping views are
+read-only (489-512) and pair_overlap gives the three-valued verdict the
+pipeline uses to clone aliased operands (515-526).  Storage lives in device
+memory; host reads/writes are explicit staged copies.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+
+import numpy as np
+
+from . import _native, abi, devices, dtypes
+from .errors import CastError, DeviceError, ReadOnlyError, ShapeError, StorageError
+from .plan import MAX_DIMS, build_plan, canonicalize
+
+_defaults = threading.local()
+
+
+def set_default_dtype(d):
+    _defaults.dtype = d
+
+
+def set_default_device(dev):
+    _defaults.device = dev
+
+
+def default_dtype():
+    return getattr(_defaults, "dtype", dtypes.DOUBLE)
+
+
+def default_device():
+    return getattr(_defaults, "device", None) or devices.gpu(0)
+
+
+# ---------------------------------------------------------------------------
+class Storage:
+    """Flat device buffer with a display dtype, byte order and owning stream."""
+
+    def __init__(self, device, nbytes: int, dtype=dtypes.UINT8, ptr: int | None = None,
+                 owned: bool = True):
+        self.device = device
+        self.stream = device.default_stream()
+        self.nbytes = int(nbytes)
+        self.ptr = ptr if ptr is not None else device.allocate(self.nbytes)
+        self.dtype = dtype
+        self.byteorder = dtypes.NATIVE_ORDER
+        self.readonly = False
+        self.owned = owned
+
+    def view(self):
+        return self  # table entries receive the buffer handle (.ptr)
+
+    def snapshot(self) -> bytes:
+        out = bytearray(self.nbytes)
+        if self.nbytes:
+            buf = (C.c_char * self.nbytes).from_buffer(out)
+            _native.check(_native.lib().tpg_memcpy_d2h(buf, self.ptr, self.nbytes,
+                                                       self.stream.handle), "d2h")
+        self.stream.sync()
+        return bytes(out)
+
+    def write(self, data, offset: int = 0) -> None:
+        mv = memoryview(data).cast("B")
+        n = mv.nbytes
+        if offset < 0 or offset + n > self.nbytes:
+            raise StorageError("write outside storage")
+        if n:
+            arr = np.frombuffer(mv, dtype=np.uint8)
+            _native.check(_native.lib().tpg_memcpy_h2d(self.ptr + offset, arr.ctypes.data, n,
+                                                       self.stream.handle), "h2d")
+            self.stream.sync()
+
+    def release(self) -> None:
+        if self.owned and self.ptr is not None:
+            self.device.release(self.ptr, self.stream)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+    def __repr__(self):
+        return f"<storage {self.nbytes} bytes on {self.device.name}>"
+
+
+def storage_alloc(device, nbytes: int, dtype=dtypes.UINT8) -> Storage:
+    if nbytes < 0:
+        raise StorageError("storage size must be >= 0")
+    return Storage(device, nbytes, dtype)
+
+
+class Scalar:
+    __slots__ = ("value", "dtype")
+
+    def __init__(self, value, dtype=None):
+        if dtype is None:
+            dtype = dtypes.infer_scalar_dtype(value)
+        self.dtype = dtype
+        self.value = dtypes.cast_scalar(value, dtype)
+
+    def __repr__(self):
+        return f"{self.value!r} ({self.dtype.name})"
+
+
+class OverlapVerdict:
+    DISJOINT = "disjoint"
+    EXACT = "exact_overlap"
+    POSSIBLE = "possible_overlap"
+
+
+def column_major_strides(dims, itemsize):
+    out, step = [], itemsize
+    for e in dims:
+        out.append(step)
+        step *= e
+    return tuple(out)
+
+
+def _check_dims(dims):
+    dims = tuple(int(d) for d in dims)
+    if len(dims) > MAX_DIMS:
+        raise ShapeError(f"{len(dims)} dimensions exceed the limit of {MAX_DIMS}")
+    if any(d < 0 for d in dims):
+        raise ShapeError(f"negative extent in dims {dims}")
+    return dims
+
+
+class Tensor:
+    __slots__ = ("storage", "offset", "dims", "strides", "dtype", "byteorder", "_so")
+
+    def __init__(self, storage, offset, dims, strides, dtype, byteorder=None):
+        dims = _check_dims(dims)
+        strides = tuple(int(s) for s in strides)
+        if len(strides) != len(dims):
+            raise ShapeError("dims and strides must have equal length")
+        self.storage = storage
+        self.offset = int(offset)
+        self.dims = dims
+        self.strides = strides
+        self.dtype = dtype
+        self.byteorder = byteorder or storage.byteorder
+        self._so = None
+        lo, hi = byte_extent(self)
+        if self.nelem and (lo < 0 or hi > storage.nbytes):
+            raise ShapeError(f"view reaches bytes [{lo}, {hi}) outside storage of "
+                             f"{storage.nbytes} bytes")
+
+    @property
+    def ndim(self):
+        return len(self.dims)
+
+    @property
+    def device(self):
+        return self.storage.device
+
+    @property
+    def nelem(self):
+        return math.prod(self.dims)
+
+    @property
+    def readonly(self):
+        return self.storage.readonly or self_overlap(self)
+
+    def item(self):
+        if self.nelem != 1:
+            raise ShapeError(f"item() needs exactly one element, not {self.nelem}")
+        return read_values(self)[0]
+
+    def tolist(self):
+        vals = read_values(self)
+        if not self.dims:
+            return vals[0]
+        arr = np.empty(len(vals), dtype=object)
+        arr[:] = vals
+        return arr.reshape(self.dims, order="F").tolist()
+
+    def numpy(self):
+        return to_numpy(self)
+
+    def __repr__(self):
+        return f"<tensor {'x'.join(map(str, self.dims)) or 'scalar'} {self.dtype.name} on {self.device.name}>"
+
+
+def byte_extent(t):
+    if t.nelem == 0:
+        return (0, 0)
+    lo = hi = t.offset
+    for d, s in zip(t.dims, t.strides):
+        span = s * (d - 1)
+        if span >= 0:
+            hi += span
+        else:
+            lo += span
+    return (lo, hi + t.dtype.size)
+
+
+# ---------------------------------------------------------------------------
+# construction and host interop
+# ---------------------------------------------------------------------------
+def tensor_create(dims, dtype=None, device=None) -> Tensor:
+    dims = _check_dims(dims)
+    dtype = dtype or default_dtype()
+    device = device or default_device()
+    st = storage_alloc(device, math.prod(dims) * dtype.size, dtype)
+    return Tensor(st, 0, dims, column_major_strides(dims, dtype.size), dtype)
+
+
+tensor = tensor_create
+
+
+def tensor_from_storage(store, dims=None, dtype=None, offset=0) -> Tensor:
+    dtype = dtype or store.dtype
+    if dims is None:
+        dims = ((store.nbytes - offset) // dtype.size,)
+    return Tensor(store, offset, dims, column_major_strides(dims, dtype.size), dtype)
+
+
+_NP = {d: np.dtype(n) for d, n in dtypes.NUMPY_NAME.items() if n}
+_FROM_NP = {np.dtype(v): k for k, v in dtypes.NUMPY_NAME.items() if v}
+
+
+def from_numpy(arr: np.ndarray, device=None, dtype=None) -> Tensor:
+    """Copy a numpy array to the device keeping its dims and byte strides.
+
+    numpy's shape indexes the same way tensor dims do (the reference
+    frontend bridge carries shape/strides over directly,
+    frontend/.../numpy_bridge.py:48-76); byte order is carried as the flag.
+    `dtype` overrides the element type for raw uint16 bfloat16 payloads.
+    """
+    arr = np.asarray(arr)
+    device = device or default_device()
+    order = "big" if arr.dtype.byteorder == ">" else "little"
+    base = arr.dtype.newbyteorder("=")
+    td = dtype or _FROM_NP.get(np.dtype(base))
+    if td is None:
+        raise CastError(f"numpy dtype {arr.dtype} has no gpu equivalent")
+    if not (arr.flags.c_contiguous or arr.flags.f_contiguous):
+        arr = np.asfortranarray(arr)
+    st = storage_alloc(device, arr.nbytes, td)
+    st.write(arr.reshape(-1, order="K").view(np.uint8) if arr.nbytes else b"")
+    strides = arr.strides if arr.ndim else ()
+    t = Tensor(st, 0, arr.shape, strides, td, order)
+    return t
+
+
+def to_numpy(t: Tensor) -> np.ndarray:
+    """Host copy of the tensor's values (numpy dims == tensor dims)."""
+    npd = _NP.get(t.dtype)
+    if npd is None and t.dtype is not dtypes.CHALF:
+        raise CastError(f"dtype {t.dtype.name} has no numpy equivalent")
+    lo, hi = byte_extent(t)
+    raw = bytearray(max(hi - lo, 0))
+    if raw:
+        buf = (C.c_char * len(raw)).from_buffer(raw)
+        _native.check(_native.lib().tpg_memcpy_d2h(buf, t.storage.ptr + lo, len(raw),
+                                                   t.storage.stream.handle), "d2h")
+    t.storage.stream.sync()
+    if t.dtype is dtypes.CHALF:
+        h = np.dtype(np.float16).newbyteorder("<" if t.byteorder == "little" else ">")
+        out = np.empty(t.dims, dtype=np.complex64, order="F")
+        flat = np.frombuffer(bytes(raw), dtype=np.uint8)
+        for idx in np.ndindex(*t.dims):
+            off = t.offset - lo + sum(i * s for i, s in zip(idx, t.strides))
+            re_, im = np.frombuffer(flat[off:off + 4].tobytes(), dtype=h)
+            out[idx] = complex(float(re_), float(im))
+        return out
+    npd = npd.newbyteorder("<" if t.byteorder == "little" else ">")
+    if t.nelem == 0:
+        return np.empty(t.dims, dtype=npd)
+    base = np.frombuffer(bytes(raw), dtype=np.uint8)
+    start = base[t.offset - lo:]
+    usable = (len(start) // t.dtype.size) * t.dtype.size
+    anchor = start[:usable].view(npd)
+    return np.lib.stride_tricks.as_strided(anchor, shape=t.dims, strides=t.strides).copy()
+
+
+def read_values(t: Tensor) -> list:
+    """All element values in logical column-major order (Python objects)."""
+    if t.dtype is dtypes.BFLOAT16:
+        u = to_numpy(Tensor(t.storage, t.offset, t.dims, t.strides, dtypes.UINT16, t.byteorder))
+        vals = u.ravel(order="F").astype(np.uint32) << 16
+        return [float(v) for v in vals.view(np.float32)]
+    arr = to_numpy(t)
+    return [v.item() if hasattr(v, "item") else v for v in arr.ravel(order="F")]
+
+
+def _nested_dims(data):
+    dims, probe = [], data
+    while isinstance(probe, (list, tuple)):
+        dims.append(len(probe))
+        probe = probe[0] if probe else None
+    return tuple(dims)
+
+
+def tensor_from_nested(data, dtype=None, device=None) -> Tensor:
+    """Tensor from nested sequences (outermost list = axis 0)."""
+    dims = _nested_dims(data)
+    flat = np.array(data, dtype=object).reshape(-1) if dims else [data]
+    if dtype is None:
+        d = dtypes.BOOL
+        for v in flat:
+            d = dtypes.promote(d, dtypes.infer_scalar_dtype(v))
+        dtype = d
+    t = tensor_create(dims, dtype, device)
+    # values in logical (column-major) order
+    vals = np.array(flat, dtype=object).reshape(dims or (1,)).ravel(order="F") if dims else flat
+    payload = b"".join(dtypes.pack_value(dtype, dtypes.cast_scalar(v, dtype)) for v in vals)
+    t.storage.write(payload)
+    return t
+
+
+from_nested = tensor_from_nested
+
+
+def scalar_tensor(value, dtype=None, device=None) -> Tensor:
+    if isinstance(value, Scalar):
+        dtype = dtype or value.dtype
+        value = value.value
+    dtype = dtype or dtypes.infer_scalar_dtype(value)
+    t = tensor_create((), dtype, device)
+    t.storage.write(dtypes.pack_value(dtype, dtypes.cast_scalar(value, dtype)))
+    return t
+
+
+def as_scalar(t) -> Scalar:
+    return Scalar(t.item(), t.dtype)
+
+
+# ---------------------------------------------------------------------------
+# views
+# ---------------------------------------------------------------------------
+def _view(t, offset, dims, strides, dtype=None, byteorder=None):
+    return Tensor(t.storage, offset, dims, strides, dtype or t.dtype, byteorder or t.byteorder)
+
+
+def _reshape_strides(t, new_dims):
+    if t.nelem == 0:
+        return column_major_strides(new_dims, t.dtype.size)
+    old = [(d, s) for d, s in zip(t.dims, t.strides) if d != 1]
+    if not old:
+        return tuple(t.dtype.size for _ in new_dims) if all(d == 1 for d in new_dims) else None
+    runs = [[old[0]]]
+    for d, s in old[1:]:
+        pd, ps = runs[-1][-1]
+        if s == ps * pd:
+            runs[-1].append((d, s))
+        else:
+            runs.append([(d, s)])
+    sizes = [math.prod(d for d, _ in r) for r in runs]
+    firsts = [r[0][1] for r in runs]
+    out, ri, filled = [], 0, 1
+    for d in new_dims:
+        if d == 1:
+            out.append(t.dtype.size)
+            continue
+        if ri >= len(runs) or filled * d > sizes[ri]:
+            return None
+        out.append(firsts[ri] * filled)
+        filled *= d
+        if filled == sizes[ri]:
+            ri, filled = ri + 1, 1
+    if ri != len(runs) or filled != 1:
+        return None
+    return tuple(out)
+
+
+def reshape(t, dims) -> Tensor:
+    dims = _check_dims(dims)
+    if math.prod(dims) != t.nelem:
+        raise ShapeError(f"cannot reshape {t.nelem} elements into {dims}")
+    s = _reshape_strides(t, dims)
+    if s is not None:
+        return _view(t, t.offset, dims, s)
+    out = tensor_create(dims, t.dtype, t.device)
+    out.byteorder = t.byteorder
+    raw_gather(t, out)
+    return out
+
+
+def permute_axes(t, order) -> Tensor:
+    order = tuple(int(a) for a in order)
+    if sorted(order) != list(range(t.ndim)):
+        raise ShapeError(f"{order} is not a permutation of 0..{t.ndim - 1}")
+    return _view(t, t.offset, tuple(t.dims[a] for a in order), tuple(t.strides[a] for a in order))
+
+
+def transpose(t) -> Tensor:
+    if t.ndim == 1:
+        return _view(t, t.offset, (1, t.dims[0]), (t.dtype.size, t.strides[0]))
+    return permute_axes(t, tuple(reversed(range(t.ndim))))
+
+
+def broadcast_dims(src, dst):
+    if len(src) > len(dst):
+        raise ShapeError(f"cannot broadcast {src} to fewer-dim {dst}")
+    for k, d in enumerate(src):
+        if d != 1 and d != dst[k]:
+            raise ShapeError(f"cannot broadcast {src} to {dst}: axis {k}")
+
+
+def broadcast_to(t, dims) -> Tensor:
+    dims = _check_dims(dims)
+    broadcast_dims(t.dims, dims)
+    strides = [t.strides[k] if k < t.ndim and t.dims[k] == d else 0 for k, d in enumerate(dims)]
+    return _view(t, t.offset, dims, tuple(strides))
+
+
+def broadcast_result_dims(a, b):
+    out = []
+    for k in range(max(len(a), len(b))):
+        da = a[k] if k < len(a) else 1
+        db = b[k] if k < len(b) else 1
+        if da == db or db == 1:
+            out.append(da)
+        elif da == 1:
+            out.append(db)
+        else:
+            raise ShapeError(f"shapes {a} and {b} do not broadcast (axis {k}: {da} vs {db})")
+    return tuple(out)
+
+
+def diag_view(t, k=0) -> Tensor:
+    if t.ndim != 2:
+        raise ShapeError("diag_view requires a 2-D tensor")
+    rows, cols = t.dims
+    if k >= 0:
+        n, off = max(0, min(rows, cols - k)), t.offset + k * t.strides[1]
+    else:
+        n, off = max(0, min(rows + k, cols)), t.offset - k * t.strides[0]
+    return _view(t, off if n else t.offset, (n,), (t.strides[0] + t.strides[1],))
+
+
+def real_view(t):
+    return _view(t, t.offset, t.dims, t.strides,
+                 dtype=dtypes.real_counterpart(t.dtype) if t.dtype.is_complex else None)
+
+
+def imag_view(t):
+    if not t.dtype.is_complex:
+        raise CastError(f"imag_view requires a complex tensor, not {t.dtype.name}")
+    return _view(t, t.offset + t.dtype.component_size, t.dims, t.strides,
+                 dtype=dtypes.real_counterpart(t.dtype))
+
+
+def apply_index(t, index) -> Tensor:
+    """Basic indexing: per-axis int (drops the axis) or slice (a view)."""
+    if not isinstance(index, tuple):
+        index = (index,)
+    if len(index) > t.ndim:
+        raise ShapeError("too many indices")
+    off, dims, strides = t.offset, [], []
+    for k in range(t.ndim):
+        d, s = t.dims[k], t.strides[k]
+        it = index[k] if k < len(index) else slice(None)
+        if isinstance(it, int):
+            i = it + d if it < 0 else it
+            if not 0 <= i < d:
+                raise ShapeError(f"index {it} out of range for axis {k}")
+            off += i * s
+        elif isinstance(it, slice):
+            start, stop, step = it.indices(d)
+            n = len(range(start, stop, step))
+            off += (start * s) if n else 0
+            dims.append(n)
+            strides.append(s * step)
+        else:
+            raise ShapeError(f"unsupported index {it!r}")
+    return _view(t, off, dims, strides)
+
+
+# ---------------------------------------------------------------------------
+# overlap analysis
+# ---------------------------------------------------------------------------
+def self_overlap(t) -> bool:
+    if t._so is None:
+        axes = sorted((abs(s), d) for d, s in zip(t.dims, t.strides) if d > 1)
+        if any(s == 0 for s, _ in axes):
+            t._so = True
+        else:
+            cov, res = t.dtype.size, False
+            for s, d in axes:
+                if s < cov:
+                    res = True
+                    break
+                cov += s * (d - 1)
+            t._so = res
+    return t._so
+
+
+def pair_overlap(a, b) -> str:
+    if a.storage is not b.storage:
+        return OverlapVerdict.DISJOINT
+    la, ha = byte_extent(a)
+    lb, hb = byte_extent(b)
+    if ha <= lb or hb <= la:
+        return OverlapVerdict.DISJOINT
+    if a.offset == b.offset and a.dims == b.dims and a.strides == b.strides and a.dtype is b.dtype:
+        return OverlapVerdict.EXACT
+    return OverlapVerdict.POSSIBLE
+
+
+# ---------------------------------------------------------------------------
+# raw data movement and byte order
+# ---------------------------------------------------------------------------
+def raw_gather(src, dst) -> None:
+    """Byte-exact element copy in logical order (tensors._raw_gather,
+    tensors.py:686-699) through the descriptor gather (no pair list)."""
+    if src.dtype.size != dst.dtype.size or src.dims != dst.dims:
+        raise ShapeError("raw gather needs equal dims and element size")
+    if src.nelem == 0:
+        return
+    plan = canonicalize(dst, src)
+    stream = dst.storage.stream
+    if src.storage.stream is not stream:
+        src.storage.stream.sync()
+    _native.check(_native.lib().tpg_gather_plan(
+        stream.handle, C.byref(plan.to_c()), dst.storage.ptr, dst.offset, src.storage.ptr,
+        src.offset, src.dtype.size), "gather")
+
+
+def contiguous_clone(t) -> Tensor:
+    out = tensor_create(t.dims, t.dtype, t.device)
+    out.byteorder = t.byteorder
+    raw_gather(t, out)
+    return out
+
+
+def _flip(order):
+    return "big" if order == "little" else "little"
+
+
+def byteswap(t) -> None:
+    """Reverse every element's bytes in place and flip the flag (tensors.py:615-631)."""
+    from . import dispatch
+    if t.readonly:
+        raise ReadOnlyError("byteswap target is read-only")
+    h = dispatch.lookup("core", t.device.type.name, "byteswap")
+    plan = canonicalize(t)
+    buf, base, dtype = t.storage.view(), t.offset, t.dtype
+    t.storage.stream.submit(lambda: h(buf, base, plan, dtype, t.byteorder))
+    t.byteorder = _flip(t.byteorder)
+
+
+def set_byteorder(t, order: str) -> None:
+    if order not in ("little", "big"):
+        raise ValueError(f"byte order must be 'little' or 'big', not {order!r}")
+    t.byteorder = order
+
+
+def device_transfer(t, device) -> Tensor:
+    """Copy to another gpu keeping bytes and byte order (ops.py:110-118)."""
+    src = t if _is_dense(t) else contiguous_clone(t)
+    out = tensor_create(t.dims, t.dtype, device)
+    out.byteorder = t.byteorder
+    out.strides = src.strides
+    lo, hi = byte_extent(src)
+    if hi > lo:
+        src.storage.stream.sync()
+        _native.check(_native.lib().tpg_memcpy_d2d(out.storage.ptr, src.storage.ptr + lo, hi - lo,
+                                                   out.storage.stream.handle), "peer copy")
+    out.offset = src.offset - lo
+    return out
+
+
+def _is_dense(t) -> bool:
+    lo, hi = byte_extent(t)
+    return hi - lo == t.nelem * t.dtype.size and not self_overlap(t) and all(s >= 0 for s in t.strides)

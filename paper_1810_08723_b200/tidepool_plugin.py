@@ -1,0 +1,272 @@
+"""Drop-in adapter: the gpu table for an UNMODIFIED reference `tidepool`.
+
+The reference hands Python closures across its function table (SURVEY.md
+§8b): `store` (ops._make_store, ops.py:145-152), codec `unpack` functions
+(dtypes.codec, dtypes.py:357-391), scalar `fn`s (kernels.py:50-158) and
+reduction (init, step, fin) triples (ops.py:522-556).  This module recovers
+the descriptors those closures encode (dtype, byte order, mode, op, compute
+dtype, norm order) by introspection, so the same C-ABI kernels serve the
+reference's own pipeline:
+
+    import tidepool
+    from paper_1810_08723_b200 import tidepool_plugin
+    tidepool_plugin.register(tidepool)      # adds device type "gpu"
+    x = tidepool.cast(t, device=tidepool.devices.by_name("gpu0"))
+
+The decoding helpers are also used by tests/golden/make_golden.py to turn
+captured reference table calls into golden vectors.
+"""
+
+from __future__ import annotations
+
+
+def _cells(fn) -> dict:
+    code = getattr(fn, "__code__", None)
+    if code is None or fn.__closure__ is None:
+        return {}
+    return {n: c.cell_contents for n, c in zip(code.co_freevars, fn.__closure__)}
+
+
+def decode_codec(ref_dtypes, fn):
+    """(dtype name, byteorder) of a reference codec unpack/pack function."""
+    for (d, order), pair in ref_dtypes._CODEC_CACHE.items():
+        if fn is pair[0] or fn is pair[1]:
+            return d.name, order
+    raise LookupError("function is not a reference codec")
+
+
+def prime_codecs(ref_dtypes) -> None:
+    """Populate every (dtype, byteorder) codec so reverse lookups succeed."""
+    for d in ref_dtypes.ALL_DTYPES:
+        for order in ("little", "big"):
+            ref_dtypes.codec(d, order)
+
+
+def decode_store(ref_dtypes, store):
+    """(dtype name, byteorder, mode) of an ops._make_store closure (or the
+    assign_index store, indexing.py:459-460: same free variables)."""
+    cells = _cells(store)
+    if set(cells) >= {"pack", "to", "mode"}:
+        name, order = decode_codec(ref_dtypes, cells["pack"])
+        return cells["to"].name, order, cells["mode"]
+    if "pack" in cells:  # a bare pack wrapper (tests wrap pack in a lambda)
+        name, order = decode_codec(ref_dtypes, cells["pack"])
+        return name, order, "standard"
+    raise LookupError("unrecognised store closure")
+
+
+def unary_forces_complex(fn) -> bool:
+    """unary_scalar_fn returns `lambda v: complex_fn(complex(v))` for the
+    complex branch (kernels.py:145-146)."""
+    code = getattr(fn, "__code__", None)
+    return code is not None and code.co_freevars == ("complex_fn",)
+
+
+def norm_order(step) -> float:
+    cells = _cells(step)
+    return float(cells.get("p", 2.0))
+
+
+# ---------------------------------------------------------------------------
+# registration into the reference
+# ---------------------------------------------------------------------------
+def register(tidepool_module, count: int | None = None):
+    """Attach B200 gpu devices and the ("core", "gpu") table to `tidepool`.
+
+    Storage for gpu tensors must be host-addressable in the reference object
+    model (storage.view() memoryviews), so buffers are CUDA
+    managed allocations exposed as ctypes arrays; kernels read/write them
+    in place.  Returns the list of registered devices.
+    """
+    import ctypes as C
+
+    from . import _native, abi
+    from . import table as tb
+
+    tp = tidepool_module
+    ref_devices, ref_dispatch, ref_dtypes = tp.devices, tp.dispatch, tp.dtypes
+    prime_codecs(ref_dtypes)
+    L = _native.lib()
+    gpu_type = ref_devices.DeviceType("gpu", supports_byteswapped=True, async_capable=False)
+
+    class ManagedBuffer:
+        def __init__(self, nbytes):
+            cudart = C.CDLL("libcudart.so.12", mode=C.RTLD_GLOBAL)
+            self._cudart = cudart
+            ptr = C.c_void_p()
+            rc = cudart.cudaMallocManaged(C.byref(ptr), C.c_size_t(max(nbytes, 1)), C.c_uint(1))
+            if rc != 0:
+                raise tp.errors.AllocationError(f"cudaMallocManaged failed ({rc})")
+            self.ptr = ptr.value
+            self.nbytes = nbytes
+            self.arr = (C.c_ubyte * max(nbytes, 1)).from_address(self.ptr)
+
+        def __len__(self):
+            return self.nbytes
+
+        def __buffer__(self, flags):
+            return memoryview(self.arr)[: self.nbytes]
+
+        def __del__(self):
+            try:
+                self._cudart.cudaDeviceSynchronize()
+                self._cudart.cudaFree(C.c_void_p(self.ptr))
+            except Exception:
+                pass
+
+    class GpuDevice(ref_devices.Device):
+        def __init__(self, index):
+            super().__init__(gpu_type, index)
+
+        def allocate(self, nbytes):
+            if nbytes < 0:
+                raise tp.errors.AllocationError("negative allocation size")
+            self.alloc_count += 1
+            buf = ManagedBuffer(nbytes)
+            view = memoryview(buf.arr).cast("B")[:nbytes]
+            return _Owned(view, buf)
+
+    class _Owned(bytearray):
+        pass
+
+    # the reference Storage calls memoryview(buf): hand it a memoryview-able
+    # object that keeps the managed buffer alive
+    class _OwnedView:
+        def __init__(self, view, owner):
+            self.view = view
+            self.owner = owner
+
+    def _allocate(self, nbytes):
+        buf = ManagedBuffer(nbytes)
+        self.alloc_count += 1
+        arr = buf.arr
+        arr._tpg_owner = buf  # keep alive with the ctypes array
+        return arr
+
+    GpuDevice.allocate = _allocate
+
+    def _ptr(buf) -> int:
+        return C.addressof(C.c_char.from_buffer(buf)) if not isinstance(buf, memoryview) else \
+            _mv_ptr(buf)
+
+    def _mv_ptr(mv) -> int:
+        import numpy as np
+        return int(np.frombuffer(mv, dtype=np.uint8).ctypes.data)
+
+    class _Buf:
+        __slots__ = ("ptr",)
+
+        def __init__(self, mv):
+            self.ptr = _mv_ptr(mv)
+
+    def _codec(fn):
+        name, order = decode_codec(ref_dtypes, fn)
+        from . import dtypes as D
+        return tb.Codec(D.by_name(name), order)
+
+    def _store(store):
+        name, order, mode = decode_store(ref_dtypes, store)
+        from . import dtypes as D
+        return tb.Store(D.by_name(name), order, mode)
+
+    from . import dtypes as D
+    from .plan import IterPlan
+
+    def _plan(p):
+        return IterPlan(p.extents, p.strides)
+
+    def _sync():
+        L.tpg_stream_sync(None)
+
+    def binary(op):
+        entry = tb.binary_entry(op)
+
+        def h(plan, d_buf, store, a_buf, a_unpack, b_buf, b_unpack, fn, bases):
+            ca = _codec(a_unpack)
+            entry(_plan(plan), _Buf(d_buf), _store(store), _Buf(a_buf), ca, _Buf(b_buf),
+                  _codec(b_unpack), tb.BinaryFn(op, D.widen_for_compute(ca.dtype)), bases)
+            _sync()
+        return h
+
+    def unary(op):
+        entry = tb.unary_entry(op)
+
+        def h(plan, d_buf, store, a_buf, a_unpack, fn, bases):
+            ca = _codec(a_unpack)
+            fc = op != "identity" and unary_forces_complex(fn) and not ca.dtype.is_complex
+            entry(_plan(plan), _Buf(d_buf), _store(store), _Buf(a_buf), ca,
+                  tb.UnaryFn(op, D.widen_for_compute(ca.dtype), "standard", fc), bases)
+            _sync()
+        return h
+
+    def reduce_(op):
+        entry = tb.reduce_entry(op)
+
+        def h(outer, inner, d_buf, store, a_buf, a_unpack, init, step, fin, bases):
+            ca = _codec(a_unpack)
+            p = norm_order(step) if op == "norm" else 2.0
+            acc = tb.ReduceAcc(op, D.widen_for_compute(ca.dtype), p)
+            entry(_plan(outer), _plan(inner), _Buf(d_buf), _store(store), _Buf(a_buf), ca,
+                  acc, acc, acc, bases)
+            _sync()
+        return h
+
+    def matmul(d_buf, d_base, d_strides, store, a_buf, a_base, a_strides, a_unpack, b_buf,
+               b_base, b_strides, b_unpack, m, n, k, mul, init, step, fin):
+        ca = _codec(a_unpack)
+        tb.matmul_entry(_Buf(d_buf), d_base, d_strides, _store(store), _Buf(a_buf), a_base,
+                        a_strides, ca, _Buf(b_buf), b_base, b_strides, _codec(b_unpack), m, n, k,
+                        tb.MatmulFn(D.widen_for_compute(ca.dtype)), None, None, None)
+        _sync()
+
+    def fill(plan, buf, pack, value, base):
+        c = _codec(pack)
+        tb.fill_entry(_plan(plan), _Buf(buf), c, value, base)
+        _sync()
+
+    def arange(plan, buf, pack, cast_fn, base):
+        tb.arange_entry(_plan(plan), _Buf(buf), _codec(pack), cast_fn, base)
+        _sync()
+
+    def byteswap(buf, base, plan, dtype):
+        tb.byteswap_entry(_Buf(buf), base, _plan(plan), D.by_name(dtype.name))
+        _sync()
+
+    def gather(dst_buf, src_buf, pairs, size):
+        tb.gather_entry(_Buf(dst_buf), _Buf(src_buf), pairs, size)
+        _sync()
+
+    def scatter(pairs, d_buf, store, s_buf, s_unpack):
+        tb.scatter_entry(pairs, _Buf(d_buf), _store(store), _Buf(s_buf), _codec(s_unpack))
+        _sync()
+
+    def scatter_fill(offsets, d_buf, pack, value):
+        tb.scatter_fill_entry(offsets, _Buf(d_buf), _codec(pack), value)
+        _sync()
+
+    table = {}
+    for op in tb.BINARY_OPS:
+        table[op] = binary(op)
+    for op in tb.UNARY_OPS:
+        table[op] = unary(op)
+    table["copy"] = unary("identity")
+    for op in tb.REDUCE_OPS:
+        table[f"reduce_{op}" if op in ("minimum", "maximum") else op] = reduce_(op)
+    table.update(matmul=matmul, fill=fill, arange=arange, byteswap=byteswap, gather=gather,
+                 scatter=scatter, scatter_fill=scatter_fill)
+    ref_dispatch.register_device_impl("core", "gpu", table)
+
+    n = C.c_int(0)
+    L.tpg_device_count(C.byref(n))
+    n = n.value if count is None else min(n.value, count)
+    devs = [GpuDevice(i) for i in range(n)]
+    ref_devices._devices.extend(devs)
+    orig_configure = ref_devices.configure
+
+    def configure(*a, **k):
+        orig_configure(*a, **k)
+        ref_devices._devices.extend(devs)
+
+    ref_devices.configure = configure
+    _ = abi
+    return devs

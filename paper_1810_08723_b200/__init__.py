@@ -10,7 +10,7 @@ kernels to an unmodified reference `tidepool` as its "gpu" device type.
 """
 
 from . import dispatch as _dispatch
-from . import dtypes, errors, plan, table
+from . import dtypes, errors, plan, table, tensors
 from .devices import GPU_TYPE, configure, gpu, list_devices
 from .dispatch import lookup, override_op, register_device_impl, register_module, table_stats
 from .dtypes import (cast_scalar, implicit_casting, promote, set_implicit_casting,
@@ -22,7 +22,7 @@ from .ops import (absolute, add, arange, arccosine, arcsine, array_equal, bytesw
                   maximum, minimum, multiply, negate, ones, outer, reduce, sine, square_root,
                   subtract, zeros)
 from .plan import IterPlan, build_plan, canonicalize
-from .tensor import (MAX_DIMS, Scalar, Tensor, apply_index, broadcast_to, contiguous_clone,
+from .tensors import (MAX_DIMS, Scalar, Tensor, apply_index, broadcast_to, contiguous_clone,
                      diag_view, from_nested, from_numpy, imag_view, pair_overlap, permute_axes,
                      read_values, real_view, reshape, scalar_tensor, self_overlap, set_byteorder,
                      set_default_device, set_default_dtype, tensor, tensor_create,

@@ -51,7 +51,11 @@ struct Dom<K_FLT> {
   static __device__ T zero() { return 0.0; }
   static __device__ T load(int dt, R16 r) { return dec_flt(dt, r); }
   static __device__ T mac(T acc, T x, T y) { return __dadd_rn(acc, __dmul_rn(x, y)); }
-  static __device__ R16 enc(int dt, T v, uint32_t* fl) { return enc_from_flt(dt, v, fl); }
+  // the reference accumulates with Neumaier compensation (kernels.py:192-198),
+  // which turns any non-finite partial sum into NaN ((s - t) = inf - inf)
+  static __device__ R16 enc(int dt, T v, uint32_t* fl) {
+    return enc_from_flt(dt, isfinite(v) ? v : __longlong_as_double(0x7ff8000000000000ll), fl);
+  }
 };
 template <>
 struct Dom<K_CPX> {
@@ -63,7 +67,10 @@ struct Dom<K_CPX> {
     const double im = __dadd_rn(__dmul_rn(x.x, y.y), __dmul_rn(x.y, y.x));
     return make_double2(__dadd_rn(acc.x, re), __dadd_rn(acc.y, im));
   }
-  static __device__ R16 enc(int dt, T v, uint32_t* fl) { return enc_from_cpx(dt, v.x, v.y, fl); }
+  static __device__ R16 enc(int dt, T v, uint32_t* fl) {
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    return enc_from_cpx(dt, isfinite(v.x) ? v.x : nan, isfinite(v.y) ? v.y : nan, fl);
+  }
 };
 
 constexpr int GT = 64, GK = 16;

@@ -118,7 +118,9 @@ __device__ __forceinline__ void acc_feed(Acc& x, const RedParams& p, R16 r, int6
     } else if (KIND == K_FLT) {
       const double v = dec_flt(p.sdt, r);
       if (isnan(v)) {
-        if (idx == 0) { x.b = 1.0; x.d = v; }  // first element NaN: sticks
+        // first element NaN sticks; p < 0 selects the NaN-skipping variant
+        // used for per-shard partials (sharded.py)
+        if (idx == 0 && p.p >= 0.0) { x.b = 1.0; x.d = v; }
         return;
       }
       if (x.i < 0 || (mn ? v < x.a : v > x.a)) { x.a = v; x.i = idx; }
@@ -236,7 +238,8 @@ __device__ __forceinline__ void acc_store(const RedParams& p, const Acc& x, int6
   } else {  // min / max
     if (KIND == K_INT) o = enc_from_int(p.ddt, x.v, false, fl);
     else if (KIND == K_UINT) o = enc_from_int(p.ddt, x.v, true, fl);
-    else if (KIND == K_FLT) o = enc_from_flt(p.ddt, x.b != 0.0 ? x.d : x.a, fl);
+    else if (KIND == K_FLT)
+      o = enc_from_flt(p.ddt, x.b != 0.0 ? x.d : (x.i < 0 ? __longlong_as_double(0x7ff8000000000000ll) : x.a), fl);
     else if (x.b != 0.0) o = enc_from_cpx(p.ddt, x.d, __longlong_as_double(x.v), fl);
     else o = enc_from_cpx(p.ddt, x.a, x.c, fl);
   }
@@ -388,9 +391,33 @@ __global__ void __launch_bounds__(256) k_red_final(RedParams p) {
   if (st) atomicOr(p.flags, st);
 }
 
+// sequential: one thread per output walks the inner plan in order, exactly
+// like reduce_strided; used where the combine order is observable beyond
+// rounding (complex products: inf/NaN propagation depends on the order).
+template <int OP, int KIND>
+__global__ void __launch_bounds__(128) k_red_seq(RedParams p) {
+  uint32_t st = 0;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < p.O;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    int64_t doff, soff;
+    outer_offsets(p, o, doff, soff);
+    Acc x = acc_init<OP, KIND>();
+    for (int64_t j = 0; j < p.N; ++j)
+      acc_feed<OP, KIND>(x, p, load_raw(p.sdt, p.sbase + soff + inner_offset(p, j), p.saligned), j);
+    acc_store<OP, KIND>(p, x, doff, st);
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
 template <int OP, int KIND>
 static int launch_red(RedParams& p, Stream* st, bool col) {
   const int dev = st->device;
+  if (OP == TPG_RPRODUCT && KIND == K_CPX) {
+    const int g = (int)std::min<int64_t>((p.O + 127) / 128, 65535);
+    k_red_seq<OP, KIND><<<g, 128, 0, st->s>>>(p);
+    TPG_LAUNCH_CHECK("reduce seq");
+    return TPG_OK;
+  }
   const int64_t target = (int64_t)sm_count(dev) * 8;
   if (col) {
     const int64_t nob = (p.O + 255) / 256;

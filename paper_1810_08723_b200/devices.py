@@ -45,12 +45,9 @@ class GpuStream:
         self._pending: BaseException | None = None
 
     def submit(self, task) -> None:
-        try:
-            task()
-        except BaseException as exc:
-            if self._pending is None:
-                self._pending = exc
-            raise
+        # launches are asynchronous on the CUDA stream; host-side failures
+        # (argument errors, error-mode checks) raise here, synchronously
+        task()
 
     def sync(self) -> None:
         _native.check(_native.lib().tpg_stream_sync(self.handle), "stream sync")

@@ -1,0 +1,205 @@
+"""Multi-GPU sharding of the hot path, one process per GPU.
+
+Elementwise ops, casts and batched gemm shard along the slowest axis (the
+last axis of a column-major tensor, or the batch axis) into contiguous
+slabs, one per rank, with no data-path collective.  A full reduction runs
+locally on each slab to one partial and is finished by ONE all-reduce:
+
+    sum      partial sums in double, all-reduce SUM
+    norm     partial sum |x|^p in double, all-reduce SUM, then ^(1/p)
+    product  partial products, all-reduce PROD
+    min/max  partial extreme over non-NaN values, all-reduce MIN/MAX, plus
+             the reference's first-element rule (ops.py:533-544: the
+             result is NaN iff the first element in plan order is NaN),
+             carried as a flag from the rank holding element 0
+    any/all  all-reduce MAX / MIN of 0/1
+
+The reference itself is single-process with placement-only multi-device
+support (devices.py:195, ops.py:110-118); sharding and the all-reduce are
+new.  The communicator is pluggable: NcclComm drives libnccl through the C
+ABI (tpg_nccl_*) over NVLink/NVSwitch; TorchComm uses torch.distributed
+(gloo on CPU for the host-logic tests).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import _native
+
+SUM, PROD, MAX, MIN = 0, 1, 2, 3
+
+
+def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous [lo, hi) slab of n units for `rank` (balanced, ordered)."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+# ---------------------------------------------------------------------------
+# communicators
+# ---------------------------------------------------------------------------
+class TorchComm:
+    """torch.distributed all-reduce on small host arrays (any backend)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def allreduce(self, values: np.ndarray, op: int) -> np.ndarray:
+        import torch
+        t = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64).copy())
+        rop = {SUM: self.dist.ReduceOp.SUM, PROD: self.dist.ReduceOp.PRODUCT,
+               MAX: self.dist.ReduceOp.MAX, MIN: self.dist.ReduceOp.MIN}[op]
+        self.dist.all_reduce(t, op=rop, group=self.group)
+        return t.numpy()
+
+
+class NcclComm:
+    """libnccl over NVLink through the C ABI; rendezvous via any object
+    exchange (e.g. torch.distributed.broadcast_object_list)."""
+
+    def __init__(self, device, rank: int, world: int, share_id):
+        L = _native.lib()
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            _native.check(L.tpg_nccl_get_unique_id(uid), "nccl unique id")
+        raw = share_id(bytes(uid) if rank == 0 else None)
+        C.memmove(uid, raw, 128)
+        _native.check(L.tpg_nccl_init(device.index, world, rank, uid), "nccl init")
+        self.device, self.rank, self.world = device, rank, world
+        self._buf = device.allocate(64)
+
+    def allreduce(self, values: np.ndarray, op: int) -> np.ndarray:
+        L = _native.lib()
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        s = self.device.default_stream()
+        _native.check(L.tpg_memcpy_h2d(self._buf, v.ctypes.data, v.nbytes, s.handle))
+        _native.check(L.tpg_nccl_allreduce(s.handle, self._buf, v.size, 11, op), "allreduce")
+        out = np.empty_like(v)
+        _native.check(L.tpg_memcpy_d2h(out.ctypes.data, self._buf, v.nbytes, s.handle))
+        s.sync()
+        return out
+
+    def close(self):
+        _native.lib().tpg_nccl_destroy()
+
+
+# ---------------------------------------------------------------------------
+# combining local partials (pure host logic, tested with gloo on CPU)
+# ---------------------------------------------------------------------------
+def combine_partials(op: str, partial: float, comm, *, holds_first: bool = False,
+                     first_is_nan: bool = False, has_values: bool = True, p: float = 2.0):
+    """Finish a full reduction from one local partial per rank."""
+    if op in ("sum", "norm"):
+        s = float(comm.allreduce(np.array([partial]), SUM)[0])
+        return s if op == "sum" else (math.sqrt(s) if p == 2.0 else s ** (1.0 / p))
+    if op == "product":
+        return float(comm.allreduce(np.array([partial]), PROD)[0])
+    if op in ("minimum", "maximum"):
+        mx = op == "maximum"
+        val = partial if (has_values and not math.isnan(partial)) else (-math.inf if mx else math.inf)
+        flag = 1.0 if (holds_first and first_is_nan) else 0.0
+        cnt = 1.0 if has_values else 0.0
+        v = comm.allreduce(np.array([val]), MAX if mx else MIN)[0]
+        f, c = comm.allreduce(np.array([flag, cnt]), SUM)
+        if f > 0:
+            return math.nan
+        if c == 0:
+            raise TypeError(f"{op} of an empty range")
+        return float(v)
+    if op == "any":
+        return bool(comm.allreduce(np.array([1.0 if partial else 0.0]), MAX)[0])
+    if op == "all":
+        return bool(comm.allreduce(np.array([1.0 if partial else 0.0]), MIN)[0])
+    raise ValueError(op)
+
+
+# ---------------------------------------------------------------------------
+# device-side sharded operations
+# ---------------------------------------------------------------------------
+class Sharded:
+    """A tensor split into contiguous slabs along `axis`, one per rank."""
+
+    def __init__(self, local, dims, axis, lo, rank, world):
+        self.local, self.dims, self.axis, self.lo = local, tuple(dims), axis, lo
+        self.rank, self.world = rank, world
+
+    @classmethod
+    def from_numpy(cls, arr, rank, world, device, axis=None):
+        from . import tensors as tz
+        axis = arr.ndim - 1 if axis is None else axis
+        lo, hi = shard_bounds(arr.shape[axis], world, rank)
+        sl = [slice(None)] * arr.ndim
+        sl[axis] = slice(lo, hi)
+        return cls(tz.from_numpy(np.asfortranarray(arr[tuple(sl)]), device), arr.shape, axis, lo,
+                   rank, world)
+
+    def map(self, fn, *others):
+        """Apply a local op slab by slab (no communication)."""
+        out = fn(self.local, *[o.local if isinstance(o, Sharded) else o for o in others])
+        return Sharded(out, self.dims, self.axis, self.lo, self.rank, self.world)
+
+    def reduce_full(self, op: str, comm, p: float = 2.0):
+        """Full reduction: local kernel + one all-reduce."""
+        from . import dtypes, ops
+        from . import tensors as tz
+        t = self.local
+        has = t.nelem > 0
+        if op in ("sum", "norm"):
+            part = (_local_sum(t) if op == "sum" else _local_power_sum(t, p)) if has else 0.0
+            return combine_partials(op, part, comm, p=p)
+        if op in ("minimum", "maximum"):
+            first_nan = False
+            part = math.nan
+            if has:
+                if self.lo == 0:
+                    v0 = tz.read_values(tz.apply_index(t, tuple(0 for _ in t.dims)) if t.ndim else t)
+                    first_nan = isinstance(v0[0], float) and math.isnan(v0[0])
+                part = _local_extreme(t, op)
+            return combine_partials(op, part, comm, holds_first=self.lo == 0,
+                                    first_is_nan=first_nan, has_values=has)
+        if op == "product":
+            return combine_partials(op, float(ops.reduce("product", t).item()) if has else 1.0,
+                                    comm)
+        if op in ("any", "all"):
+            v = bool(ops.reduce(op, t).item()) if has else (op == "all")
+            return combine_partials(op, v, comm)
+        raise ValueError(op)
+
+
+def _scalar_double(t):
+    from . import dtypes
+    from . import tensors as tz
+    return tz.tensor_create((), dtypes.DOUBLE, t.device)
+
+
+def _local_sum(t) -> float:
+    """Slab sum, compensated on the device, stored once as a double."""
+    from . import ops
+    dst = _scalar_double(t)
+    ops.reduce("sum", t, dest=dst)
+    return float(dst.item())
+
+
+def _local_power_sum(t, p) -> float:
+    from . import ops
+    dst = _scalar_double(t)
+    ops.reduce("norm", t, dest=dst, p=p)
+    return float(dst.item()) ** p
+
+
+def _local_extreme(t, op) -> float:
+    """Extreme over the non-NaN values of the slab, on the device (the
+    reduce kernel's NaN-skipping variant, selected by p < 0)."""
+    from . import ops
+    dst = _scalar_double(t)
+    ops.reduce(op, t, dest=dst, p=-1.0)
+    return float(dst.item())

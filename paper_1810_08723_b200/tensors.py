@@ -248,7 +248,7 @@ def from_numpy(arr: np.ndarray, device=None, dtype=None) -> Tensor:
     if not (arr.flags.c_contiguous or arr.flags.f_contiguous):
         arr = np.asfortranarray(arr)
     st = storage_alloc(device, arr.nbytes, td)
-    st.write(arr.reshape(-1, order="K").view(np.uint8) if arr.nbytes else b"")
+    st.write(arr.ravel(order="K").view(np.uint8) if arr.nbytes else b"")
     strides = arr.strides if arr.ndim else ()
     t = Tensor(st, 0, arr.shape, strides, td, order)
     return t

@@ -53,10 +53,10 @@ class ShadowOracle:
 
     @staticmethod
     def _dbuf(op, args):
-        if op == "matmul":
+        if op in ("matmul", "byteswap"):
             return args[0]
-        if op in ("fill", "arange", "byteswap"):
-            return args[1] if op != "byteswap" else args[0]
+        if op in ("sum", "product", "reduce_minimum", "reduce_maximum", "any", "all", "norm"):
+            return args[2]
         return args[1]
 
     def _capture(self, op, args):

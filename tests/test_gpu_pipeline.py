@@ -72,7 +72,7 @@ def test_random_binary_programs():
             a = rand_tensor(rng, pr)
             b = rand_tensor(rng, pr)
             try:
-                tp.tensor.broadcast_result_dims(a.dims, b.dims)
+                tp.tensors.broadcast_result_dims(a.dims, b.dims)
             except tp.ShapeError:
                 continue
             op = pr.choice(tp.ops.BINARY_OPS)

@@ -300,21 +300,36 @@ def extras(tp, dev, L, warmup=3, steps=5):
     run("cfg5_cast_i16BE_to_f16_2^28", lambda: tp.copy(s16, h16), nbytes=4 * n5, fl=False)
     del s16, h16
 
-    for dname, dt in (("f16", tp.half), ("bf16", tp.bfloat16), ("f32", tp.float)):
-        m = 4096
-        base = np.random.default_rng(6).uniform(-1, 1, (m, m)).astype(np.float32)
-        if dt is tp.bfloat16:
-            raw = (base.view(np.uint32) >> 16).astype(np.uint16)
-            A = tp.from_numpy(np.asfortranarray(raw), dev, dtype=tp.bfloat16)
-            B = tp.from_numpy(np.asfortranarray(raw), dev, dtype=tp.bfloat16)
-        else:
+    def gemm_operands(dt, m, k, n, batch=None):
+        rng6 = np.random.default_rng(6)
+        def mk(rows, cols):
+            shape = (rows, cols) if batch is None else (rows, cols, batch)
+            base = rng6.uniform(-1, 1, shape).astype(np.float32)
+            if dt is tp.bfloat16:
+                raw = (base.view(np.uint32) >> 16).astype(np.uint16)
+                return tp.from_numpy(np.asfortranarray(raw), dev, dtype=tp.bfloat16)
             npd = np.float16 if dt is tp.half else np.float32
-            A = tp.from_numpy(np.asfortranarray(base.astype(npd)), dev)
-            B = tp.from_numpy(np.asfortranarray(base.astype(npd)), dev)
-        At = tp.transpose(A)  # K-major A, as SURVEY cfg4
+            return tp.from_numpy(np.asfortranarray(base.astype(npd)), dev)
+        return mk, mk
+
+    # SURVEY cfg4: A = transpose of a column-major base (K-major), B
+    # column-major, C column-major; 2*8192^3 flop per step
+    for dname, dt, m in (("f16", tp.half, 8192), ("bf16", tp.bfloat16, 8192),
+                         ("f32", tp.float, 4096)):
+        mk, _ = gemm_operands(dt, m, m, m)
+        At = tp.transpose(mk(m, m))
+        B = mk(m, m)
         Cm = tp.tensor_create((m, m), dt, dev)
         run(f"cfg4_gemm_{dname}_{m}^3", lambda: tp.matmul(At, B, dest=Cm), flops=2 * m ** 3,
             fl=False, st=3)
+        del At, B, Cm
+    # batched: 64 x (2048 x 2048 x 2048), batch slowest
+    mk, _ = gemm_operands(tp.half, 2048, 2048, 2048, batch=64)
+    Ab, Bb = mk(2048, 2048), mk(2048, 2048)
+    Cb = tp.tensor_create((2048, 2048, 64), tp.half, dev)
+    run("cfg4_gemm_batched_f16_64x2048^3", lambda: tp.matmul_batched(Ab, Bb, dest=Cb),
+        flops=64 * 2 * 2048 ** 3, fl=False, st=3)
+    del Ab, Bb, Cb
     dev.release(flush_buf, stream)
     return res
 

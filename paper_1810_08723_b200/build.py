@@ -26,7 +26,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
           "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", f"-I{ROOT / 'include'}"]
 # files whose double arithmetic must not be contracted into FMAs (the
 # reference computes every + - * as a separately rounded CPython float op)
-NO_FMA = {"tpg_ewise.cu", "tpg_reduce.cu"}
+NO_FMA_PREFIX = ("tpg_ewise", "tpg_reduce")
 
 
 def _headers():
@@ -43,7 +43,7 @@ def _stale(obj: Path, src: Path, deps) -> bool:
 def _compile(src: Path, verbose: bool) -> Path:
     obj = BUILD / (src.stem + ".o")
     cmd = [NVCC, *ARCH, *COMMON, "-c", str(src), "-o", str(obj)]
-    if src.name in NO_FMA:
+    if src.name.startswith(NO_FMA_PREFIX):
         cmd.insert(1, "-fmad=false")
     if verbose:
         print(" ".join(cmd), flush=True)

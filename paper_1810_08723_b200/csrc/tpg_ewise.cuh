@@ -369,6 +369,126 @@ __global__ void __launch_bounds__(256) k_tile(EwParams p, int q, int64_t nt0, in
   if (st) atomicOr(p.flags, st);
 }
 
+// tile_fast: typed variant of `tile` for full 64x64 tiles with unit-stride,
+// 16-B-aligned access along both fast axes (SURVEY cfg2).  Phase 1: each
+// thread loads 16 B of X along q (i0 fastest across a warp, so the
+// transposing smem writes are conflict-free); phase 2: each thread reads 4
+// consecutive i0 of one q column, combines them with Y (imm, broadcast or
+// unit-stride along axis 0) and writes 4*SD bytes to the destination.
+template <int S>
+struct RawT;
+template <>
+struct RawT<1> { typedef uint8_t T; };
+template <>
+struct RawT<2> { typedef uint16_t T; };
+template <>
+struct RawT<4> { typedef uint32_t T; };
+template <>
+struct RawT<8> { typedef uint64_t T; };
+
+template <class F, int NIN, int X, int SD, int SX, int SY>
+__global__ void __launch_bounds__(256) k_tile_fast(EwParams p, int q, int64_t nt0, int64_t ntq,
+                                                   int64_t nrest, int ymode) {
+  typedef typename RawT<SX>::T TX;
+  constexpr int VX = 16 / SX;          // X elements per 16-B load
+  constexpr int CHUNKS = TT / VX;      // 16-B chunks per tile row
+  __shared__ __align__(16) TX sm[TT][TT];  // [q][i0]
+  constexpr int Y = 3 - X;
+  const int dtd = F::dtd(p);
+  uint32_t st = 0;
+  const int64_t nwork = nt0 * ntq * nrest;
+  // tile origin offsets of work item w (per view)
+  auto origin = [&](int64_t w, int64_t (&off)[3], int64_t& t0, int64_t& tq) {
+    t0 = w % nt0;
+    tq = (w / nt0) % ntq;
+    int64_t rr = w / (nt0 * ntq);
+    off[0] = off[1] = off[2] = 0;
+    for (int k = 1; k < p.ndim; ++k) {
+      if (k == q) continue;
+      const int64_t e = p.ext[k];
+      const int64_t c = rr % e;
+      rr /= e;
+#pragma unroll
+      for (int v = 0; v < 3; ++v) off[v] += c * p.str[v][k];
+    }
+  };
+  // X chunks of the next tile are prefetched into registers while the
+  // current tile is combined and stored (software pipelining)
+  constexpr int NP = CHUNKS / 4;
+  uint4 pre[NP];
+  auto prefetch = [&](int64_t w) {
+    int64_t off[3], t0, tq;
+    origin(w, off, t0, tq);
+    const char* xb = p.base[X] + off[X] + t0 * TT * p.str[X][0] + tq * TT * SX;
+#pragma unroll
+    for (int pass = 0; pass < NP; ++pass) {
+      const int i0 = threadIdx.x % TT, c = threadIdx.x / TT + 4 * pass;
+      pre[pass] = __ldcs((const uint4*)(xb + (int64_t)i0 * p.str[X][0] + c * 16));
+    }
+  };
+  if (blockIdx.x < nwork) prefetch(blockIdx.x);
+  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    int64_t off[3], t0, tq;
+    origin(w, off, t0, tq);
+    // phase 1: prefetched chunks -> transposed smem tile
+#pragma unroll
+    for (int pass = 0; pass < NP; ++pass) {
+      const int i0 = threadIdx.x % TT, c = threadIdx.x / TT + 4 * pass;
+      const TX* e = (const TX*)&pre[pass];
+#pragma unroll
+      for (int j = 0; j < VX; ++j) sm[c * VX + j][i0] = e[j];
+    }
+    if (w + gridDim.x < nwork) prefetch(w + gridDim.x);
+    __syncthreads();
+    // phase 2
+    char* db = p.base[0] + off[0] + t0 * TT * SD + tq * TT * p.str[0][q];
+    const char* yb = NIN >= 2 ? p.base[Y] + off[Y] + t0 * TT * p.str[Y][0] + tq * TT * p.str[Y][q]
+                              : nullptr;
+#pragma unroll
+    for (int pass = 0; pass < 4; ++pass) {
+      const int ig = threadIdx.x % 16, qq = threadIdx.x / 16 + 16 * pass;
+      R16 ry[4];
+      if (NIN >= 2) {
+        if (ymode == 0) {
+          ry[0] = ry[1] = ry[2] = ry[3] = p.imm[Y];
+        } else if (ymode == 1) {
+          ry[0] = load_raw(Y == 1 ? F::dta(p) : F::dtb(p), yb + qq * p.str[Y][q], true);
+          ry[1] = ry[2] = ry[3] = ry[0];
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            ry[u] = load_raw(Y == 1 ? F::dta(p) : F::dtb(p),
+                             yb + qq * p.str[Y][q] + (int64_t)(ig * 4 + u) * p.str[Y][0], true);
+        }
+      }
+      R16 o[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const R16 rx{(uint64_t)sm[qq][ig * 4 + u], 0};
+        o[u] = (X == 1) ? F::apply(p, rx, ry[u], 0, st) : F::apply(p, ry[u], rx, 0, st);
+      }
+      if (!p.dry) {
+        char* dp = db + (int64_t)qq * p.str[0][q] + ig * 4 * SD;
+        if constexpr (SD == 4) {
+          *(uint4*)dp = make_uint4((uint32_t)o[0].lo, (uint32_t)o[1].lo, (uint32_t)o[2].lo,
+                                   (uint32_t)o[3].lo);
+        } else if constexpr (SD == 8) {
+          *(ulonglong2*)dp = make_ulonglong2(o[0].lo, o[1].lo);
+          *(ulonglong2*)(dp + 16) = make_ulonglong2(o[2].lo, o[3].lo);
+        } else if constexpr (SD == 2) {
+          *(uint2*)dp = make_uint2((uint32_t)(o[0].lo & 0xffff) | ((uint32_t)o[1].lo << 16),
+                                   (uint32_t)(o[2].lo & 0xffff) | ((uint32_t)o[3].lo << 16));
+        } else {
+          *(uint32_t*)dp = (uint32_t)(o[0].lo & 0xff) | ((uint32_t)(o[1].lo & 0xff) << 8) |
+                           ((uint32_t)(o[2].lo & 0xff) << 16) | ((uint32_t)(o[3].lo & 0xff) << 24);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
 // contig: 1-D unit-stride views, compile-time element sizes; 8 elements per
 // thread per operand moved with the widest aligned vector accesses.
 constexpr int CV = 8;
@@ -564,6 +684,36 @@ int launch_ew(EwParams& p, Stream* st) {
       const int64_t nt0 = (p.ext[0] + TT - 1) / TT, ntq = (p.ext[c.q] + TT - 1) / TT;
       const int64_t nrest = total / (p.ext[0] * p.ext[c.q]);
       const int g = grid_for(nt0 * ntq * nrest, dev, 8);
+      if constexpr (typed) {
+        constexpr int SD = dt_size(DTD);
+        constexpr int SA = DTA >= 0 ? dt_size(DTA) : 1;
+        constexpr int SB = DTB >= 0 ? dt_size(DTB) : 1;
+        const int x = c.x, y = 3 - x, qa = c.q;
+        const int sx = x == 1 ? SA : SB;
+        bool fast = p.ext[0] % TT == 0 && p.ext[qa] % TT == 0 && p.str[0][0] == SD &&
+                    (uintptr_t)p.base[0] % 16 == 0 && p.str[0][qa] % 16 == 0 &&
+                    p.str[x][qa] == sx && (uintptr_t)p.base[x] % 16 == 0 && p.str[x][0] % 16 == 0 &&
+                    SD <= 8 && sx <= 8;
+        for (int k = 1; k < p.ndim && fast; ++k)
+          if (k != qa && (p.str[0][k] % 16 || p.str[x][k] % 16)) fast = false;
+        int ymode = 0;
+        if (NIN >= 2 && fast) {
+          const int sy = y == 1 ? SA : SB;
+          if (p.isimm[y]) ymode = 0;
+          else if (p.str[y][0] == 0) ymode = 1;
+          else if (p.str[y][0] == sy) ymode = 2;
+          else fast = false;
+          if (ymode > 0 && ((uintptr_t)p.base[y] % sy)) fast = false;
+        }
+        if (fast) {
+          if constexpr (SD <= 8 && SA <= 8 && SB <= 8) {
+            if (x == 1) k_tile_fast<F, NIN, 1, SD, SA, SB><<<g, 256, 0, st->s>>>(p, qa, nt0, ntq, nrest, ymode);
+            else if constexpr (NIN >= 2) k_tile_fast<F, NIN, 2, SD, SB, SA><<<g, 256, 0, st->s>>>(p, qa, nt0, ntq, nrest, ymode);
+            TPG_LAUNCH_CHECK("tile_fast launch");
+            return TPG_OK;
+          }
+        }
+      }
       if (c.x == 1) {
         k_tile<F, NIN, 1><<<g, 256, 0, st->s>>>(p, c.q, nt0, ntq, nrest);
       } else {

@@ -11,7 +11,9 @@
 // sum|a||b| for f16/bf16).  A non-finite accumulator becomes
 // NaN, as the reference's compensated sum does.
 //
-// Kernel shape (one output tile per CTA, 192 threads, 1 CTA / SM):
+// Kernel shape (persistent: one CTA per SM loops over output tiles in a
+// grouped raster; 192 threads; two 128x256 fp32 accumulators in TMEM so
+// the epilogue of one tile overlaps the mainloop of the next):
 //   warp 0 lane 0   TMA producer: A tile 128x64 and B tile 256x64 (K-major,
 //                   128B swizzle) per stage, 4-stage mbarrier ring
 //   warp 1 lane 0   MMA issuer: 4 x tcgen05.mma.cta_group::1.kind::f16
@@ -38,7 +40,7 @@ constexpr int TMEM_COLS = 256;
 constexpr int GEMM_THREADS = 192;
 constexpr int GROUP_M = 16;
 constexpr size_t GEMM_SMEM =
-    1024 + (size_t)GSTAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 8 * (2 * GSTAGES + 2) + 16;
+    1024 + (size_t)GSTAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 8 * (2 * GSTAGES + 4) + 16;
 
 struct Sm100Args {
   char* d;
@@ -127,9 +129,31 @@ __device__ __forceinline__ uint32_t cvt_out(int ddt, float f) {
   return __float_as_uint(f);
 }
 
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// grouped raster: GROUP_M row-tiles share the in-flight B tiles in L2
+__device__ __forceinline__ void tile_coords(int t, const Sm100Args& g, int& m_tile, int& n_tile,
+                                            int& batch) {
+  const int per_batch = g.tiles_m * g.tiles_n;
+  batch = t / per_batch;
+  t -= batch * per_batch;
+  const int per_group = GROUP_M * g.tiles_n;
+  const int group = t / per_group;
+  const int first_m = group * GROUP_M;
+  const int gm = min(g.tiles_m - first_m, GROUP_M);
+  const int r = t - group * per_group;
+  m_tile = first_m + r % gm;
+  n_tile = r / gm;
+}
+
+// Persistent: one CTA per SM loops over output tiles.  Two TMEM
+// accumulators (2 x 256 columns) let the epilogue of tile i overlap the
+// mainloop of tile i+1 (tfull/tempty mbarrier pair per accumulator).
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm_sm100(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                 Sm100Args g, uint32_t idesc) {
+                 Sm100Args g, uint32_t idesc, int ntiles) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* As = smem;
@@ -137,27 +161,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* bars = (uint64_t*)(Bs + GSTAGES * B_STAGE_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + GSTAGES;
-  uint64_t* tfull = bars + 2 * GSTAGES;
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * GSTAGES + 1);
+  uint64_t* tfull = bars + 2 * GSTAGES;       // [2]
+  uint64_t* tempty = bars + 2 * GSTAGES + 2;  // [2]
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * GSTAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int batch = blockIdx.y;
-  // grouped raster: GROUP_M row-tiles share the in-flight B tiles in L2
-  const int t = blockIdx.x;
-  const int per_group = GROUP_M * g.tiles_n;
-  const int group = t / per_group;
-  const int first_m = group * GROUP_M;
-  const int gm = min(g.tiles_m - first_m, GROUP_M);
-  const int r = t - group * per_group;
-  const int m_tile = first_m + r % gm;
-  const int n_tile = r / gm;
-
   if (threadIdx.x == 0) {
     for (int s = 0; s < GSTAGES; ++s) {
       mbar_init(su32(&full[s]), 1);
       mbar_init(su32(&empty[s]), 1);
     }
-    mbar_init(su32(tfull), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(su32(&tfull[b]), 1);
+      mbar_init(su32(&tempty[b]), 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_b) : "memory");
@@ -165,7 +182,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(tmem_slot)),
-                 "r"(TMEM_COLS));
+                 "r"(2 * TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -176,91 +193,117 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % GSTAGES;
-        const uint32_t ph = (kb / GSTAGES) & 1;
-        mbar_wait(su32(&empty[s]), ph ^ 1);
-        mbar_expect_tx(su32(&full[s]), A_STAGE_BYTES + B_STAGE_BYTES);
-        tma_load_3d(su32(As + s * A_STAGE_BYTES), &tma_a, su32(&full[s]), kb * GBK, m_tile * GBM,
-                    batch);
-        tma_load_3d(su32(Bs + s * B_STAGE_BYTES), &tma_b, su32(&full[s]), kb * GBK, n_tile * GBN,
-                    batch);
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int m_tile, n_tile, batch;
+        tile_coords(t, g, m_tile, n_tile, batch);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % GSTAGES;
+          const uint32_t ph = (it / GSTAGES) & 1;
+          mbar_wait(su32(&empty[s]), ph ^ 1);
+          mbar_expect_tx(su32(&full[s]), A_STAGE_BYTES + B_STAGE_BYTES);
+          tma_load_3d(su32(As + s * A_STAGE_BYTES), &tma_a, su32(&full[s]), kb * GBK,
+                      m_tile * GBM, batch);
+          tma_load_3d(su32(Bs + s * B_STAGE_BYTES), &tma_b, su32(&full[s]), kb * GBK,
+                      n_tile * GBN, batch);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % GSTAGES;
-        const uint32_t ph = (kb / GSTAGES) & 1;
-        mbar_wait(su32(&full[s]), ph);
+      uint32_t it = 0, lt = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+        const uint32_t b = lt & 1, use = lt >> 1;
+        mbar_wait(su32(&tempty[b]), (use & 1) ^ 1);  // accumulator drained
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t ad = umma_desc_sw128(su32(As + s * A_STAGE_BYTES));
-        const uint64_t bd = umma_desc_sw128(su32(Bs + s * B_STAGE_BYTES));
+        const uint32_t acc = tmem + b * TMEM_COLS;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % GSTAGES;
+          const uint32_t ph = (it / GSTAGES) & 1;
+          mbar_wait(su32(&full[s]), ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t ad = umma_desc_sw128(su32(As + s * A_STAGE_BYTES));
+          const uint64_t bd = umma_desc_sw128(su32(Bs + s * B_STAGE_BYTES));
 #pragma unroll
-        for (int k = 0; k < GBK / 16; ++k)  // +32 B per K16 step inside the swizzle atom
-          umma_f16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-        umma_commit(su32(&empty[s]));
+          for (int k = 0; k < GBK / 16; ++k)  // +32 B per K16 step inside the swizzle atom
+            umma_f16(acc, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          umma_commit(su32(&empty[s]));
+        }
+        umma_commit(su32(&tfull[b]));
       }
-      umma_commit(su32(tfull));
     }
   } else {
     // epilogue: warp w reads TMEM lanes [32*(w%4), 32*(w%4)+32)
     const int q = warp & 3;
-    mbar_wait(su32(tfull), 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int row = m_tile * GBM + q * 32 + lane;
-    char* dbase = g.d + (int64_t)batch * g.dsb;
     const int es = dt_size(g.ddt);
+    uint32_t lt = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      int m_tile, n_tile, batch;
+      tile_coords(t, g, m_tile, n_tile, batch);
+      const uint32_t b = lt & 1, use = lt >> 1;
+      mbar_wait(su32(&tfull[b]), use & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = m_tile * GBM + q * 32 + lane;
+      char* dbase = g.d + (int64_t)batch * g.dsb;
 #pragma unroll 1
-    for (int c = 0; c < GBN / 32; ++c) {
-      uint32_t v[32];
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
-      TMEM_LD32(taddr, v);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      const int n0 = n_tile * GBN + c * 32;
-      if (row < g.m) {
-        char* rp = dbase + (int64_t)row * g.ds0;
-        if (g.epi == 2 && n0 + 32 <= g.n) {
-          // row-major destination: 32 contiguous values per thread
-          if (es == 2) {
-            uint32_t w[16];
+      for (int c = 0; c < GBN / 32; ++c) {
+        uint32_t v[32];
+        const uint32_t taddr =
+            tmem + b * TMEM_COLS + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
+        TMEM_LD32(taddr, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c == GBN / 32 - 1) {
+          // accumulator fully read: hand it back to the MMA warp
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(su32(&tempty[b]));
+        }
+        const int n0 = n_tile * GBN + c * 32;
+        if (row < g.m) {
+          char* rp = dbase + (int64_t)row * g.ds0;
+          if (g.epi == 2 && n0 + 32 <= g.n) {
+            // row-major destination: 32 contiguous values per thread
+            if (es == 2) {
+              uint32_t w[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              w[j] = cvt_out(g.ddt, __uint_as_float(v[2 * j])) |
-                     (cvt_out(g.ddt, __uint_as_float(v[2 * j + 1])) << 16);
-            uint4* dst = (uint4*)(rp + (int64_t)n0 * 2);
+              for (int j = 0; j < 16; ++j)
+                w[j] = cvt_out(g.ddt, __uint_as_float(v[2 * j])) |
+                       (cvt_out(g.ddt, __uint_as_float(v[2 * j + 1])) << 16);
+              uint4* dst = (uint4*)(rp + (int64_t)n0 * 2);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+              for (int j = 0; j < 4; ++j)
+                dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+            } else {
+              uint4* dst = (uint4*)(rp + (int64_t)n0 * 4);
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                dst[j] = make_uint4(cvt_out(g.ddt, __uint_as_float(v[4 * j])),
+                                    cvt_out(g.ddt, __uint_as_float(v[4 * j + 1])),
+                                    cvt_out(g.ddt, __uint_as_float(v[4 * j + 2])),
+                                    cvt_out(g.ddt, __uint_as_float(v[4 * j + 3])));
+            }
           } else {
-            uint4* dst = (uint4*)(rp + (int64_t)n0 * 4);
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              dst[j] = make_uint4(cvt_out(g.ddt, __uint_as_float(v[4 * j])),
-                                  cvt_out(g.ddt, __uint_as_float(v[4 * j + 1])),
-                                  cvt_out(g.ddt, __uint_as_float(v[4 * j + 2])),
-                                  cvt_out(g.ddt, __uint_as_float(v[4 * j + 3])));
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int n = n0 + j;
-            if (n < g.n) {
-              const uint32_t o = cvt_out(g.ddt, __uint_as_float(v[j]));
-              char* p = rp + (int64_t)n * g.ds1;
-              if (es == 2) *(uint16_t*)p = (uint16_t)o;
-              else *(uint32_t*)p = o;
+            for (int j = 0; j < 32; ++j) {
+              const int n = n0 + j;
+              if (n < g.n) {
+                const uint32_t o = cvt_out(g.ddt, __uint_as_float(v[j]));
+                char* pp = rp + (int64_t)n * g.ds1;
+                if (es == 2) *(uint16_t*)pp = (uint16_t)o;
+                else *(uint32_t*)pp = o;
+              }
             }
           }
         }
       }
     }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS));
+                 "r"(2 * TMEM_COLS));
   }
 }
 
@@ -332,7 +375,7 @@ int gemm_sm100(Stream* st, int64_t batch, const tpg_operand* d, const int64_t* d
   if (!(d->dtype == TPG_HALF || d->dtype == TPG_BF16 || d->dtype == TPG_FLOAT)) return 0;
   if (dt_kind(compute) != K_FLT || mode != TPG_STANDARD || d->big_endian) return 0;
   if (m < 128 || n < 128 || k < 64 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) return 0;
-  if (batch > 65535) return 0;
+  if (batch * ((m + GBM - 1) / GBM) * ((n + GBN - 1) / GBN) > INT32_MAX) return 0;
   if (sm_count(st->device) <= 0) return 0;
   {
     int major = 0;
@@ -393,8 +436,9 @@ int gemm_sm100(Stream* st, int64_t batch, const tpg_operand* d, const int64_t* d
                                         (int)GEMM_SMEM));
     attr_set[st->device] = true;
   }
-  dim3 grid((unsigned)(g.tiles_m * g.tiles_n), (unsigned)batch);
-  k_gemm_sm100<<<grid, GEMM_THREADS, GEMM_SMEM, st->s>>>(ma, mb, g, idesc);
+  const int ntiles = g.tiles_m * g.tiles_n * (int)batch;
+  const int grid = ntiles < sm_count(st->device) ? ntiles : sm_count(st->device);
+  k_gemm_sm100<<<grid, GEMM_THREADS, GEMM_SMEM, st->s>>>(ma, mb, g, idesc, ntiles);
   TPG_LAUNCH_CHECK("gemm sm100");
   if (apack) TPG_CUDA_CHECK(cudaFreeAsync(apack, st->s));
   if (bpack) TPG_CUDA_CHECK(cudaFreeAsync(bpack, st->s));

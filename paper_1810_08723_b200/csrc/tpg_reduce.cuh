@@ -1,0 +1,710 @@
+// tpg_reduce.cuh — axis and full reductions (shared by tpg_reduce_*.cu).
+//
+// Replaces kernels.reduce_strided (pkg/src/tidepool/kernels.py:305-320)
+// driven by ops.reduce (ops.py:437-513) with the accumulators of
+// ops._reduction_acc (ops.py:522-556), kernels.make_sum_acc (169-198) and
+// make_product_acc (201-206).  The outer plan walks (dest, src base); the
+// inner plan walks the reduced source axes.
+//
+// Semantics kept from the reference:
+//   sum      floats/complex: compensated (the reference uses Neumaier in
+//            double; here each partial is a double-double TwoSum accumulator,
+//            at least as accurate), ints: exact then wrapped (mod 2^64 is
+//            exact after the final wrap).
+//   product  plain double / complex / wrapped-int product.
+//   min/max  `v if acc is None or v < acc`: the result is NaN iff the first
+//            element in plan order is NaN, otherwise the extreme over the
+//            non-NaN elements, ties keep the earliest element.
+//   any/all  `v != 0` (NaN is truthy).
+//   norm     (sum |v|^p)^(1/p) in double.
+// Work split: each output's inner range is cut into C chunks; a block (row
+// mode: inner axis coalesced) or a thread (column mode: outputs coalesced)
+// produces one partial per (output, chunk); a finalize pass combines the C
+// partials of each output in a fixed order, so results are deterministic.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "tpg_common.cuh"
+#include "tpg_internal.h"
+
+namespace tpg {
+
+struct Acc {
+  double a, b, c, d;  // float / complex payload (double-double pairs)
+  int64_t i;          // index of the selected element (min/max), -1 = none
+  int64_t v;          // integer payload
+};
+
+struct RedParams {
+  int ndo, ndi;
+  int64_t eo[TPG_MAX_DIMS];
+  int64_t so_d[TPG_MAX_DIMS], so_s[TPG_MAX_DIMS];
+  int64_t ei[TPG_MAX_DIMS];
+  int64_t si[TPG_MAX_DIMS];
+  char* dbase;
+  const char* sbase;
+  int ddt, sdt, dswap, sswap, daligned, saligned;
+  int track;
+  double p;
+  uint32_t* flags;
+  int64_t O, N, C, chunk;
+  Acc* ws;
+};
+
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+__device__ __forceinline__ void dd_add(double& hi, double& lo, double v) {
+  double s, e;
+  two_sum(hi, v, s, e);
+  hi = s;
+  lo = __dadd_rn(lo, e);
+}
+__device__ __forceinline__ void dd_merge(double& hi, double& lo, double hi2, double lo2) {
+  double s, e;
+  two_sum(hi, hi2, s, e);
+  hi = s;
+  lo = __dadd_rn(lo, __dadd_rn(lo2, e));
+}
+
+template <int OP, int KIND>
+__device__ __forceinline__ Acc acc_init() {
+  Acc x;
+  x.a = x.b = x.c = x.d = 0.0;
+  x.i = -1;
+  x.v = 0;
+  if (OP == TPG_RPRODUCT) {
+    x.a = 1.0;
+    x.v = 1;
+  }
+  if (OP == TPG_RALL) x.v = 1;
+  return x;
+}
+
+__device__ __forceinline__ bool cpx_nonzero(double2 z) { return z.x != 0.0 || z.y != 0.0; }
+
+// fold one element (plan index idx) into acc
+template <int OP, int KIND>
+__device__ __forceinline__ void acc_feed(Acc& x, const RedParams& p, int sdt, R16 r, int64_t idx) {
+  if (p.sswap) r = swap_raw(sdt, r);
+  if (OP == TPG_RSUM) {
+    if (KIND == K_INT || KIND == K_UINT) x.v = (int64_t)((uint64_t)x.v + (uint64_t)dec_int(sdt, r));
+    else if (KIND == K_FLT) dd_add(x.a, x.b, dec_flt(sdt, r));
+    else {
+      double2 z = dec_cpx(sdt, r);
+      dd_add(x.a, x.b, z.x);
+      dd_add(x.c, x.d, z.y);
+    }
+  } else if (OP == TPG_RPRODUCT) {
+    if (KIND == K_INT || KIND == K_UINT) x.v = (int64_t)((uint64_t)x.v * (uint64_t)dec_int(sdt, r));
+    else if (KIND == K_FLT) x.a = __dmul_rn(x.a, dec_flt(sdt, r));
+    else {
+      double2 z = dec_cpx(sdt, r);
+      const double re = __dsub_rn(__dmul_rn(x.a, z.x), __dmul_rn(x.c, z.y));
+      const double im = __dadd_rn(__dmul_rn(x.a, z.y), __dmul_rn(x.c, z.x));
+      x.a = re;
+      x.c = im;
+    }
+  } else if (OP == TPG_RMIN || OP == TPG_RMAX) {
+    const bool mn = OP == TPG_RMIN;
+    if (KIND == K_INT || KIND == K_UINT) {
+      const int64_t v = dec_int(sdt, r);
+      bool take;
+      if (x.i < 0) take = true;
+      else if (KIND == K_UINT) take = mn ? (uint64_t)v < (uint64_t)x.v : (uint64_t)v > (uint64_t)x.v;
+      else take = mn ? v < x.v : v > x.v;
+      if (take) { x.v = v; x.i = idx; }
+    } else if (KIND == K_FLT) {
+      const double v = dec_flt(sdt, r);
+      if (isnan(v)) {
+        // first element NaN sticks; p < 0 selects the NaN-skipping variant
+        // used for per-shard partials (sharded.py)
+        if (idx == 0 && p.p >= 0.0) { x.b = 1.0; x.d = v; }
+        return;
+      }
+      if (x.i < 0 || (mn ? v < x.a : v > x.a)) { x.a = v; x.i = idx; }
+    } else {
+      const double2 z = dec_cpx(sdt, r);
+      if (isnan(z.x)) {
+        if (idx == 0) { x.b = 1.0; x.d = z.x; x.v = (int64_t)__double_as_longlong(z.y); }
+        return;
+      }
+      const double2 cur = make_double2(x.a, x.c);
+      if (x.i < 0 || (mn ? cpx_lt(z, cur) : cpx_gt(z, cur))) { x.a = z.x; x.c = z.y; x.i = idx; }
+    }
+  } else if (OP == TPG_RANY || OP == TPG_RALL) {
+    bool nz;
+    if (KIND == K_CPX) nz = cpx_nonzero(dec_cpx(sdt, r));
+    else if (KIND == K_FLT) nz = dec_flt(sdt, r) != 0.0;
+    else nz = dec_int(sdt, r) != 0;
+    if (OP == TPG_RANY) x.v |= nz;
+    else x.v &= nz;
+  } else {  // norm
+    double m;
+    if (KIND == K_CPX) {
+      double2 z = dec_cpx(sdt, r);
+      m = hypot(z.x, z.y);
+    } else if (KIND == K_FLT) {
+      m = fabs(dec_flt(sdt, r));
+    } else {
+      const int64_t v = dec_int(sdt, r);
+      if (KIND == K_UINT) m = __ull2double_rn((uint64_t)v);
+      else m = v < 0 ? __ull2double_rn(0ull - (uint64_t)v) : __ll2double_rn(v);
+    }
+    const double t = p.p == 2.0 ? __dmul_rn(m, m) : pow(m, p.p);
+    dd_add(x.a, x.b, t);
+  }
+}
+
+// combine x (earlier chunk) with y (later chunk)
+template <int OP, int KIND>
+__device__ __forceinline__ Acc acc_comb(Acc x, const Acc& y) {
+  if (OP == TPG_RSUM || OP == TPG_RNORM) {
+    if (KIND == K_INT || KIND == K_UINT) {
+      if (OP == TPG_RSUM) x.v = (int64_t)((uint64_t)x.v + (uint64_t)y.v);
+      else dd_merge(x.a, x.b, y.a, y.b);
+    } else {
+      dd_merge(x.a, x.b, y.a, y.b);
+      if (KIND == K_CPX && OP == TPG_RSUM) dd_merge(x.c, x.d, y.c, y.d);
+    }
+  } else if (OP == TPG_RPRODUCT) {
+    if (KIND == K_INT || KIND == K_UINT) x.v = (int64_t)((uint64_t)x.v * (uint64_t)y.v);
+    else if (KIND == K_FLT) x.a = __dmul_rn(x.a, y.a);
+    else {
+      const double re = __dsub_rn(__dmul_rn(x.a, y.a), __dmul_rn(x.c, y.c));
+      const double im = __dadd_rn(__dmul_rn(x.a, y.c), __dmul_rn(x.c, y.a));
+      x.a = re;
+      x.c = im;
+    }
+  } else if (OP == TPG_RMIN || OP == TPG_RMAX) {
+    const bool mn = OP == TPG_RMIN;
+    if (y.b != 0.0) { x.b = y.b; x.d = y.d; if (KIND == K_CPX) x.v = y.v; }
+    if (y.i >= 0) {
+      bool take;
+      if (x.i < 0) {
+        take = true;
+      } else if (KIND == K_INT) {
+        take = mn ? (y.v < x.v || (y.v == x.v && y.i < x.i)) : (y.v > x.v || (y.v == x.v && y.i < x.i));
+      } else if (KIND == K_UINT) {
+        const uint64_t a = (uint64_t)x.v, b = (uint64_t)y.v;
+        take = mn ? (b < a || (b == a && y.i < x.i)) : (b > a || (b == a && y.i < x.i));
+      } else if (KIND == K_FLT) {
+        take = mn ? (y.a < x.a || (y.a == x.a && y.i < x.i)) : (y.a > x.a || (y.a == x.a && y.i < x.i));
+      } else {
+        const double2 a = make_double2(x.a, x.c), b = make_double2(y.a, y.c);
+        const bool better = mn ? cpx_lt(b, a) : cpx_gt(b, a);
+        const bool worse = mn ? cpx_lt(a, b) : cpx_gt(a, b);
+        take = better || (!worse && y.i < x.i);
+      }
+      if (take) {
+        const double sb = x.b, sd = x.d;
+        const int64_t sv = x.v;
+        x.a = y.a; x.c = y.c; x.i = y.i;
+        if (KIND == K_INT || KIND == K_UINT) x.v = y.v;
+        x.b = sb; x.d = sd;
+        if (KIND == K_CPX) x.v = sv;
+      }
+    }
+  } else if (OP == TPG_RANY) {
+    x.v |= y.v;
+  } else {  // all
+    x.v &= y.v;
+  }
+  return x;
+}
+
+template <int OP, int KIND>
+__device__ __forceinline__ void acc_store(const RedParams& p, const Acc& x, int64_t doff,
+                                          uint32_t& st) {
+  uint32_t* fl = p.track ? &st : nullptr;
+  R16 o;
+  if (OP == TPG_RANY || OP == TPG_RALL) {
+    o = enc_from_int(p.ddt, x.v, false, fl);
+  } else if (OP == TPG_RNORM) {
+    const double s = __dadd_rn(x.a, x.b);
+    const double r = p.p == 2.0 ? sqrt(s) : pow(s, 1.0 / p.p);
+    o = enc_from_flt(p.ddt, r, fl);
+  } else if (OP == TPG_RSUM) {
+    if (KIND == K_INT) o = enc_from_int(p.ddt, x.v, false, fl);
+    else if (KIND == K_UINT) o = enc_from_int(p.ddt, x.v, true, fl);
+    else if (KIND == K_FLT) o = enc_from_flt(p.ddt, __dadd_rn(x.a, x.b), fl);
+    else o = enc_from_cpx(p.ddt, __dadd_rn(x.a, x.b), __dadd_rn(x.c, x.d), fl);
+  } else if (OP == TPG_RPRODUCT) {
+    if (KIND == K_INT) o = enc_from_int(p.ddt, x.v, false, fl);
+    else if (KIND == K_UINT) o = enc_from_int(p.ddt, x.v, true, fl);
+    else if (KIND == K_FLT) o = enc_from_flt(p.ddt, x.a, fl);
+    else o = enc_from_cpx(p.ddt, x.a, x.c, fl);
+  } else {  // min / max
+    if (KIND == K_INT) o = enc_from_int(p.ddt, x.v, false, fl);
+    else if (KIND == K_UINT) o = enc_from_int(p.ddt, x.v, true, fl);
+    else if (KIND == K_FLT)
+      o = enc_from_flt(p.ddt, x.b != 0.0 ? x.d : (x.i < 0 ? __longlong_as_double(0x7ff8000000000000ll) : x.a), fl);
+    else if (x.b != 0.0) o = enc_from_cpx(p.ddt, x.d, __longlong_as_double(x.v), fl);
+    else o = enc_from_cpx(p.ddt, x.a, x.c, fl);
+  }
+  if (p.dswap) o = swap_raw(p.ddt, o);
+  store_raw(p.ddt, p.dbase + doff, o, p.daligned);
+}
+
+__device__ __forceinline__ void outer_offsets(const RedParams& p, int64_t o, int64_t& doff,
+                                              int64_t& soff) {
+  doff = 0;
+  soff = 0;
+  for (int k = 0; k < p.ndo; ++k) {
+    const int64_t e = p.eo[k];
+    const int64_t c = o % e;
+    o /= e;
+    doff += c * p.so_d[k];
+    soff += c * p.so_s[k];
+  }
+}
+
+__device__ __forceinline__ int64_t inner_offset(const RedParams& p, int64_t j) {
+  if (p.ndi == 1) return j * p.si[0];
+  int64_t off = 0;
+  for (int k = 0; k < p.ndi; ++k) {
+    const int64_t e = p.ei[k];
+    const int64_t c = j % e;
+    j /= e;
+    off += c * p.si[k];
+  }
+  return off;
+}
+
+template <int OP, int KIND>
+__device__ __forceinline__ Acc warp_comb(Acc x) {
+  // lanes hold consecutive sub-ranges in lane order; combine in order.
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    Acc y;
+    y.a = __shfl_down_sync(0xffffffffu, x.a, s);
+    y.b = __shfl_down_sync(0xffffffffu, x.b, s);
+    y.c = __shfl_down_sync(0xffffffffu, x.c, s);
+    y.d = __shfl_down_sync(0xffffffffu, x.d, s);
+    y.i = __shfl_down_sync(0xffffffffu, x.i, s);
+    y.v = __shfl_down_sync(0xffffffffu, x.v, s);
+    const int lane = threadIdx.x & 31;
+    if ((lane & (2 * s - 1)) == 0 && lane + s < 32) x = acc_comb<OP, KIND>(x, y);
+  }
+  return x;
+}
+
+// Source dtype SDT is a template parameter for the hot dtypes (f64, f32) so
+// decoding is resolved at compile time; SDT = -1 reads it from the params.
+template <int SDT>
+__device__ __forceinline__ int sdt_of(const RedParams& p) { return SDT >= 0 ? SDT : p.sdt; }
+
+// row mode: one block per (output, chunk); threads stride the chunk with U
+// independent accumulators each (latency hiding, U loads in flight).
+template <int OP, int KIND, int SDT>
+__global__ void __launch_bounds__(256) k_red_rows(RedParams p) {
+  constexpr int U = 8;
+  __shared__ Acc sh[8];
+  uint32_t st = 0;
+  const int sdt = sdt_of<SDT>(p);
+  const int64_t nwork = p.O * p.C;
+  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int64_t o = w / p.C, c = w - o * p.C;
+    int64_t doff, soff;
+    outer_offsets(p, o, doff, soff);
+    const int64_t j0 = c * p.chunk;
+    const int64_t j1 = min(p.N, j0 + p.chunk);
+    Acc x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = acc_init<OP, KIND>();
+    if (p.ndi == 1) {
+      const int64_t s0 = p.si[0];
+      const char* base = p.sbase + soff;
+      for (int64_t jb = j0 + threadIdx.x; jb < j1; jb += 256 * U) {
+        R16 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t j = jb + u * 256;
+          if (j < j1) r[u] = load_raw(sdt, base + j * s0, p.saligned);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t j = jb + u * 256;
+          if (j < j1) acc_feed<OP, KIND>(x[u], p, sdt, r[u], j);
+        }
+      }
+    } else {
+      for (int64_t jb = j0 + threadIdx.x; jb < j1; jb += 256 * U) {
+        R16 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t j = jb + u * 256;
+          if (j < j1) r[u] = load_raw(sdt, p.sbase + soff + inner_offset(p, j), p.saligned);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t j = jb + u * 256;
+          if (j < j1) acc_feed<OP, KIND>(x[u], p, sdt, r[u], j);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 1; u < U; ++u) x[0] = acc_comb<OP, KIND>(x[0], x[u]);
+    Acc t = warp_comb<OP, KIND>(x[0]);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) sh[warp] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Acc a = sh[0];
+      for (int k = 1; k < 8; ++k) a = acc_comb<OP, KIND>(a, sh[k]);
+      if (p.C == 1) acc_store<OP, KIND>(p, a, doff, st);
+      else p.ws[o * p.C + c] = a;
+    }
+    __syncthreads();
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+// column mode: one thread per (output, chunk); outputs along outer axis 0
+// are adjacent in memory so a warp's loads coalesce.  Two accumulators
+// alternate to break the dependency chain; U loads are in flight.
+template <int OP, int KIND, int SDT>
+__global__ void __launch_bounds__(256) k_red_cols(RedParams p, int64_t nob) {
+  constexpr int U = 8;
+  uint32_t st = 0;
+  const int sdt = sdt_of<SDT>(p);
+  const int64_t nwork = nob * p.C;
+  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int64_t ob = w % nob, c = w / nob;
+    const int64_t o = ob * 256 + threadIdx.x;
+    if (o >= p.O) continue;
+    int64_t doff, soff;
+    outer_offsets(p, o, doff, soff);
+    const int64_t j0 = c * p.chunk;
+    const int64_t j1 = min(p.N, j0 + p.chunk);
+    Acc x[2];
+    x[0] = x[1] = acc_init<OP, KIND>();
+    const bool flat = p.ndi == 1;
+    const int64_t s0 = p.si[0];
+    for (int64_t jb = j0; jb < j1; jb += U) {
+      R16 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (jb + u < j1)
+          r[u] = load_raw(sdt, p.sbase + soff + (flat ? (jb + u) * s0 : inner_offset(p, jb + u)),
+                          p.saligned);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (jb + u < j1) acc_feed<OP, KIND>(x[u & 1], p, sdt, r[u], jb + u);
+    }
+    x[0] = acc_comb<OP, KIND>(x[0], x[1]);
+    if (p.C == 1) acc_store<OP, KIND>(p, x[0], doff, st);
+    else p.ws[o * p.C + c] = x[0];
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+// finalize for few partials per output (C <= 32): one warp per output, lane
+// c holds partial c, combined by the fixed warp tree.
+template <int OP, int KIND>
+__global__ void __launch_bounds__(256) k_red_final_warp(RedParams p) {
+  uint32_t st = 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t o = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); o < p.O; o += nw) {
+    Acc x = lane < p.C ? p.ws[o * p.C + lane] : acc_init<OP, KIND>();
+    x = warp_comb<OP, KIND>(x);
+    if (lane == 0) {
+      int64_t doff, soff;
+      outer_offsets(p, o, doff, soff);
+      acc_store<OP, KIND>(p, x, doff, st);
+    }
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+// finalize: one block per output; all partials are loaded up front
+// (coalesced, independent), then combined in a fixed tree order.
+template <int OP, int KIND>
+__global__ void __launch_bounds__(256) k_red_final(RedParams p) {
+  __shared__ Acc sh[8];
+  uint32_t st = 0;
+  for (int64_t o = blockIdx.x; o < p.O; o += gridDim.x) {
+    Acc x = acc_init<OP, KIND>();
+    constexpr int PF = 8;
+    for (int64_t c0 = threadIdx.x; c0 < p.C; c0 += 256 * PF) {
+      Acc y[PF];
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int64_t c = c0 + u * 256;
+        y[u] = c < p.C ? p.ws[o * p.C + c] : acc_init<OP, KIND>();
+      }
+#pragma unroll
+      for (int u = 0; u < PF; ++u) x = acc_comb<OP, KIND>(x, y[u]);
+    }
+    x = warp_comb<OP, KIND>(x);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) sh[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Acc a = sh[0];
+      for (int k = 1; k < 8; ++k) a = acc_comb<OP, KIND>(a, sh[k]);
+      int64_t doff, soff;
+      outer_offsets(p, o, doff, soff);
+      acc_store<OP, KIND>(p, a, doff, st);
+    }
+    __syncthreads();
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+// sequential: one thread per output walks the inner plan in order, exactly
+// like reduce_strided; used where the combine order is observable beyond
+// rounding (complex products: inf/NaN propagation depends on the order).
+template <int OP, int KIND>
+__global__ void __launch_bounds__(128) k_red_seq(RedParams p) {
+  uint32_t st = 0;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < p.O;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    int64_t doff, soff;
+    outer_offsets(p, o, doff, soff);
+    Acc x = acc_init<OP, KIND>();
+    for (int64_t j = 0; j < p.N; ++j)
+      acc_feed<OP, KIND>(x, p, p.sdt, load_raw(p.sdt, p.sbase + soff + inner_offset(p, j), p.saligned), j);
+    acc_store<OP, KIND>(p, x, doff, st);
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+// ---------------------------------------------------------------------------
+// Float fast path (SURVEY cfg3: f64/f32 sum, norm, min, max).  Same
+// semantics as the Acc machinery (it produces an Acc at the end), but the
+// per-element state is just the double-double pair or (best, index), with
+// NA independent accumulators per thread and U loads in flight.
+template <int OP>
+struct FAcc {
+  double hi, lo;  // sum / norm: double-double; min/max: hi = best value
+  int64_t idx;    // min/max: index of best (-1 none)
+  double nanv;    // min/max: first element (when NaN)
+  bool fnan;
+  __device__ __forceinline__ void init() {
+    hi = lo = 0.0;
+    idx = -1;
+    nanv = 0.0;
+    fnan = false;
+  }
+  __device__ __forceinline__ void feed(double v, int64_t j, double pp) {
+    if (OP == TPG_RSUM) {
+      dd_add(hi, lo, v);
+    } else if (OP == TPG_RNORM) {
+      const double m = fabs(v);
+      dd_add(hi, lo, pp == 2.0 ? __dmul_rn(m, m) : pow(m, pp));
+    } else {
+      if (isnan(v)) {
+        if (j == 0 && pp >= 0.0) { fnan = true; nanv = v; }
+      } else if (idx < 0 || (OP == TPG_RMIN ? v < hi : v > hi)) {
+        hi = v;
+        idx = j;
+      }
+    }
+  }
+  __device__ __forceinline__ Acc to_acc() const {
+    Acc x = acc_init<OP, K_FLT>();
+    if (OP == TPG_RSUM || OP == TPG_RNORM) {
+      x.a = hi;
+      x.b = lo;
+    } else {
+      x.a = hi;
+      x.i = idx;
+      if (fnan) { x.b = 1.0; x.d = nanv; }
+    }
+    return x;
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ double ld_real(const char* ptr) {
+  return (double)__ldcs((const T*)ptr);
+}
+
+template <int OP, typename T>
+__global__ void __launch_bounds__(256) k_red_rows_flt(RedParams p) {
+  constexpr int U = 8, NA = 4;
+  __shared__ Acc sh[8];
+  uint32_t st = 0;
+  const int64_t nwork = p.O * p.C;
+  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int64_t o = w / p.C, c = w - o * p.C;
+    int64_t doff, soff;
+    outer_offsets(p, o, doff, soff);
+    const int64_t j0 = c * p.chunk;
+    const int64_t j1 = min(p.N, j0 + p.chunk);
+    FAcc<OP> x[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) x[a].init();
+    const int64_t s0 = p.si[0];
+    const char* base = p.sbase + soff;
+    for (int64_t jb = j0 + threadIdx.x; jb < j1; jb += 256 * U) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = jb + u * 256;
+        v[u] = j < j1 ? ld_real<T>(base + j * s0) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = jb + u * 256;
+        if (j < j1) x[u % NA].feed(v[u], j, p.p);
+      }
+    }
+    Acc t = x[0].to_acc();
+#pragma unroll
+    for (int a = 1; a < NA; ++a) t = acc_comb<OP, K_FLT>(t, x[a].to_acc());
+    t = warp_comb<OP, K_FLT>(t);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) sh[warp] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Acc a = sh[0];
+      for (int k = 1; k < 8; ++k) a = acc_comb<OP, K_FLT>(a, sh[k]);
+      if (p.C == 1) acc_store<OP, K_FLT>(p, a, doff, st);
+      else p.ws[o * p.C + c] = a;
+    }
+    __syncthreads();
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+template <int OP, typename T>
+__global__ void __launch_bounds__(256) k_red_cols_flt(RedParams p, int64_t nob) {
+  constexpr int U = 8, NA = 2;
+  uint32_t st = 0;
+  const int64_t nwork = nob * p.C;
+  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int64_t ob = w % nob, c = w / nob;
+    const int64_t o = ob * 256 + threadIdx.x;
+    if (o >= p.O) continue;
+    int64_t doff, soff;
+    outer_offsets(p, o, doff, soff);
+    const int64_t j0 = c * p.chunk;
+    const int64_t j1 = min(p.N, j0 + p.chunk);
+    FAcc<OP> x[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) x[a].init();
+    const int64_t s0 = p.si[0];
+    const char* base = p.sbase + soff;
+    for (int64_t jb = j0; jb < j1; jb += U) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = jb + u < j1 ? ld_real<T>(base + (jb + u) * s0) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (jb + u < j1) x[u % NA].feed(v[u], jb + u, p.p);
+    }
+    Acc t = acc_comb<OP, K_FLT>(x[0].to_acc(), x[1].to_acc());
+    if (p.C == 1) acc_store<OP, K_FLT>(p, t, doff, st);
+    else p.ws[o * p.C + c] = t;
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+template <int OP, typename T>
+void launch_flt(RedParams& p, Stream* st, bool col) {
+  if (col) {
+    const int64_t nob = (p.O + 255) / 256;
+    const int64_t work = nob * p.C;
+    const int g = (int)(work < (int64_t)1 << 30 ? work : (int64_t)1 << 30);
+    k_red_cols_flt<OP, T><<<g, 256, 0, st->s>>>(p, nob);
+  } else {
+    const int64_t work = p.O * p.C;
+    const int g = (int)(work < (int64_t)1 << 30 ? work : (int64_t)1 << 30);
+    k_red_rows_flt<OP, T><<<g, 256, 0, st->s>>>(p);
+  }
+}
+
+template <int OP, int KIND, int SDT>
+void launch_main(RedParams& p, Stream* st, bool col) {
+  if constexpr (KIND == K_FLT && SDT >= 0 &&
+                (OP == TPG_RSUM || OP == TPG_RNORM || OP == TPG_RMIN || OP == TPG_RMAX)) {
+    if (p.ndi == 1 && p.saligned) {
+      if (SDT == TPG_DOUBLE) launch_flt<OP, double>(p, st, col);
+      else launch_flt<OP, float>(p, st, col);
+      return;
+    }
+  }
+  if (col) {
+    const int64_t nob = (p.O + 255) / 256;
+    const int64_t work = nob * p.C;
+    const int g = (int)(work < (int64_t)1 << 30 ? work : (int64_t)1 << 30);
+    k_red_cols<OP, KIND, SDT><<<g, 256, 0, st->s>>>(p, nob);
+  } else {
+    const int64_t work = p.O * p.C;
+    const int g = (int)(work < (int64_t)1 << 30 ? work : (int64_t)1 << 30);
+    k_red_rows<OP, KIND, SDT><<<g, 256, 0, st->s>>>(p);
+  }
+}
+
+template <int OP, int KIND>
+int launch_red(RedParams& p, Stream* st, bool col) {
+  const int dev = st->device;
+  if (OP == TPG_RPRODUCT && KIND == K_CPX) {
+    const int g = (int)std::min<int64_t>((p.O + 127) / 128, 65535);
+    k_red_seq<OP, KIND><<<g, 128, 0, st->s>>>(p);
+    TPG_LAUNCH_CHECK("reduce seq");
+    return TPG_OK;
+  }
+  const int64_t target = (int64_t)sm_count(dev) * 8;
+  if (col) {
+    const int64_t nob = (p.O + 255) / 256;
+    int64_t C = (target + nob - 1) / nob;
+    const int64_t minchunk = 64;
+    if (C > (p.N + minchunk - 1) / minchunk) C = (p.N + minchunk - 1) / minchunk;
+    if (C > 32) C = 32;  // partials of one output fit one warp in the finalize
+    if (C < 1) C = 1;
+    p.chunk = (p.N + C - 1) / C;
+  } else {
+    int64_t C = (target + p.O - 1) / p.O;
+    const int64_t minchunk = 8192;
+    if (C > (p.N + minchunk - 1) / minchunk) C = (p.N + minchunk - 1) / minchunk;
+    if (C < 1) C = 1;
+    p.chunk = (p.N + C - 1) / C;
+  }
+  p.C = (p.N + p.chunk - 1) / p.chunk;
+  if (p.C < 1) p.C = 1;
+  p.ws = nullptr;
+  if (p.C > 1) TPG_CUDA_CHECK(cudaMallocAsync((void**)&p.ws, sizeof(Acc) * p.O * p.C, st->s));
+  bool done = false;
+  if constexpr (KIND == K_FLT) {
+    if (!p.sswap && p.sdt == TPG_DOUBLE) { launch_main<OP, KIND, TPG_DOUBLE>(p, st, col); done = true; }
+    else if (!p.sswap && p.sdt == TPG_FLOAT) { launch_main<OP, KIND, TPG_FLOAT>(p, st, col); done = true; }
+  }
+  if (!done) launch_main<OP, KIND, -1>(p, st, col);
+  TPG_LAUNCH_CHECK("reduce launch");
+  if (p.C > 1) {
+    const int g = (int)(p.O < 65536 ? p.O : 65536);
+    if (p.C <= 32) {
+      const int gw = (int)std::min<int64_t>((p.O + 7) / 8, 65536);
+      k_red_final_warp<OP, KIND><<<gw, 256, 0, st->s>>>(p);
+    } else {
+      k_red_final<OP, KIND><<<g, 256, 0, st->s>>>(p);
+    }
+    TPG_LAUNCH_CHECK("reduce finalize");
+    TPG_CUDA_CHECK(cudaFreeAsync(p.ws, st->s));
+  }
+  return TPG_OK;
+}
+
+template <int OP>
+int launch_kind(RedParams& p, Stream* st, bool col, int kind) {
+  switch (kind) {
+    case K_INT: return launch_red<OP, K_INT>(p, st, col);
+    case K_UINT: return launch_red<OP, K_UINT>(p, st, col);
+    case K_FLT: return launch_red<OP, K_FLT>(p, st, col);
+    default: return launch_red<OP, K_CPX>(p, st, col);
+  }
+}
+
+int reduce_sum_norm(int op, RedParams& p, Stream* st, bool col, int kind);
+int reduce_minmax(int op, RedParams& p, Stream* st, bool col, int kind);
+int reduce_other(int op, RedParams& p, Stream* st, bool col, int kind);
+
+}  // namespace tpg

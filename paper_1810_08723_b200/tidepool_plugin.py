@@ -70,49 +70,66 @@ def norm_order(step) -> float:
 # ---------------------------------------------------------------------------
 # registration into the reference
 # ---------------------------------------------------------------------------
+class _Cudart:
+    """Minimal libcudart access for managed allocations and pointer kinds."""
+
+    def __init__(self):
+        import ctypes as C
+        self.C = C
+        self.lib = C.CDLL("libcudart.so.12", mode=C.RTLD_GLOBAL)
+
+    def malloc_managed(self, n: int) -> int:
+        C = self.C
+        ptr = C.c_void_p()
+        rc = self.lib.cudaMallocManaged(C.byref(ptr), C.c_size_t(max(n, 1)), C.c_uint(1))
+        if rc != 0:
+            raise MemoryError(f"cudaMallocManaged({n}) failed ({rc})")
+        return ptr.value
+
+    def free(self, ptr: int) -> None:
+        self.lib.cudaDeviceSynchronize()
+        self.lib.cudaFree(self.C.c_void_p(ptr))
+
+    def is_device_accessible(self, ptr: int) -> bool:
+        """True for device / managed / pinned memory (cudaPointerGetAttributes)."""
+        C = self.C
+
+        class Attr(C.Structure):
+            _fields_ = [("type", C.c_int), ("device", C.c_int), ("devicePointer", C.c_void_p),
+                        ("hostPointer", C.c_void_p)]
+
+        a = Attr()
+        rc = self.lib.cudaPointerGetAttributes(C.byref(a), C.c_void_p(ptr))
+        if rc != 0:
+            self.lib.cudaGetLastError()
+            return False
+        return a.type in (1, 2, 3)
+
+
 def register(tidepool_module, count: int | None = None):
     """Attach B200 gpu devices and the ("core", "gpu") table to `tidepool`.
 
-    Storage for gpu tensors must be host-addressable in the reference object
+    Storage of gpu tensors must stay host-addressable in the reference object
     model (storage.view() memoryviews), so buffers are CUDA
-    managed allocations exposed as ctypes arrays; kernels read/write them
-    in place.  Returns the list of registered devices.
+    managed allocations exposed as ctypes arrays that kernels read and write
+    in place.  Host (cpu-device) source buffers are staged into managed
+    memory for the duration of one call.  Returns the registered devices.
     """
     import ctypes as C
 
-    from . import _native, abi
+    import numpy as np
+
+    from . import _native
+    from . import dtypes as D
     from . import table as tb
+    from .plan import IterPlan
 
     tp = tidepool_module
     ref_devices, ref_dispatch, ref_dtypes = tp.devices, tp.dispatch, tp.dtypes
     prime_codecs(ref_dtypes)
     L = _native.lib()
+    rt = _Cudart()
     gpu_type = ref_devices.DeviceType("gpu", supports_byteswapped=True, async_capable=False)
-
-    class ManagedBuffer:
-        def __init__(self, nbytes):
-            cudart = C.CDLL("libcudart.so.12", mode=C.RTLD_GLOBAL)
-            self._cudart = cudart
-            ptr = C.c_void_p()
-            rc = cudart.cudaMallocManaged(C.byref(ptr), C.c_size_t(max(nbytes, 1)), C.c_uint(1))
-            if rc != 0:
-                raise tp.errors.AllocationError(f"cudaMallocManaged failed ({rc})")
-            self.ptr = ptr.value
-            self.nbytes = nbytes
-            self.arr = (C.c_ubyte * max(nbytes, 1)).from_address(self.ptr)
-
-        def __len__(self):
-            return self.nbytes
-
-        def __buffer__(self, flags):
-            return memoryview(self.arr)[: self.nbytes]
-
-        def __del__(self):
-            try:
-                self._cudart.cudaDeviceSynchronize()
-                self._cudart.cudaFree(C.c_void_p(self.ptr))
-            except Exception:
-                pass
 
     class GpuDevice(ref_devices.Device):
         def __init__(self, index):
@@ -122,61 +139,66 @@ def register(tidepool_module, count: int | None = None):
             if nbytes < 0:
                 raise tp.errors.AllocationError("negative allocation size")
             self.alloc_count += 1
-            buf = ManagedBuffer(nbytes)
-            view = memoryview(buf.arr).cast("B")[:nbytes]
-            return _Owned(view, buf)
+            ptr = rt.malloc_managed(nbytes)
+            arr = (C.c_ubyte * max(nbytes, 1)).from_address(ptr)
+            arr._tpg_free = _Free(ptr)  # freed with the last reference
+            return arr
 
-    class _Owned(bytearray):
-        pass
+        @property
+        def properties(self):
+            props = super().properties
+            props.update(tb_props(self.index))
+            return props
 
-    # the reference Storage calls memoryview(buf): hand it a memoryview-able
-    # object that keeps the managed buffer alive
-    class _OwnedView:
-        def __init__(self, view, owner):
-            self.view = view
-            self.owner = owner
+    class _Free:
+        def __init__(self, ptr):
+            self.ptr = ptr
 
-    def _allocate(self, nbytes):
-        buf = ManagedBuffer(nbytes)
-        self.alloc_count += 1
-        arr = buf.arr
-        arr._tpg_owner = buf  # keep alive with the ctypes array
-        return arr
+        def __del__(self):
+            try:
+                rt.free(self.ptr)
+            except Exception:
+                pass
 
-    GpuDevice.allocate = _allocate
-
-    def _ptr(buf) -> int:
-        return C.addressof(C.c_char.from_buffer(buf)) if not isinstance(buf, memoryview) else \
-            _mv_ptr(buf)
-
-    def _mv_ptr(mv) -> int:
-        import numpy as np
-        return int(np.frombuffer(mv, dtype=np.uint8).ctypes.data)
+    def tb_props(index):
+        from . import abi
+        p = abi.DeviceProps()
+        L.tpg_device_props_get(index, C.byref(p))
+        return {"name": p.name.decode(), "processor-count": str(p.sm_count),
+                "free-memory": str(p.free_mem)}
 
     class _Buf:
-        __slots__ = ("ptr",)
+        """Device-visible pointer for a reference memoryview (staged when
+        the buffer is ordinary host memory)."""
+        __slots__ = ("ptr", "_tmp")
 
         def __init__(self, mv):
-            self.ptr = _mv_ptr(mv)
+            self._tmp = None
+            if mv is None:
+                self.ptr = None
+                return
+            n = len(mv)
+            host = int(np.frombuffer(mv, dtype=np.uint8).ctypes.data) if n else 0
+            if n == 0 or rt.is_device_accessible(host):
+                self.ptr = host
+            else:
+                self._tmp = _Free(rt.malloc_managed(n))
+                C.memmove(self._tmp.ptr, host, n)
+                self.ptr = self._tmp.ptr
 
     def _codec(fn):
         name, order = decode_codec(ref_dtypes, fn)
-        from . import dtypes as D
         return tb.Codec(D.by_name(name), order)
 
     def _store(store):
         name, order, mode = decode_store(ref_dtypes, store)
-        from . import dtypes as D
         return tb.Store(D.by_name(name), order, mode)
 
-    from . import dtypes as D
-    from .plan import IterPlan
-
-    def _plan(p):
-        return IterPlan(p.extents, p.strides)
+    def _plan(pl):
+        return IterPlan(pl.extents, pl.strides)
 
     def _sync():
-        L.tpg_stream_sync(None)
+        _native.check(L.tpg_stream_sync(None), "sync")
 
     def binary(op):
         entry = tb.binary_entry(op)
@@ -220,8 +242,7 @@ def register(tidepool_module, count: int | None = None):
         _sync()
 
     def fill(plan, buf, pack, value, base):
-        c = _codec(pack)
-        tb.fill_entry(_plan(plan), _Buf(buf), c, value, base)
+        tb.fill_entry(_plan(plan), _Buf(buf), _codec(pack), value, base)
         _sync()
 
     def arange(plan, buf, pack, cast_fn, base):
@@ -268,5 +289,4 @@ def register(tidepool_module, count: int | None = None):
         ref_devices._devices.extend(devs)
 
     ref_devices.configure = configure
-    _ = abi
     return devs

@@ -17,3 +17,13 @@ echo "ncu rc=$?" >> gpurun_out/ncu_bench.log
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_tile -s 3 -c 1 -o gpurun_out/prof_cfg2 -f python bench.py --steps 3 --warmup 3 --no-extras > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?" >> gpurun_out/ncu_full.log
 fi
+if [ "${NCU_RED:-1}" = "1" ]; then
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_red_rows -s 2 -c 1 -o gpurun_out/prof_red -f python -c "
+import sys; sys.path.insert(0,'.')
+import numpy as np, paper_1810_08723_b200 as tp
+X = tp.from_numpy(np.asfortranarray(np.random.default_rng(5).random((8192, 8192))))
+for _ in range(4): tp.reduce('sum', X, axes=(0,))
+tp.gpu(0).synchronize()
+" > gpurun_out/ncu_red.log 2>&1
+echo "ncu red rc=$?" >> gpurun_out/ncu_red.log
+fi

@@ -1,0 +1,86 @@
+"""Drop-in check: the UNMODIFIED reference `tidepool` (installed into
+baseline/_ref by `pip install --target`) runs on the B200 through
+tidepool_plugin.register(); programs on gpu0 must match the same programs
+on the reference's own cpu device (the pattern of the reference's
+tests/test_device_parity.py:17-57).  Skipped when baseline/_ref is absent."""
+
+import math
+import random
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REF = Path(__file__).resolve().parents[1] / "baseline" / "_ref"
+
+
+@pytest.fixture(scope="module")
+def tp():
+    if not (REF / "tidepool").exists():
+        pytest.skip("reference not installed in baseline/_ref")
+    sys.path.insert(0, str(REF))
+    import tidepool
+    from paper_1810_08723_b200 import tidepool_plugin
+    if not any(d.type.name == "gpu" for d in tidepool.devices.list_devices()):
+        tidepool_plugin.register(tidepool, count=1)
+    return tidepool
+
+
+def _eq(x, y):
+    if isinstance(x, complex) or isinstance(y, complex):
+        return _eq(complex(x).real, complex(y).real) and _eq(complex(x).imag, complex(y).imag)
+    if isinstance(x, float) and isinstance(y, float):
+        return (math.isnan(x) and math.isnan(y)) or x == y
+    return x == y
+
+
+def _program(tp, seed, device):
+    tz = tp.tensors
+    a = tp.tensor_create((4, 3), tp.double, device)
+    b = tp.tensor_create((4, 3), tp.double, device)
+    st = random.Random(seed)
+    for t in (a, b):
+        _, pack = tp.dtypes.codec(t.dtype, t.byteorder)
+        buf = t.storage.view()
+        for off in tz.iter_offsets(t):
+            pack(buf, off, round(st.uniform(-4, 4), 3) or 1.0)
+    trace = []
+    c = tp.add(a, b)
+    trace.append(c)
+    tp.multiply(c, 2.0, dest=c)
+    d = tp.subtract(c, tp.apply_index(c, (slice(None, None, -1), slice(None))))
+    trace.append(d)
+    e = tp.square_root(tp.absolute(d))
+    trace.append(e)
+    f = tp.reduce("sum", e, axes=(1,))
+    trace.append(f)
+    g = tp.matmul(tp.transpose(a), b)
+    trace.append(g)
+    h = tp.cast(g, tp.int16)
+    trace.append(h)
+    i = tp.reduce("maximum", tp.cast(a, tp.float))
+    trace.append(i)
+    return [(t.dims, t.dtype.name, tz.read_values(t)) for t in trace]
+
+
+def test_reference_programs_match_on_gpu(tp):
+    gpu = tp.devices.by_name("gpu0")
+    for seed in range(10):
+        cpu_run = _program(tp, seed, tp.cpu())
+        gpu_run = _program(tp, seed, gpu)
+        for (cd, ct, cv), (gd, gt, gv) in zip(cpu_run, gpu_run):
+            assert cd == gd and ct == gt
+            assert all(_eq(x, y) for x, y in zip(cv, gv)), (seed, ct, cv, gv)
+
+
+def test_cross_device_round_trip_and_table_counts(tp):
+    gpu = tp.devices.by_name("gpu0")
+    t = tp.from_nested([[1, 2], [3, 4]], tp.int32)
+    there = tp.cast(t, device=gpu)
+    assert there.device is gpu
+    back = tp.cast(there, device=tp.cpu())
+    assert tp.tensors.read_values(back) == [1, 3, 2, 4]
+    stats = tp.dispatch.table_stats("core", "gpu")
+    assert len(stats) == 31 and stats["copy"] >= 1

@@ -136,6 +136,9 @@ int tpg_memcpy_h2d(void* dst, const void* src, size_t n, tpg_stream stream);
 int tpg_memcpy_d2h(void* dst, const void* src, size_t n, tpg_stream stream);
 int tpg_memcpy_d2d(void* dst, const void* src, size_t n, tpg_stream stream);
 int tpg_memset(void* dst, int value, size_t n, tpg_stream stream);
+/* pitched 2-D copy (any direction; host memory should be pinned to overlap) */
+int tpg_memcpy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                 size_t height, tpg_stream stream);
 
 /* Sticky status word (ops._status) in host-mapped memory, OR-ed by kernels. */
 int tpg_flags_get(int device, uint32_t* flags);

@@ -94,6 +94,7 @@ PROTOTYPES = {
     "tpg_memcpy_d2h": (_i32, [_vp, _vp, C.c_size_t, _vp]),
     "tpg_memcpy_d2d": (_i32, [_vp, _vp, C.c_size_t, _vp]),
     "tpg_memset": (_i32, [_vp, C.c_int, C.c_size_t, _vp]),
+    "tpg_memcpy2d": (_i32, [_vp, C.c_size_t, _vp, C.c_size_t, C.c_size_t, C.c_size_t, _vp]),
     "tpg_flags_get": (_i32, [C.c_int, P(C.c_uint32)]),
     "tpg_flags_clear": (_i32, [C.c_int]),
     "tpg_gate_arm": (_i32, [_vp]),

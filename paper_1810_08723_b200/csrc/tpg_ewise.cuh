@@ -489,6 +489,130 @@ __global__ void __launch_bounds__(256) k_tile_fast(EwParams p, int q, int64_t nt
   if (st) atomicOr(p.flags, st);
 }
 
+// tile_native: the cfg2 family in native float arithmetic.  When every
+// operand value is exactly representable in float and the destination is
+// float, a float +,-,*,/,min,max is bit-identical to the reference's
+// double compute followed by one rounding to float (p_double = 53 >=
+// 2*24+2, so the double rounding is innocuous), and NaN inputs give NaN
+// either way.  Native types instead of R16 keep registers (occupancy) and
+// instruction count low.  No byte swaps, standard mode only.
+__host__ __device__ constexpr bool f32_exact(int dt) {
+  return dt == TPG_INT8 || dt == TPG_UINT8 || dt == TPG_INT16 || dt == TPG_UINT16 ||
+         dt == TPG_HALF || dt == TPG_FLOAT;
+}
+template <int DT>
+struct Native { typedef float T; };
+template <>
+struct Native<TPG_INT8> { typedef int8_t T; };
+template <>
+struct Native<TPG_UINT8> { typedef uint8_t T; };
+template <>
+struct Native<TPG_INT16> { typedef int16_t T; };
+template <>
+struct Native<TPG_UINT16> { typedef uint16_t T; };
+template <>
+struct Native<TPG_HALF> { typedef __half T; };
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v) { return (float)v; }
+template <typename T>
+__device__ __forceinline__ T from_bits(uint64_t b) { return (T)b; }
+template <>
+__device__ __forceinline__ float from_bits<float>(uint64_t b) { return __uint_as_float((uint32_t)b); }
+template <>
+__device__ __forceinline__ __half from_bits<__half>(uint64_t b) { return __ushort_as_half((uint16_t)b); }
+template <>
+__device__ __forceinline__ float to_f<__half>(__half v) { return __half2float(v); }
+
+template <int OP>
+__device__ __forceinline__ float fop(float a, float b) {
+  if (OP == TPG_ADD) return __fadd_rn(a, b);
+  if (OP == TPG_SUBTRACT) return __fsub_rn(a, b);
+  if (OP == TPG_MULTIPLY) return __fmul_rn(a, b);
+  if (OP == TPG_DIVIDE) {
+    if (b == 0.0f) {
+      if (a == 0.0f || isnan(a)) return __int_as_float(0x7fc00000);
+      return copysignf(INFINITY, a) * copysignf(1.0f, b);
+    }
+    return __fdiv_rn(a, b);
+  }
+  if (OP == TPG_MINIMUM) return a <= b ? a : b;
+  return a >= b ? a : b;
+}
+
+// X (transposed) is operand XI (1 or 2); Y: 0 imm, 1 broadcast along
+// axis 0, 2 unit stride along axis 0; NIN == 1: cast-copy of X.
+template <int OP, int NIN, int XI, typename TX, typename TY>
+__global__ void __launch_bounds__(256) k_tile_native(EwParams p, int q, int64_t nt0, int64_t ntq,
+                                                     int64_t nrest, int ymode) {
+  constexpr int VX = 16 / sizeof(TX);
+  constexpr int CHUNKS = TT / VX;
+  __shared__ __align__(16) TX sm[TT][TT];  // [q][i0]
+  constexpr int Y = 3 - XI;
+  const int64_t nwork = nt0 * ntq * nrest;
+  const int64_t sx0 = p.str[XI][0], sdq = p.str[0][q];
+  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int64_t t0 = w % nt0;
+    const int64_t tq = (w / nt0) % ntq;
+    int64_t rr = w / (nt0 * ntq);
+    int64_t off[3] = {0, 0, 0};
+    for (int k = 1; k < p.ndim; ++k) {
+      if (k == q) continue;
+      const int64_t e = p.ext[k];
+      const int64_t c = rr % e;
+      rr /= e;
+#pragma unroll
+      for (int v = 0; v < 3; ++v) off[v] += c * p.str[v][k];
+    }
+    const char* xb = p.base[XI] + off[XI] + t0 * TT * sx0 + tq * TT * (int64_t)sizeof(TX);
+    uint4 buf[CHUNKS / 4];
+#pragma unroll
+    for (int pass = 0; pass < CHUNKS / 4; ++pass) {
+      const int i0 = threadIdx.x % TT, c = threadIdx.x / TT + 4 * pass;
+      buf[pass] = __ldcs((const uint4*)(xb + i0 * sx0 + c * 16));
+    }
+#pragma unroll
+    for (int pass = 0; pass < CHUNKS / 4; ++pass) {
+      const int i0 = threadIdx.x % TT, c = threadIdx.x / TT + 4 * pass;
+      const TX* e = (const TX*)&buf[pass];
+#pragma unroll
+      for (int j = 0; j < VX; ++j) sm[c * VX + j][i0] = e[j];
+    }
+    __syncthreads();
+    float* db = (float*)(p.base[0] + off[0] + t0 * TT * 4 + tq * TT * sdq);
+    const char* yb = NIN >= 2 ? p.base[Y] + off[Y] + t0 * TT * p.str[Y][0] + tq * TT * p.str[Y][q]
+                              : nullptr;
+    float yimm = 0.0f;
+    if (NIN >= 2 && ymode == 0) yimm = to_f<TY>(from_bits<TY>(p.imm[Y].lo));
+#pragma unroll
+    for (int pass = 0; pass < 4; ++pass) {
+      const int ig = threadIdx.x % 16, qq = threadIdx.x / 16 + 16 * pass;
+      float y[4];
+      if (NIN >= 2) {
+        if (ymode == 0) {
+          y[0] = y[1] = y[2] = y[3] = yimm;
+        } else if (ymode == 1) {
+          y[0] = to_f<TY>(__ldg((const TY*)(yb + qq * p.str[Y][q])));
+          y[1] = y[2] = y[3] = y[0];
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            y[u] = to_f<TY>(__ldg((const TY*)(yb + qq * p.str[Y][q] + (ig * 4 + u) * p.str[Y][0])));
+        }
+      }
+      float o[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float x = to_f<TX>(sm[qq][ig * 4 + u]);
+        if (NIN == 1) o[u] = x;
+        else o[u] = XI == 1 ? fop<OP>(x, y[u]) : fop<OP>(y[u], x);
+      }
+      __stcs((float4*)((char*)db + qq * sdq) + ig, make_float4(o[0], o[1], o[2], o[3]));
+    }
+    __syncthreads();
+  }
+}
+
 // contig: 1-D unit-stride views, compile-time element sizes; 8 elements per
 // thread per operand moved with the widest aligned vector accesses.
 constexpr int CV = 8;
@@ -683,7 +807,9 @@ int launch_ew(EwParams& p, Stream* st) {
     if constexpr (NIN >= 1) {
       const int64_t nt0 = (p.ext[0] + TT - 1) / TT, ntq = (p.ext[c.q] + TT - 1) / TT;
       const int64_t nrest = total / (p.ext[0] * p.ext[c.q]);
-      const int g = grid_for(nt0 * ntq * nrest, dev, 8);
+      // one 64x64 tile per block where possible: more independent tiles
+      // in flight per SM than a persistent loop (measured, scripts/ubench.cu)
+      const int g = grid_for(nt0 * ntq * nrest, dev, 32);
       if constexpr (typed) {
         constexpr int SD = dt_size(DTD);
         constexpr int SA = DTA >= 0 ? dt_size(DTA) : 1;
@@ -704,6 +830,19 @@ int launch_ew(EwParams& p, Stream* st) {
           else if (p.str[y][0] == sy) ymode = 2;
           else fast = false;
           if (ymode > 0 && ((uintptr_t)p.base[y] % sy)) fast = false;
+        }
+        const bool plain = !p.swap[0] && !p.swap[1] && !p.swap[2] && !p.track && !p.dry;
+        if constexpr (DTD == TPG_FLOAT && f32_exact(DTA) && (NIN < 2 || f32_exact(DTB)) &&
+                      ((OC == OC_BINARY && KIND == K_FLT) || OC == OC_COPY)) {
+          if (fast && plain) {
+            typedef typename Native<DTA>::T TA;
+            typedef typename Native<(NIN >= 2 ? DTB : DTA)>::T TB;
+            if (NIN == 1) k_tile_native<0, 1, 1, TA, TA><<<g, 256, 0, st->s>>>(p, qa, nt0, ntq, nrest, 0);
+            else if (x == 1) k_tile_native<OP, 2, 1, TA, TB><<<g, 256, 0, st->s>>>(p, qa, nt0, ntq, nrest, ymode);
+            else k_tile_native<OP, 2, 2, TB, TA><<<g, 256, 0, st->s>>>(p, qa, nt0, ntq, nrest, ymode);
+            TPG_LAUNCH_CHECK("tile_native launch");
+            return TPG_OK;
+          }
         }
         if (fast) {
           if constexpr (SD <= 8 && SA <= 8 && SB <= 8) {

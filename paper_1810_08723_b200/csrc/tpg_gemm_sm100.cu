@@ -40,7 +40,7 @@ constexpr int TMEM_COLS = 256;
 constexpr int GEMM_THREADS = 192;
 constexpr int GROUP_M = 16;
 constexpr size_t GEMM_SMEM =
-    1024 + (size_t)GSTAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 8 * (2 * GSTAGES + 4) + 16;
+    1024 + (size_t)GSTAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 4 * 4096 + 8 * (2 * GSTAGES + 4) + 16;
 
 struct Sm100Args {
   char* d;
@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* As = smem;
   uint8_t* Bs = smem + GSTAGES * A_STAGE_BYTES;
-  uint64_t* bars = (uint64_t*)(Bs + GSTAGES * B_STAGE_BYTES);
+  uint8_t* epi_stage = Bs + GSTAGES * B_STAGE_BYTES;  // 4 warps x 4 KB
+  uint64_t* bars = (uint64_t*)(epi_stage + 4 * 4096);
   uint64_t* full = bars;
   uint64_t* empty = bars + GSTAGES;
   uint64_t* tfull = bars + 2 * GSTAGES;       // [2]
@@ -259,6 +260,38 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (lane == 0) mbar_arrive(su32(&tempty[b]));
         }
         const int n0 = n_tile * GBN + c * 32;
+        const int row0 = m_tile * GBM + q * 32;
+        if (g.epi == 1 && row0 + 32 <= g.m && n0 + 32 <= g.n) {
+          // column-major destination: transpose the warp's 32x32 chunk
+          // through shared memory so each lane writes 16-B pieces of columns
+          uint8_t* stg = epi_stage + (warp - 2) * 4096;
+          if (es == 2) {
+            uint16_t* s16 = (uint16_t*)stg;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              s16[j * 32 + lane] = (uint16_t)cvt_out(g.ddt, __uint_as_float(v[j]));
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {
+              const int j = lane / 4 + 8 * it, part = lane % 4;
+              const uint4 val = *(const uint4*)(s16 + j * 32 + part * 8);
+              *(uint4*)(dbase + (int64_t)(row0 + part * 8) * 2 + (int64_t)(n0 + j) * g.ds1) = val;
+            }
+          } else {
+            uint32_t* s32 = (uint32_t*)stg;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) s32[j * 32 + lane] = cvt_out(g.ddt, __uint_as_float(v[j]));
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int j = lane / 8 + 4 * it, part = lane % 8;
+              const uint4 val = *(const uint4*)(s32 + j * 32 + part * 4);
+              *(uint4*)(dbase + (int64_t)(row0 + part * 4) * 4 + (int64_t)(n0 + j) * g.ds1) = val;
+            }
+          }
+          __syncwarp();
+          continue;
+        }
         if (row < g.m) {
           char* rp = dbase + (int64_t)row * g.ds0;
           if (g.epi == 2 && n0 + 32 <= g.n) {
@@ -424,7 +457,8 @@ int gemm_sm100(Stream* st, int64_t batch, const tpg_operand* d, const int64_t* d
   g.ddt = d->dtype;
   const int es = dt_size(d->dtype);
   const bool al = ((uintptr_t)g.d % 16) == 0;
-  g.epi = (ds[1] == es && ds[0] % 16 == 0 && al) ? 2 : (ds[0] == es ? 1 : 0);
+  g.epi = (ds[1] == es && ds[0] % 16 == 0 && al) ? 2
+          : (ds[0] == es && ds[1] % 16 == 0 && al && (batch == 1 || ds[2] % 16 == 0)) ? 1 : 0;
   g.tiles_m = (int)((m + GBM - 1) / GBM);
   g.tiles_n = (int)((n + GBN - 1) / GBN);
   const uint32_t fmt = adt == TPG_BF16 ? 1u : 0u;

@@ -521,14 +521,26 @@ struct FAcc {
   }
 };
 
+// Streaming loads as volatile asm so a batch of them is issued back to back
+// (ptxas otherwise pairs each load with its consumer, leaving one in flight).
 template <typename T>
-__device__ __forceinline__ double ld_real(const char* ptr) {
-  return (double)__ldcs((const T*)ptr);
+__device__ __forceinline__ double ld_real(const char* ptr);
+template <>
+__device__ __forceinline__ double ld_real<double>(const char* ptr) {
+  double v;
+  asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(v) : "l"(ptr));
+  return v;
+}
+template <>
+__device__ __forceinline__ double ld_real<float>(const char* ptr) {
+  float v;
+  asm volatile("ld.global.cs.f32 %0, [%1];" : "=f"(v) : "l"(ptr));
+  return (double)v;
 }
 
 template <int OP, typename T>
-__global__ void __launch_bounds__(256) k_red_rows_flt(RedParams p) {
-  constexpr int U = 8, NA = 4;
+__global__ void __launch_bounds__(256, 4) k_red_rows_flt(RedParams p) {
+  constexpr int U = 4, NA = 4;  // 2 x U loads in flight (double-buffered)
   __shared__ Acc sh[8];
   uint32_t st = 0;
   const int64_t nwork = p.O * p.C;
@@ -543,19 +555,35 @@ __global__ void __launch_bounds__(256) k_red_rows_flt(RedParams p) {
     for (int a = 0; a < NA; ++a) x[a].init();
     const int64_t s0 = p.si[0];
     const char* base = p.sbase + soff;
-    for (int64_t jb = j0 + threadIdx.x; jb < j1; jb += 256 * U) {
-      double v[U];
+    // full iterations: U unconditional loads issued back to back (all in
+    // flight), then consumed; a predicated form lets the compiler pair each
+    // load with its use and serialise them
+    int64_t jb = j0 + threadIdx.x;
+    // Full batches of U loads per thread, software-pipelined: batch k+1 is
+    // loaded while batch k is folded in, so U loads stay in flight whatever
+    // order ptxas schedules the arithmetic in.
+    const int64_t avail = j1 - jb;
+    const int64_t nfull = avail > 256 * (U - 1) ? (avail - 256 * (U - 1) - 1) / (256 * U) + 1 : 0;
+    const char* ptr = base + jb * s0;
+    const int64_t step = 256 * s0;
+    if (nfull > 0) {
+      double v[U], nv[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t j = jb + u * 256;
-        v[u] = j < j1 ? ld_real<T>(base + j * s0) : 0.0;
-      }
+      for (int u = 0; u < U; ++u) v[u] = ld_real<T>(ptr + u * step);
+      for (int64_t k = 0; k < nfull; ++k) {
+        if (k + 1 < nfull) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t j = jb + u * 256;
-        if (j < j1) x[u % NA].feed(v[u], j, p.p);
+          for (int u = 0; u < U; ++u) nv[u] = ld_real<T>(ptr + (U + u) * step);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u % NA].feed(v[u], jb + u * 256, p.p);
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = nv[u];
+        jb += 256 * U;
+        ptr += U * step;
       }
     }
+    for (; jb < j1; jb += 256, ptr += step) x[0].feed(ld_real<T>(ptr), jb, p.p);
     Acc t = x[0].to_acc();
 #pragma unroll
     for (int a = 1; a < NA; ++a) t = acc_comb<OP, K_FLT>(t, x[a].to_acc());
@@ -575,8 +603,8 @@ __global__ void __launch_bounds__(256) k_red_rows_flt(RedParams p) {
 }
 
 template <int OP, typename T>
-__global__ void __launch_bounds__(256) k_red_cols_flt(RedParams p, int64_t nob) {
-  constexpr int U = 8, NA = 2;
+__global__ void __launch_bounds__(256, 4) k_red_cols_flt(RedParams p, int64_t nob) {
+  constexpr int U = 4, NA = 2;  // 2 x U loads in flight (double-buffered)
   uint32_t st = 0;
   const int64_t nwork = nob * p.C;
   for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
@@ -592,14 +620,27 @@ __global__ void __launch_bounds__(256) k_red_cols_flt(RedParams p, int64_t nob) 
     for (int a = 0; a < NA; ++a) x[a].init();
     const int64_t s0 = p.si[0];
     const char* base = p.sbase + soff;
-    for (int64_t jb = j0; jb < j1; jb += U) {
-      double v[U];
+    int64_t jb = j0;
+    const char* ptr = base + j0 * s0;
+    const int64_t nfull = (j1 - j0) / U;
+    if (nfull > 0) {
+      double v[U], nv[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = jb + u < j1 ? ld_real<T>(base + (jb + u) * s0) : 0.0;
+      for (int u = 0; u < U; ++u) v[u] = ld_real<T>(ptr + u * s0);
+      for (int64_t k = 0; k < nfull; ++k) {
+        if (k + 1 < nfull) {
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (jb + u < j1) x[u % NA].feed(v[u], jb + u, p.p);
+          for (int u = 0; u < U; ++u) nv[u] = ld_real<T>(ptr + (U + u) * s0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u % NA].feed(v[u], jb + u, p.p);
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = nv[u];
+        jb += U;
+        ptr += U * s0;
+      }
     }
+    for (; jb < j1; ++jb, ptr += s0) x[0].feed(ld_real<T>(ptr), jb, p.p);
     Acc t = acc_comb<OP, K_FLT>(x[0].to_acc(), x[1].to_acc());
     if (p.C == 1) acc_store<OP, K_FLT>(p, t, doff, st);
     else p.ws[o * p.C + c] = t;

@@ -291,6 +291,16 @@ int tpg_memcpy_d2d(void* dst, const void* src, size_t n, tpg_stream stream) {
   return TPG_OK;
 }
 
+int tpg_memcpy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                 size_t height, tpg_stream stream) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  if (width == 0 || height == 0) return TPG_OK;
+  TPG_CUDA_CHECK(
+      cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault, st->s));
+  return TPG_OK;
+}
+
 int tpg_memset(void* dst, int value, size_t n, tpg_stream stream) {
   Stream* st = resolve_stream(stream);
   if (!st) return arg_fail("no stream");

@@ -28,11 +28,11 @@ def tp():
     return tidepool
 
 
-def _eq(x, y):
+def _eq(x, y, rel=0.0):
     if isinstance(x, complex) or isinstance(y, complex):
-        return _eq(complex(x).real, complex(y).real) and _eq(complex(x).imag, complex(y).imag)
+        return _eq(complex(x).real, complex(y).real, rel) and _eq(complex(x).imag, complex(y).imag, rel)
     if isinstance(x, float) and isinstance(y, float):
-        return (math.isnan(x) and math.isnan(y)) or x == y
+        return (math.isnan(x) and math.isnan(y)) or x == y or abs(x - y) <= rel * abs(y)
     return x == y
 
 
@@ -62,7 +62,10 @@ def _program(tp, seed, device):
     trace.append(h)
     i = tp.reduce("maximum", tp.cast(a, tp.float))
     trace.append(i)
-    return [(t.dims, t.dtype.name, tz.read_values(t)) for t in trace]
+    # elementwise / cast / min-max results are bit-exact; compensated sums
+    # and matmul accumulate in a different order (rel 1e-12)
+    tol = [0.0, 0.0, 0.0, 1e-12, 1e-12, 0.0, 0.0]
+    return [(t.dims, t.dtype.name, tz.read_values(t), r) for t, r in zip(trace, tol)]
 
 
 def test_reference_programs_match_on_gpu(tp):
@@ -70,9 +73,9 @@ def test_reference_programs_match_on_gpu(tp):
     for seed in range(10):
         cpu_run = _program(tp, seed, tp.cpu())
         gpu_run = _program(tp, seed, gpu)
-        for (cd, ct, cv), (gd, gt, gv) in zip(cpu_run, gpu_run):
+        for (cd, ct, cv, rel), (gd, gt, gv, _) in zip(cpu_run, gpu_run):
             assert cd == gd and ct == gt
-            assert all(_eq(x, y) for x, y in zip(cv, gv)), (seed, ct, cv, gv)
+            assert all(_eq(x, y, rel) for x, y in zip(cv, gv)), (seed, ct, cv, gv)
 
 
 def test_cross_device_round_trip_and_table_counts(tp):

@@ -144,6 +144,9 @@ int tpg_memcpy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_
 int tpg_flags_get(int device, uint32_t* flags);
 int tpg_flags_clear(int device);
 
+/* Measurement helper: write then re-read `n` bytes of `scratch` (> L2) on
+   `stream`, leaving the L2 full of clean unrelated lines. */
+int tpg_l2_flush(void* scratch, size_t n, tpg_stream stream);
 /* Measurement helper: hold `stream` until tpg_gate_release() so a batch of
  * timed steps is fully enqueued before the device starts on it. */
 int tpg_gate_arm(tpg_stream stream);

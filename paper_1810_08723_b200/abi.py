@@ -97,6 +97,7 @@ PROTOTYPES = {
     "tpg_memcpy2d": (_i32, [_vp, C.c_size_t, _vp, C.c_size_t, C.c_size_t, C.c_size_t, _vp]),
     "tpg_flags_get": (_i32, [C.c_int, P(C.c_uint32)]),
     "tpg_flags_clear": (_i32, [C.c_int]),
+    "tpg_l2_flush": (_i32, [_vp, C.c_size_t, _vp]),
     "tpg_gate_arm": (_i32, [_vp]),
     "tpg_gate_release": (_i32, []),
     "tpg_binary": (_i32, [_vp, C.c_int, _PLAN, _OP, _OP, _OP, C.c_int, C.c_int]),

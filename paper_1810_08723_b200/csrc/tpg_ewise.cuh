@@ -540,77 +540,140 @@ __device__ __forceinline__ float fop(float a, float b) {
   return a >= b ? a : b;
 }
 
-// X (transposed) is operand XI (1 or 2); Y: 0 imm, 1 broadcast along
-// axis 0, 2 unit stride along axis 0; NIN == 1: cast-copy of X.
+// k_tile_f32: the transposing float kernel (SURVEY cfg2).  X (operand XI,
+// coalesced along plan axis q) is read a 64(i) x 64(j) tile at a time with
+// LPR lanes per tile row, so every warp load covers whole 128-B lines; the
+// conversion to float and any Y that is constant along axis 0 (immediate
+// or broadcast row) are applied in registers right after the load, and the
+// float results go to a shared tile [j][i ^ swz(j)] (XOR swizzle: the
+// transposing stores and the float4 reads are both bank-conflict free).
+// Phase 2 streams float4 columns to the destination (16-B coalesced
+// stores), applying a Y that varies along axis 0 (ymode 2).  Persistent
+// grid; the next tile's X chunks (and its Y row slice) are loaded into
+// registers before the current tile is stored.
+// Y: 0 imm, 1 broadcast along axis 0, 2 unit stride along axis 0;
+// NIN == 1: cast-copy of X.
 template <int OP, int NIN, int XI, typename TX, typename TY>
-__global__ void __launch_bounds__(256) k_tile_native(EwParams p, int q, int64_t nt0, int64_t ntq,
-                                                     int64_t nrest, int ymode) {
-  constexpr int VX = 16 / sizeof(TX);
-  constexpr int CHUNKS = TT / VX;
-  __shared__ __align__(16) TX sm[TT][TT];  // [q][i0]
+__global__ void __launch_bounds__(256, sizeof(TX) >= 4 ? 4 : 5) k_tile_f32(EwParams p, int q, int nt0, int ntq, int ymode) {
+  constexpr int SX = sizeof(TX);
+  constexpr int VX = 16 / SX;          // X elements per 16-B chunk
+  constexpr int LPR = TT * SX / 16;    // lanes per tile row (4, 8 or 16)
+  constexpr int RPW = 32 / LPR;        // tile rows per warp load
+  constexpr int NLD = TT / (8 * RPW);  // 16-B X loads per thread per tile
+  constexpr int SWM = RPW > 4 ? RPW : 4;
   constexpr int Y = 3 - XI;
-  const int64_t nwork = nt0 * ntq * nrest;
-  const int64_t sx0 = p.str[XI][0], sdq = p.str[0][q];
-  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
-    const int64_t t0 = w % nt0;
-    const int64_t tq = (w / nt0) % ntq;
-    int64_t rr = w / (nt0 * ntq);
+  __shared__ __align__(16) float sm[TT][TT];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane % LPR;
+  const int r0 = warp * RPW + lane / LPR;
+  const int swz1 = (c * SWM) & 31;
+  // the plan's remaining axes (other than 0 and q) index blockIdx.y
+  const char* xs;
+  const char* ys = nullptr;
+  char* ds;
+  {
     int64_t off[3] = {0, 0, 0};
+    int64_t rr = blockIdx.y;
     for (int k = 1; k < p.ndim; ++k) {
       if (k == q) continue;
       const int64_t e = p.ext[k];
-      const int64_t c = rr % e;
+      const int64_t cc = rr % e;
       rr /= e;
 #pragma unroll
-      for (int v = 0; v < 3; ++v) off[v] += c * p.str[v][k];
+      for (int v = 0; v < 3; ++v) off[v] += cc * p.str[v][k];
     }
-    const char* xb = p.base[XI] + off[XI] + t0 * TT * sx0 + tq * TT * (int64_t)sizeof(TX);
-    uint4 buf[CHUNKS / 4];
+    xs = p.base[XI] + off[XI];
+    if (NIN >= 2) ys = p.base[Y] + off[Y];
+    ds = p.base[0] + off[0];
+  }
+  const int64_t sx0 = p.str[XI][0], sdq = p.str[0][q];
+  const int64_t syq = NIN >= 2 ? p.str[Y][q] : 0;
+  const int nwork = nt0 * ntq;
+  float yimm = 0.0f;
+  if (NIN >= 2 && ymode == 0) yimm = to_f<TY>(from_bits<TY>(p.imm[Y].lo));
+  uint4 xb[NLD];
+  float yr[VX];
+  auto load = [&](int w) {
+    const int t0 = w % nt0, tq = w / nt0;
+    const char* x = xs + (int64_t)(t0 * TT + r0) * sx0 + tq * TT * SX + c * 16;
 #pragma unroll
-    for (int pass = 0; pass < CHUNKS / 4; ++pass) {
-      const int i0 = threadIdx.x % TT, c = threadIdx.x / TT + 4 * pass;
-      buf[pass] = __ldcs((const uint4*)(xb + i0 * sx0 + c * 16));
+    for (int l = 0; l < NLD; ++l) xb[l] = __ldcs((const uint4*)(x + (int64_t)(l * 8 * RPW) * sx0));
+    if (NIN >= 2 && ymode == 1) {
+      const char* y = ys + (int64_t)(tq * TT + c * VX) * syq;
+#pragma unroll
+      for (int k = 0; k < VX; ++k) yr[k] = to_f<TY>(__ldg((const TY*)(y + k * syq)));
     }
+  };
+  if ((int)blockIdx.x < nwork) load(blockIdx.x);
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+    // phase 1: registers -> float tile (convert, combine with a row-constant Y)
 #pragma unroll
-    for (int pass = 0; pass < CHUNKS / 4; ++pass) {
-      const int i0 = threadIdx.x % TT, c = threadIdx.x / TT + 4 * pass;
-      const TX* e = (const TX*)&buf[pass];
+    for (int l = 0; l < NLD; ++l) {
+      const int i = r0 + l * 8 * RPW;
+      const TX* e = (const TX*)&xb[l];
 #pragma unroll
-      for (int j = 0; j < VX; ++j) sm[c * VX + j][i0] = e[j];
+      for (int k = 0; k < VX; ++k) {
+        const float x = to_f<TX>(e[k]);
+        float v = x;
+        if (NIN >= 2 && ymode <= 1) {
+          const float y = ymode == 0 ? yimm : yr[k];
+          v = XI == 1 ? fop<OP>(x, y) : fop<OP>(y, x);
+        }
+        sm[c * VX + k][i ^ swz1] = v;
+      }
     }
     __syncthreads();
-    float* db = (float*)(p.base[0] + off[0] + t0 * TT * 4 + tq * TT * sdq);
-    const char* yb = NIN >= 2 ? p.base[Y] + off[Y] + t0 * TT * p.str[Y][0] + tq * TT * p.str[Y][q]
-                              : nullptr;
-    float yimm = 0.0f;
-    if (NIN >= 2 && ymode == 0) yimm = to_f<TY>(from_bits<TY>(p.imm[Y].lo));
+    const int t0 = w % nt0, tq = w / nt0;
+    if (w + (int)gridDim.x < nwork) load(w + gridDim.x);
+    // phase 2: float4 columns -> destination
+    const int ig = threadIdx.x % 16;
+    char* db = ds + (int64_t)(t0 * TT + ig * 4) * 4 + (int64_t)(tq * TT) * sdq;
 #pragma unroll
     for (int pass = 0; pass < 4; ++pass) {
-      const int ig = threadIdx.x % 16, qq = threadIdx.x / 16 + 16 * pass;
-      float y[4];
-      if (NIN >= 2) {
-        if (ymode == 0) {
-          y[0] = y[1] = y[2] = y[3] = yimm;
-        } else if (ymode == 1) {
-          y[0] = to_f<TY>(__ldg((const TY*)(yb + qq * p.str[Y][q])));
-          y[1] = y[2] = y[3] = y[0];
-        } else {
+      const int j = threadIdx.x / 16 + 16 * pass;
+      const int swz = ((j / VX) * SWM) & 31;
+      float4 f = *(const float4*)&sm[j][(ig * 4) ^ swz];
+      if (NIN >= 2 && ymode == 2) {
+        const int64_t sy0 = p.str[Y][0];
+        const char* yb = ys + (int64_t)(t0 * TT + ig * 4) * sy0 + (int64_t)(tq * TT + j) * syq;
+        float y[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            y[u] = to_f<TY>(__ldg((const TY*)(yb + qq * p.str[Y][q] + (ig * 4 + u) * p.str[Y][0])));
+        for (int u = 0; u < 4; ++u) y[u] = to_f<TY>(__ldg((const TY*)(yb + u * sy0)));
+        if (XI == 1) {
+          f.x = fop<OP>(f.x, y[0]); f.y = fop<OP>(f.y, y[1]);
+          f.z = fop<OP>(f.z, y[2]); f.w = fop<OP>(f.w, y[3]);
+        } else {
+          f.x = fop<OP>(y[0], f.x); f.y = fop<OP>(y[1], f.y);
+          f.z = fop<OP>(y[2], f.z); f.w = fop<OP>(y[3], f.w);
         }
       }
-      float o[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float x = to_f<TX>(sm[qq][ig * 4 + u]);
-        if (NIN == 1) o[u] = x;
-        else o[u] = XI == 1 ? fop<OP>(x, y[u]) : fop<OP>(y[u], x);
-      }
-      __stcs((float4*)((char*)db + qq * sdq) + ig, make_float4(o[0], o[1], o[2], o[3]));
+      __stcs((float4*)(db + j * sdq), f);
     }
     __syncthreads();
   }
+}
+
+// resident blocks per SM of kernel K at 256 threads (queried once per K)
+template <auto K>
+int blocks_per_sm() {
+  static int cached = 0;
+  if (!cached) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, K, 256, 0) != cudaSuccess || n < 1) n = 4;
+    cached = n;
+  }
+  return cached;
+}
+
+// persistent launch of k_tile_f32: grid.x sized to the resident slots,
+// grid.y = index over the plan's remaining axes
+template <auto K>
+void launch_tile_f32(EwParams& p, Stream* st, int q, int64_t nt0, int64_t ntq, int64_t nrest,
+                     int ymode) {
+  const int64_t slots =
+      std::max<int64_t>(1, (int64_t)sm_count(st->device) * blocks_per_sm<K>() / nrest);
+  const dim3 grid((unsigned)std::min<int64_t>(nt0 * ntq, slots), (unsigned)nrest);
+  K<<<grid, 256, 0, st->s>>>(p, q, (int)nt0, (int)ntq, ymode);
 }
 
 // contig: 1-D unit-stride views, compile-time element sizes; 8 elements per
@@ -834,13 +897,16 @@ int launch_ew(EwParams& p, Stream* st) {
         const bool plain = !p.swap[0] && !p.swap[1] && !p.swap[2] && !p.track && !p.dry;
         if constexpr (DTD == TPG_FLOAT && f32_exact(DTA) && (NIN < 2 || f32_exact(DTB)) &&
                       ((OC == OC_BINARY && KIND == K_FLT) || OC == OC_COPY)) {
-          if (fast && plain) {
+          if (fast && plain && nrest <= 65535 && nt0 * ntq < (1 << 30)) {
             typedef typename Native<DTA>::T TA;
             typedef typename Native<(NIN >= 2 ? DTB : DTA)>::T TB;
-            if (NIN == 1) k_tile_native<0, 1, 1, TA, TA><<<g, 256, 0, st->s>>>(p, qa, nt0, ntq, nrest, 0);
-            else if (x == 1) k_tile_native<OP, 2, 1, TA, TB><<<g, 256, 0, st->s>>>(p, qa, nt0, ntq, nrest, ymode);
-            else k_tile_native<OP, 2, 2, TB, TA><<<g, 256, 0, st->s>>>(p, qa, nt0, ntq, nrest, ymode);
-            TPG_LAUNCH_CHECK("tile_native launch");
+            if (NIN == 1)
+              launch_tile_f32<k_tile_f32<0, 1, 1, TA, TA>>(p, st, qa, nt0, ntq, nrest, 0);
+            else if (x == 1)
+              launch_tile_f32<k_tile_f32<OP, 2, 1, TA, TB>>(p, st, qa, nt0, ntq, nrest, ymode);
+            else
+              launch_tile_f32<k_tile_f32<OP, 2, 2, TB, TA>>(p, st, qa, nt0, ntq, nrest, ymode);
+            TPG_LAUNCH_CHECK("tile_f32 launch");
             return TPG_OK;
           }
         }

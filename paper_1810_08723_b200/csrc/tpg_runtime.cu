@@ -309,6 +309,32 @@ int tpg_memset(void* dst, int value, size_t n, tpg_stream stream) {
   return TPG_OK;
 }
 
+// ---- L2 flush (measurement helper): write `n` bytes of scratch, then read
+// them back with default-priority loads, so the L2 is left holding clean
+// lines of an unrelated buffer (no dirty write-backs land in the next
+// kernel's timing).
+__global__ void k_l2_read(const uint4* a, size_t n, uint32_t* sink) {
+  uint32_t acc = 0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 v = __ldcg(a + i);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x9e3779b9u) *sink = acc;  // keeps the loads live
+}
+
+int tpg_l2_flush(void* scratch, size_t n, tpg_stream stream) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  if (n < 16) return TPG_OK;
+  static int salt = 0;
+  TPG_CUDA_CHECK(cudaMemsetAsync(scratch, ++salt & 0xff, n, st->s));
+  k_l2_read<<<sm_count(st->device) * 8, 256, 0, st->s>>>((const uint4*)scratch, n / 16 - 1,
+                                                          (uint32_t*)((char*)scratch + n - 16));
+  TPG_LAUNCH_CHECK("l2 flush");
+  return TPG_OK;
+}
+
 // ---- launch gate (measurement helper): hold a stream until the host has
 // enqueued a whole batch of timed steps, so host-side enqueue latency never
 // shows up between the CUDA events of a step.

@@ -1,0 +1,120 @@
+"""GPU parity of the transposing elementwise kernels (SURVEY cfg2 family):
+views whose fastest axis is not the destination's, at sizes that take the
+shared-memory tile paths (k_tile_f32 / k_tile_fast / k_tile), every table
+call shadow-checked bit-exactly against the C oracle on the same bytes.
+
+Covers: X as operand 1 or 2, Y immediate / broadcast row / unit-stride
+along axis 0 / transposed too, all six binary ops, int8..float sources,
+reversed axes, 3-D plans (remaining axes), ragged extents (not multiples of
+the 64 tile) and the cast-copy (NIN = 1) form."""
+
+import random
+
+import numpy as np
+import pytest
+
+import paper_1810_08723_b200 as tp
+from paper_1810_08723_b200 import dtypes as D
+from shadow import ShadowOracle
+
+pytestmark = pytest.mark.gpu
+
+SRC = [D.INT8, D.UINT8, D.INT16, D.UINT16, D.HALF, D.FLOAT]
+
+
+def _arr(rng, d, dims):
+    n = int(np.prod(dims))
+    if d.is_float:
+        v = rng.uniform(-300, 300, n)
+        sel = rng.random(n)
+        v[sel < 0.01] = np.nan
+        v[(sel > 0.01) & (sel < 0.02)] = -np.inf
+        v[(sel > 0.02) & (sel < 0.03)] = 0.0
+        return v.astype(D.NUMPY_NAME[d]).reshape(dims, order="F")
+    lo, hi = D.int_range(d)
+    return rng.integers(lo, hi, n, endpoint=True).astype(D.NUMPY_NAME[d]).reshape(dims, order="F")
+
+
+def _tview(rng, d, rows, cols, reverse=True):
+    """A (rows, cols) view whose axis 1 is the unit-stride one: transpose of
+    a column-major (cols, rows) base, optionally with axis 0 reversed."""
+    base = tp.from_numpy(np.asfortranarray(_arr(rng, d, (cols, rows))))
+    v = tp.transpose(base)
+    if reverse:
+        v = tp.apply_index(v, (slice(None, None, -1), slice(None)))
+    return v
+
+
+@pytest.mark.parametrize("d", SRC)
+def test_cfg2_shape_all_sources(d):
+    rng = np.random.default_rng(100 + SRC.index(d))
+    with ShadowOracle() as so:
+        v = _tview(rng, d, 256, 192)
+        row = tp.from_numpy(np.asfortranarray(_arr(rng, D.FLOAT, (1, 192))))
+        tp.add(v, row)               # X operand 1, Y broadcast row
+        tp.subtract(row, v)          # X operand 2
+        tp.cast(v, tp.float)         # NIN = 1 transposing cast-copy
+    assert so.calls >= 3
+    assert not so.failures, so.failures[:3]
+
+
+@pytest.mark.parametrize("op", ["add", "subtract", "multiply", "divide", "minimum", "maximum"])
+def test_ops_and_y_modes(op):
+    rng = np.random.default_rng(7)
+    fn = getattr(tp, op)
+    with ShadowOracle() as so:
+        v = _tview(rng, D.FLOAT, 128, 320)
+        row = tp.from_numpy(np.asfortranarray(_arr(rng, D.FLOAT, (1, 320))))
+        col = tp.from_numpy(np.asfortranarray(_arr(rng, D.FLOAT, (128, 320))))
+        fn(v, row)
+        fn(row, v)
+        fn(v, col)                   # Y unit stride along axis 0
+        fn(col, v)
+        fn(v, tp.Scalar(-1.5, tp.float))   # Y immediate
+        fn(tp.Scalar(0.0, tp.float), v)
+        vi = _tview(rng, D.INT16, 128, 320, reverse=False)
+        fn(vi, col)
+        fn(col, vi)
+    assert so.calls >= 8
+    assert not so.failures, so.failures[:3]
+
+
+def test_ragged_and_3d_plans():
+    rng, pr = np.random.default_rng(9), random.Random(9)
+    with ShadowOracle() as so:
+        for rows, cols in ((100, 64), (64, 70), (65, 129), (200, 48), (17, 300)):
+            v = _tview(rng, D.INT16, rows, cols, reverse=pr.random() < 0.5)
+            row = tp.from_numpy(np.asfortranarray(_arr(rng, D.FLOAT, (1, cols))))
+            tp.add(v, row)
+        # 3-D: (i, j, k) with j the source's unit axis, k a remaining axis
+        base = tp.from_numpy(np.asfortranarray(_arr(rng, D.INT16, (128, 64, 3))))
+        v3 = tp.permute_axes(base, (1, 0, 2))
+        r3 = tp.from_numpy(np.asfortranarray(_arr(rng, D.FLOAT, (1, 128, 3))))
+        tp.add(v3, r3)
+        tp.multiply(r3, v3)
+        tp.cast(v3, tp.float)
+        # transposed on both sides, byte-swapped and double sources take the
+        # general tile kernels
+        a = _tview(rng, D.DOUBLE, 128, 128)
+        b = _tview(rng, D.FLOAT, 128, 128, reverse=False)
+        tp.add(a, b)
+        s = _tview(rng, D.INT16, 128, 64)
+        tp.byteswap(s)
+        tp.add(s, tp.from_numpy(np.asfortranarray(_arr(rng, D.FLOAT, (1, 64)))))
+    assert so.calls >= 10
+    assert not so.failures, so.failures[:3]
+
+
+def test_cfg2_full_size_against_numpy():
+    """BASELINE cfg2 at full size (4096^2): int16 transposed reversed view +
+    float32 broadcast row, checked bit-exactly against the exact
+    double-compute-then-round result."""
+    n = 4096
+    rng = np.random.default_rng(3)
+    x16 = np.asfortranarray(rng.integers(-32768, 32767, (n, n), endpoint=True).astype(np.int16))
+    r = np.asfortranarray(rng.standard_normal((1, n)).astype(np.float32))
+    X, R = tp.from_numpy(x16), tp.from_numpy(r)
+    V = tp.apply_index(tp.transpose(X), (slice(None, None, -1), slice(None)))
+    got = tp.to_numpy(tp.add(V, R))
+    want = (x16.T[::-1, :].astype(np.float64) + r.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(got, want)

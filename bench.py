@@ -279,9 +279,13 @@ def bench_cfg2(tp, dev, steps, warmup, L):
     return ms, e2e_ms, wall, x16.nbytes + r.nbytes, N * N * 4
 
 
-def extras(tp, dev, L, warmup=3, steps=5):
-    """Kernel-level numbers for the other configs, rank 0."""
+def extras(tp, dev, L, warmup=3, steps=5, only=None):
+    """Kernel-level numbers for the other configs, rank 0.
+    `only`: optional set of config prefixes ("cfg1", "cfg3", ...)."""
     res = {}
+
+    def want(tag):
+        return only is None or tag in only
     stream = dev.default_stream()
     flush_buf = dev.allocate(FLUSH_BYTES)
 
@@ -301,21 +305,31 @@ def extras(tp, dev, L, warmup=3, steps=5):
             rec["TFLOP/s"] = round(flops / m / 1e9, 1)
         res[name] = rec
 
-    rng = np.random.default_rng(1)
-    a = tp.from_numpy(rng.standard_normal(1 << 20).astype(np.float32), dev)
-    b = tp.from_numpy(rng.standard_normal(1 << 20).astype(np.float32), dev)
-    o = tp.tensor_create((1 << 20,), tp.float, dev)
-    run("cfg1_add_f32_2^20", lambda: tp.add(a, b, dest=o), nbytes=12 << 20)
-    del a, b, o
+    if want("cfg1"):
+        rng = np.random.default_rng(1)
+        a = tp.from_numpy(rng.standard_normal(1 << 20).astype(np.float32), dev)
+        b = tp.from_numpy(rng.standard_normal(1 << 20).astype(np.float32), dev)
+        o = tp.tensor_create((1 << 20,), tp.float, dev)
+        run("cfg1_add_f32_2^20", lambda: tp.add(a, b, dest=o), nbytes=12 << 20)
+        del a, b, o
 
-    X = tp.from_numpy(np.asfortranarray(np.random.default_rng(5).random((8192, 8192))), dev)
-    nb = 8192 * 8192 * 8
-    for op in ("sum", "maximum", "norm"):
-        for axes, tag in (((0,), "axis0"), ((1,), "axis1"), (None, "full")):
-            run(f"cfg3_{op}_{tag}_f64_8192^2", lambda op=op, axes=axes: tp.reduce(op, X, axes=axes),
-                nbytes=nb)
-    del X
+    if want("cfg3"):
+        X = tp.from_numpy(np.asfortranarray(np.random.default_rng(5).random((8192, 8192))), dev)
+        nb = 8192 * 8192 * 8
+        for op in ("sum", "maximum", "norm"):
+            for axes, tag in (((0,), "axis0"), ((1,), "axis1"), (None, "full")):
+                run(f"cfg3_{op}_{tag}_f64_8192^2",
+                    lambda op=op, axes=axes: tp.reduce(op, X, axes=axes), nbytes=nb)
+        del X
+    if want("cfg5"):
+        cfg5(tp, dev, run)
+    if want("cfg4"):
+        cfg4(tp, dev, run)
+    dev.release(flush_buf, stream)
+    return res
 
+
+def cfg5(tp, dev, run):
     n5 = 1 << 28  # a quarter of cfg5's 2^30 per step keeps extras short
     s = np.random.default_rng(8).uniform(-1e3, 1e3, n5).astype(">f8")
     S = tp.from_numpy(s, dev)
@@ -332,6 +346,8 @@ def extras(tp, dev, L, warmup=3, steps=5):
     run("cfg5_cast_i16BE_to_f16_2^28", lambda: tp.copy(s16, h16), nbytes=4 * n5, fl=False)
     del s16, h16
 
+
+def cfg4(tp, dev, run):
     def gemm_operands(dt, m, k, n, batch=None):
         rng6 = np.random.default_rng(6)
         def mk(rows, cols):
@@ -362,8 +378,6 @@ def extras(tp, dev, L, warmup=3, steps=5):
     run("cfg4_gemm_batched_f16_64x2048^3", lambda: tp.matmul_batched(Ab, Bb, dest=Cb),
         flops=64 * 2 * 2048 ** 3, fl=False, st=3)
     del Ab, Bb, Cb
-    dev.release(flush_buf, stream)
-    return res
 
 
 def cpu_baseline(steps: int = 3):

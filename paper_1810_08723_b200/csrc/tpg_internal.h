@@ -12,7 +12,14 @@ namespace tpg {
 struct Stream {
   int device;
   cudaStream_t s;
+  // zeroed arrival counters for single-pass (last-block-finalises)
+  // reductions; every kernel that uses them leaves them zero again
+  uint32_t* counters = nullptr;
+  int64_t ncounters = 0;
 };
+
+// at least n zeroed counters, stream-ordered on st
+uint32_t* stream_counters(Stream* st, int64_t n);
 
 void set_error(const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);

@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(128) k_red_seq(RedParams p) {
 // semantics as the Acc machinery (it produces an Acc at the end), but the
 // per-element state is just the double-double pair or (best, index), with
 // NA independent accumulators per thread and U loads in flight.
-template <int OP>
+template <int OP, bool GENP = true>  // GENP = false: norm order 2 only
 struct FAcc {
   double hi, lo;  // sum / norm: double-double; min/max: hi = best value
   int64_t idx;    // min/max: index of best (-1 none)
@@ -497,7 +497,7 @@ struct FAcc {
       dd_add(hi, lo, v);
     } else if (OP == TPG_RNORM) {
       const double m = fabs(v);
-      dd_add(hi, lo, pp == 2.0 ? __dmul_rn(m, m) : pow(m, pp));
+      dd_add(hi, lo, (!GENP || pp == 2.0) ? __dmul_rn(m, m) : pow(m, pp));
     } else {
       if (isnan(v)) {
         if (j == 0 && pp >= 0.0) { fnan = true; nanv = v; }
@@ -648,6 +648,475 @@ __global__ void __launch_bounds__(256, 4) k_red_cols_flt(RedParams p, int64_t no
   if (st) atomicOr(p.flags, st);
 }
 
+// ---------------------------------------------------------------------------
+// Vectorised single-pass float reductions (SURVEY cfg3: f64 / f32 sum, norm,
+// min, max).  16-byte loads (2 x f64 / 4 x f32) with a software pipeline
+// that keeps 2 x U vectors in flight per thread, and no separate finalize
+// launch: the worker that completes the last chunk of an output (arrival
+// counter + threadfence) combines that output's partials in chunk order,
+// so the result does not depend on which worker arrives last.  Counters come
+// from the stream (stream_counters) and are left zero again.
+//
+// Partials are 16 bytes (Part): sum / norm keep the double-double pair;
+// min / max keep (value, index) with index -1 = no element and -2 = "the
+// first element of the range is NaN" (value = that NaN), which makes the
+// result NaN whatever the other chunks hold (ops.py:527-544).
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<double> {
+  double x[2];
+  static constexpr int n = 2;
+};
+template <>
+struct Vec16<float> {
+  float x[4];
+  static constexpr int n = 4;
+};
+
+template <typename T>
+__device__ __forceinline__ Vec16<T> ld_vec(const char* ptr);
+template <>
+__device__ __forceinline__ Vec16<double> ld_vec<double>(const char* ptr) {
+  Vec16<double> v;
+  asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x[0]), "=d"(v.x[1]) : "l"(ptr));
+  return v;
+}
+template <>
+__device__ __forceinline__ Vec16<float> ld_vec<float>(const char* ptr) {
+  Vec16<float> v;
+  asm volatile("ld.global.cs.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x[0]), "=f"(v.x[1]), "=f"(v.x[2]), "=f"(v.x[3])
+               : "l"(ptr));
+  return v;
+}
+
+struct __align__(16) Part {
+  double hi, lo;
+};
+
+template <int OP>
+__device__ __forceinline__ Part to_part(const FAcc<OP, false>& a) {
+  Part r;
+  if (OP == TPG_RSUM || OP == TPG_RNORM) {
+    r.hi = a.hi;
+    r.lo = a.lo;
+  } else if (a.fnan) {
+    r.hi = a.nanv;
+    r.lo = __longlong_as_double(-2ll);
+  } else {
+    r.hi = a.hi;
+    r.lo = __longlong_as_double(a.idx);
+  }
+  return r;
+}
+__device__ __forceinline__ Part part_ident() {
+  Part r;
+  r.hi = 0.0;
+  r.lo = 0.0;  // for min/max the caller uses index -1 (see part_none)
+  return r;
+}
+template <int OP>
+__device__ __forceinline__ Part part_none() {
+  Part r;
+  r.hi = 0.0;
+  r.lo = (OP == TPG_RSUM || OP == TPG_RNORM) ? 0.0 : __longlong_as_double(-1ll);
+  return r;
+}
+// x covers earlier elements than y
+template <int OP>
+__device__ __forceinline__ Part part_comb(Part x, const Part& y) {
+  if (OP == TPG_RSUM || OP == TPG_RNORM) {
+    dd_merge(x.hi, x.lo, y.hi, y.lo);
+    return x;
+  }
+  const long long ix = __double_as_longlong(x.lo), iy = __double_as_longlong(y.lo);
+  if (ix == -2) return x;
+  if (iy == -2) return y;
+  if (iy < 0) return x;
+  if (ix < 0) return y;
+  const bool take = OP == TPG_RMIN ? (y.hi < x.hi || (y.hi == x.hi && iy < ix))
+                                   : (y.hi > x.hi || (y.hi == x.hi && iy < ix));
+  return take ? y : x;
+}
+template <int OP>
+__device__ __forceinline__ Acc part_acc(const Part& x) {
+  Acc a = acc_init<OP, K_FLT>();
+  if (OP == TPG_RSUM || OP == TPG_RNORM) {
+    a.a = x.hi;
+    a.b = x.lo;
+  } else {
+    const long long ix = __double_as_longlong(x.lo);
+    if (ix == -2) {
+      a.b = 1.0;
+      a.d = x.hi;
+    } else {
+      a.a = x.hi;
+      a.i = ix;
+    }
+  }
+  return a;
+}
+__device__ __forceinline__ Part ld_part(const Part* p) {
+  const double2 v = __ldcg((const double2*)p);
+  Part r;
+  r.hi = v.x;
+  r.lo = v.y;
+  return r;
+}
+__device__ __forceinline__ void st_part(Part* p, const Part& v) {
+  __stcg((double2*)p, make_double2(v.hi, v.lo));
+}
+// lane-order combine (lanes hold consecutive ranges); result in lane 0
+template <int OP>
+__device__ __forceinline__ Part warp_part(Part x) {
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    Part y;
+    y.hi = __shfl_down_sync(0xffffffffu, x.hi, s);
+    y.lo = __shfl_down_sync(0xffffffffu, x.lo, s);
+    const int lane = threadIdx.x & 31;
+    if ((lane & (2 * s - 1)) == 0 && lane + s < 32) x = part_comb<OP>(x, y);
+  }
+  return x;
+}
+// thread-order combine over the block; result in thread 0
+template <int OP, int NT>
+__device__ __forceinline__ Part block_part(Part t, Part* sh) {
+  t = warp_part<OP>(t);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) sh[warp] = t;
+  __syncthreads();
+  Part a = sh[0];
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 1; k < NT / 32; ++k) a = part_comb<OP>(a, sh[k]);
+  return a;
+}
+
+// Stream one unit-stride range [j0, j1) of T (base = element 0 of the
+// plan's inner range) through NL lanes (lane index li): scalar head up to
+// 16-byte alignment, pipelined 16-byte body, scalar tail.  Folds into x[NA]
+// (a lane's feeds reach each accumulator in increasing element order).
+template <int OP, typename T, int NL, int NA, int U>
+__device__ __forceinline__ void stream_range(FAcc<OP, false> (&x)[NA], const char* base, int64_t j0,
+                                             int64_t j1, int li, double pp) {
+  constexpr int VE = Vec16<T>::n;
+  const uintptr_t a0 = (uintptr_t)(base + j0 * (int64_t)sizeof(T));
+  int64_t ja = j0 + (int64_t)(((16 - (a0 & 15)) & 15) / sizeof(T));
+  if (ja > j1) ja = j1;
+  if (j0 + li < ja) x[0].feed(ld_real<T>(base + (j0 + li) * (int64_t)sizeof(T)), j0 + li, pp);
+  const int64_t nv = (j1 - ja) / VE;
+  const char* vb = base + ja * (int64_t)sizeof(T);
+  const int64_t nfull = nv / (NL * U);
+  int64_t vi = li;
+  if (nfull > 0) {
+    Vec16<T> v[U], nvv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld_vec<T>(vb + (vi + u * NL) * 16);
+    for (int64_t k = 0; k < nfull; ++k) {
+      if (k + 1 < nfull) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) nvv[u] = ld_vec<T>(vb + (vi + (U + u) * NL) * 16);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = ja + (vi + u * NL) * VE;
+#pragma unroll
+        for (int e = 0; e < VE; ++e) x[u % NA].feed((double)v[u].x[e], j + e, pp);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = nvv[u];
+      vi += NL * U;
+    }
+  }
+  for (; vi < nv; vi += NL) {
+    const Vec16<T> v = ld_vec<T>(vb + vi * 16);
+    const int64_t j = ja + vi * VE;
+#pragma unroll
+    for (int e = 0; e < VE; ++e) x[0].feed((double)v.x[e], j + e, pp);
+  }
+  const int64_t jt = ja + nv * VE + li;
+  if (jt < j1) x[0].feed(ld_real<T>(base + jt * (int64_t)sizeof(T)), jt, pp);
+}
+
+template <int OP, int NA>
+__device__ __forceinline__ Part fold_accs(FAcc<OP, false> (&x)[NA]) {
+  Part t = to_part<OP>(x[0]);
+#pragma unroll
+  for (int a = 1; a < NA; ++a) t = part_comb<OP>(t, to_part<OP>(x[a]));
+  return t;
+}
+
+// Row mode, warp granularity: one warp per (output, chunk) work item (many
+// outputs, e.g. cfg3 axis 0).  Warps never synchronise with each other, so
+// one warp's drain overlaps the others' streaming.
+template <int OP, typename T>
+__global__ void __launch_bounds__(256, 3) k_red_rows_wv(RedParams p, Part* ws, uint32_t* cnt) {
+  constexpr int U = 4, NA = 2;
+  uint32_t st = 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nwork = p.O * p.C;
+  for (int64_t w = gw; w < nwork; w += nw) {
+    const int64_t o = w / p.C, c = w - o * p.C;
+    int64_t doff, soff;
+    outer_offsets(p, o, doff, soff);
+    const int64_t j0 = c * p.chunk;
+    const int64_t j1 = min(p.N, j0 + p.chunk);
+    FAcc<OP, false> x[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) x[a].init();
+    stream_range<OP, T, 32, NA, U>(x, p.sbase + soff, j0, j1, lane, p.p);
+    const Part r = warp_part<OP>(fold_accs<OP, NA>(x));
+    if (p.C == 1) {
+      if (lane == 0) acc_store<OP, K_FLT>(p, part_acc<OP>(r), doff, st);
+      continue;
+    }
+    uint32_t last = 0;
+    if (lane == 0) {
+      st_part(&ws[o * p.C + c], r);
+      __threadfence();
+      last = atomicAdd(&cnt[o], 1u) == (uint32_t)(p.C - 1);
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence();
+      // lane l combines chunks [l*per, (l+1)*per), then lane order
+      const int64_t per = (p.C + 31) / 32;
+      Part y = part_none<OP>();
+      for (int64_t cc = lane * per; cc < min(p.C, (lane + 1) * per); ++cc)
+        y = part_comb<OP>(y, ld_part(&ws[o * p.C + cc]));
+      y = warp_part<OP>(y);
+      if (lane == 0) {
+        acc_store<OP, K_FLT>(p, part_acc<OP>(y), doff, st);
+        cnt[o] = 0;
+      }
+    }
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+// Row mode, block granularity: one block per (output, chunk) (few outputs,
+// e.g. full reductions).
+template <int OP, typename T>
+__global__ void __launch_bounds__(256, 3) k_red_rows_v(RedParams p, Part* ws, uint32_t* cnt) {
+  constexpr int U = 4, NA = 2, NT = 256;
+  __shared__ Part sh[NT / 32];
+  __shared__ int is_last;
+  uint32_t st = 0;
+  const int tid = threadIdx.x;
+  const int64_t nwork = p.O * p.C;
+  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int64_t o = w / p.C, c = w - o * p.C;
+    int64_t doff, soff;
+    outer_offsets(p, o, doff, soff);
+    const int64_t j0 = c * p.chunk;
+    const int64_t j1 = min(p.N, j0 + p.chunk);
+    FAcc<OP, false> x[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) x[a].init();
+    stream_range<OP, T, NT, NA, U>(x, p.sbase + soff, j0, j1, tid, p.p);
+    const Part r = block_part<OP, NT>(fold_accs<OP, NA>(x), sh);
+    if (p.C == 1) {
+      if (tid == 0) acc_store<OP, K_FLT>(p, part_acc<OP>(r), doff, st);
+      continue;
+    }
+    if (tid == 0) {
+      st_part(&ws[o * p.C + c], r);
+      __threadfence();
+      is_last = atomicAdd(&cnt[o], 1u) == (uint32_t)(p.C - 1);
+    }
+    __syncthreads();
+    if (is_last) {
+      __threadfence();
+      const int64_t per = (p.C + NT - 1) / NT;
+      Part y = part_none<OP>();
+      for (int64_t cc = tid * per; cc < min(p.C, (tid + 1) * per); ++cc)
+        y = part_comb<OP>(y, ld_part(&ws[o * p.C + cc]));
+      const Part z = block_part<OP, NT>(y, sh);
+      if (tid == 0) {
+        acc_store<OP, K_FLT>(p, part_acc<OP>(z), doff, st);
+        cnt[o] = 0;
+      }
+    }
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+// Column mode: outputs adjacent in the source (outer axis 0 unit-stride),
+// reduced axis strided (cfg3 axis 1).  Each thread owns VE adjacent outputs
+// and reads one 16-byte vector per row; a block covers NT*VE outputs x one
+// row chunk.  Partials are chunk-major (ws[c * O + o]) so the finalizing
+// block reads them coalesced, 8 chunks in flight per thread.
+template <int OP, typename T>
+__global__ void __launch_bounds__(128, 6) k_red_cols_v(RedParams p, int64_t nob, Part* ws,
+                                                       uint32_t* cnt) {
+  constexpr int VE = Vec16<T>::n, U = 4, NT = 128;
+  __shared__ int is_last;
+  uint32_t st = 0;
+  const int tid = threadIdx.x;
+  const int64_t nwork = nob * p.C;
+  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int64_t ob = w % nob, c = w / nob;
+    const int64_t o = (ob * NT + tid) * VE;
+    const bool act = o < p.O;
+    int64_t doff = 0, soff = 0;
+    if (act) outer_offsets(p, o, doff, soff);
+    const int64_t j0 = c * p.chunk;
+    const int64_t j1 = min(p.N, j0 + p.chunk);
+    if (act) {
+      FAcc<OP, false> x[VE];
+#pragma unroll
+      for (int e = 0; e < VE; ++e) x[e].init();
+      const int64_t s0 = p.si[0];
+      const char* ptr = p.sbase + soff + j0 * s0;
+      int64_t jb = j0;
+      const int64_t nfull = (j1 - j0) / U;
+      if (nfull > 0) {
+        Vec16<T> v[U], nvv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ld_vec<T>(ptr + u * s0);
+        for (int64_t k = 0; k < nfull; ++k) {
+          if (k + 1 < nfull) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) nvv[u] = ld_vec<T>(ptr + (U + u) * s0);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int e = 0; e < VE; ++e) x[e].feed((double)v[u].x[e], jb + u, p.p);
+#pragma unroll
+          for (int u = 0; u < U; ++u) v[u] = nvv[u];
+          jb += U;
+          ptr += U * s0;
+        }
+      }
+      for (; jb < j1; ++jb, ptr += s0) {
+        const Vec16<T> v = ld_vec<T>(ptr);
+#pragma unroll
+        for (int e = 0; e < VE; ++e) x[e].feed((double)v.x[e], jb, p.p);
+      }
+#pragma unroll
+      for (int e = 0; e < VE; ++e) {
+        const Part t = to_part<OP>(x[e]);
+        if (p.C == 1) acc_store<OP, K_FLT>(p, part_acc<OP>(t), doff + e * p.so_d[0], st);
+        else st_part(&ws[c * p.O + o + e], t);
+      }
+    }
+    if (p.C == 1) continue;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) is_last = atomicAdd(&cnt[ob], 1u) == (uint32_t)(p.C - 1);
+    __syncthreads();
+    if (is_last) {
+      __threadfence();
+      if (act) {
+#pragma unroll 1
+        for (int e = 0; e < VE; ++e) {
+          Part y = part_none<OP>();
+          for (int64_t c0 = 0; c0 < p.C; c0 += 8) {
+            Part q[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              q[u] = c0 + u < p.C ? ld_part(&ws[(c0 + u) * p.O + o + e]) : part_none<OP>();
+#pragma unroll
+            for (int u = 0; u < 8; ++u) y = part_comb<OP>(y, q[u]);
+          }
+          acc_store<OP, K_FLT>(p, part_acc<OP>(y), doff + e * p.so_d[0], st);
+        }
+      }
+      if (tid == 0) cnt[ob] = 0;
+    }
+    __syncthreads();
+  }
+  if (st) atomicOr(p.flags, st);
+}
+
+// eligibility of the vector kernels (else the scalar float kernels run)
+template <typename T>
+bool rows_vec_ok(const RedParams& p) {
+  return p.ndi == 1 && p.si[0] == (int64_t)sizeof(T);
+}
+template <typename T>
+bool cols_vec_ok(const RedParams& p) {
+  constexpr int VE = Vec16<T>::n;
+  if (p.ndi != 1 || p.ndo < 1 || p.so_s[0] != (int64_t)sizeof(T) || p.eo[0] % VE) return false;
+  if ((uintptr_t)p.sbase % 16 || p.si[0] % 16) return false;
+  for (int k = 1; k < p.ndo; ++k)
+    if (p.eo[k] > 1 && p.so_s[k] % 16) return false;
+  return true;
+}
+
+// Work split + launch of the vector kernels; done = false when the layout
+// is not eligible (the caller then runs the scalar kernels).
+template <int OP, typename T>
+int launch_vec(RedParams& p, Stream* st, bool col, bool& done) {
+  done = false;
+  if (OP == TPG_RNORM && p.p != 2.0) return TPG_OK;
+  const int64_t sms = sm_count(st->device);
+  Part* ws = nullptr;
+  uint32_t* cnt = nullptr;
+  auto scratch = [&](int64_t nparts, int64_t ncnt) -> int {
+    if (p.C <= 1) return TPG_OK;
+    cnt = stream_counters(st, ncnt);
+    if (!cnt) return arg_fail("reduce: counter allocation failed");
+    TPG_CUDA_CHECK(cudaMallocAsync((void**)&ws, sizeof(Part) * nparts, st->s));
+    return TPG_OK;
+  };
+  if (col) {
+    if (!cols_vec_ok<T>(p)) return TPG_OK;
+    constexpr int VE = Vec16<T>::n, NT = 128;
+    const int64_t nob = (p.O + NT * VE - 1) / (NT * VE);
+    const int64_t target = sms * 6 * 2;  // two waves of resident blocks
+    int64_t C = (target + nob - 1) / nob;
+    if (C > p.N / 32) C = p.N / 32;
+    if (C > 64) C = 64;
+    if (C < 1) C = 1;
+    p.chunk = (p.N + C - 1) / C;
+    p.C = (p.N + p.chunk - 1) / p.chunk;
+    if (int rc = scratch(p.O * p.C, nob)) return rc;
+    const int64_t work = nob * p.C;
+    k_red_cols_v<OP, T><<<(int)std::min<int64_t>(work, 1 << 30), NT, 0, st->s>>>(p, nob, ws, cnt);
+  } else {
+    if (!rows_vec_ok<T>(p)) return TPG_OK;
+    const int64_t wslots = sms * 3 * 8;  // resident warps
+    if (p.O >= wslots / 2) {
+      // warp items: enough outputs to fill the machine; split each output
+      // only as far as needed for about two warp items per slot
+      int64_t C = (2 * wslots + p.O - 1) / p.O;
+      const int64_t minchunk = 2048;
+      if (C > (p.N + minchunk - 1) / minchunk) C = (p.N + minchunk - 1) / minchunk;
+      if (C > 32) C = 32;
+      if (C < 1) C = 1;
+      p.chunk = (p.N + C - 1) / C;
+      p.chunk = (p.chunk + 7) & ~(int64_t)7;
+      p.C = (p.N + p.chunk - 1) / p.chunk;
+      if (int rc = scratch(p.O * p.C, p.O)) return rc;
+      const int64_t warps = std::min<int64_t>(p.O * p.C, wslots);
+      k_red_rows_wv<OP, T><<<(int)((warps + 7) / 8), 256, 0, st->s>>>(p, ws, cnt);
+    } else {
+      const int64_t target = sms * 3 * 2;  // two waves of resident blocks
+      int64_t C = (target + p.O - 1) / p.O;
+      const int64_t minchunk = 16384;
+      if (C > (p.N + minchunk - 1) / minchunk) C = (p.N + minchunk - 1) / minchunk;
+      if (C < 1) C = 1;
+      p.chunk = (p.N + C - 1) / C;
+      p.chunk = (p.chunk + 7) & ~(int64_t)7;  // chunk starts stay 16-B aligned
+      p.C = (p.N + p.chunk - 1) / p.chunk;
+      if (int rc = scratch(p.O * p.C, p.O)) return rc;
+      const int64_t work = p.O * p.C;
+      k_red_rows_v<OP, T><<<(int)std::min<int64_t>(work, 1 << 30), 256, 0, st->s>>>(p, ws, cnt);
+    }
+  }
+  TPG_LAUNCH_CHECK("reduce vec");
+  if (ws) TPG_CUDA_CHECK(cudaFreeAsync(ws, st->s));
+  done = true;
+  return TPG_OK;
+}
+
 template <int OP, typename T>
 void launch_flt(RedParams& p, Stream* st, bool col) {
   if (col) {
@@ -692,6 +1161,15 @@ int launch_red(RedParams& p, Stream* st, bool col) {
     k_red_seq<OP, KIND><<<g, 128, 0, st->s>>>(p);
     TPG_LAUNCH_CHECK("reduce seq");
     return TPG_OK;
+  }
+  if constexpr (KIND == K_FLT && (OP == TPG_RSUM || OP == TPG_RNORM || OP == TPG_RMIN ||
+                                  OP == TPG_RMAX)) {
+    if (!p.sswap && p.saligned && (p.sdt == TPG_DOUBLE || p.sdt == TPG_FLOAT)) {
+      bool done = false;
+      const int rc = p.sdt == TPG_DOUBLE ? launch_vec<OP, double>(p, st, col, done)
+                                         : launch_vec<OP, float>(p, st, col, done);
+      if (rc != TPG_OK || done) return rc;
+    }
   }
   const int64_t target = (int64_t)sm_count(dev) * 8;
   if (col) {

@@ -95,6 +95,21 @@ uint32_t* device_flags(int device) {
   return g_flags[device];
 }
 
+uint32_t* stream_counters(Stream* st, int64_t n) {
+  if (n <= st->ncounters) return st->counters;
+  int64_t cap = st->ncounters ? st->ncounters : 4096;
+  while (cap < n) cap *= 2;
+  if (st->counters && cudaFreeAsync(st->counters, st->s) != cudaSuccess) return nullptr;
+  st->counters = nullptr;
+  st->ncounters = 0;
+  uint32_t* c = nullptr;
+  if (cudaMallocAsync((void**)&c, cap * sizeof(uint32_t), st->s) != cudaSuccess) return nullptr;
+  if (cudaMemsetAsync(c, 0, cap * sizeof(uint32_t), st->s) != cudaSuccess) return nullptr;
+  st->counters = c;
+  st->ncounters = cap;
+  return c;
+}
+
 }  // namespace tpg
 
 using namespace tpg;
@@ -212,6 +227,7 @@ int tpg_stream_destroy(tpg_stream stream) {
   for (Stream* d : g_default)
     if (d == st) return arg_fail("cannot destroy a default stream");
   TPG_CUDA_CHECK(cudaSetDevice(st->device));
+  if (st->counters) TPG_CUDA_CHECK(cudaFreeAsync(st->counters, st->s));
   TPG_CUDA_CHECK(cudaStreamDestroy(st->s));
   delete st;
   return TPG_OK;

@@ -363,7 +363,7 @@ def cfg4(tp, dev, run):
     # SURVEY cfg4: A = transpose of a column-major base (K-major), B
     # column-major, C column-major; 2*8192^3 flop per step
     for dname, dt, m in (("f16", tp.half, 8192), ("bf16", tp.bfloat16, 8192),
-                         ("f32", tp.float, 4096)):
+                         ("f32", tp.float, 8192)):
         mk, _ = gemm_operands(dt, m, m, m)
         At = tp.transpose(mk(m, m))
         B = mk(m, m)

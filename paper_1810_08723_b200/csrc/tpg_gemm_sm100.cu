@@ -1,27 +1,32 @@
-// tpg_gemm_sm100.cu — tcgen05 / TMEM / TMA tensor-core gemm for half and
-// bfloat16 operands (fp32 accumulation in tensor memory).
+// tpg_gemm_sm100.cu — tcgen05 / TMEM / TMA tensor-core gemm.
 //
 // Serves the matmul table entry (reference kernels.matmul,
 // pkg/src/tidepool/kernels.py:323-340; ops.matmul ops.py:577-640) and the
-// batched extension when both operands are half (or both bfloat16) and the
-// destination is half / bfloat16 / float.  Contract vs the reference: the
-// reference sums exact double products with Neumaier compensation and
-// rounds once; here products are exact in fp32 and accumulate in fp32 in
-// TMEM, then round once to the destination (parity tolerance 1e-2 rel to
-// sum|a||b| for f16/bf16).  A non-finite accumulator becomes
+// batched extension for
+//   * half x half / bfloat16 x bfloat16 (MODE 0, kind::f16), and
+//   * float x float (MODE 1, kind::tf32, "3xTF32": every operand is split
+//     exactly into hi = tf32(x) and lo = x - hi, and C accumulates
+//     hi*hi + hi*lo + lo*hi in fp32 in TMEM, ~2^-21 relative per product),
+// with a half / bfloat16 / float destination.  Contract vs the reference:
+// the reference sums exact double products with Neumaier compensation and
+// rounds once; here accumulation is fp32 in TMEM, then one rounding to the
+// destination (parity tolerance, SURVEY §8a-A5 / north_star: 1e-2 of
+// sum|a||b| for f16/bf16, 1e-5 for f32).  A non-finite accumulator becomes
 // NaN, as the reference's compensated sum does.
 //
 // Kernel shape (persistent: one CTA per SM loops over output tiles in a
-// grouped raster; 192 threads; two 128x256 fp32 accumulators in TMEM so
-// the epilogue of one tile overlaps the mainloop of the next):
-//   warp 0 lane 0   TMA producer: A tile 128x64 and B tile 256x64 (K-major,
-//                   128B swizzle) per stage, 4-stage mbarrier ring
-//   warp 1 lane 0   MMA issuer: 4 x tcgen05.mma.cta_group::1.kind::f16
-//                   (M128 N256 K16) per stage, tcgen05.commit frees the stage
-//   warps 2..5      epilogue: tcgen05.ld 32x32b.x32 -> registers -> convert
-//                   -> global (coalesced along M for column-major C)
-// Operands that are not K-major (or are byte-swapped / misaligned) are
-// first packed into a K-major scratch copy by the elementwise engine.
+// grouped raster; 192 threads; two accumulators in TMEM so the epilogue of
+// one tile overlaps the mainloop of the next):
+//   warp 0 lane 0   TMA producer, STAGES-deep mbarrier ring
+//   warp 1 lane 0   MMA issuer (tcgen05.mma.cta_group::1), tcgen05.commit
+//                   releases a stage / publishes an accumulator
+//   warps 2..5      epilogue: tcgen05.ld 32x32b.x32 -> convert -> global
+// Operand layouts (half / bfloat16): an operand whose unit-stride axis is K
+// is loaded K-major, one whose unit-stride axis is M (A) or N (B) MN-major
+// (no pack, e.g. column-major batched A); both with 128-byte swizzle.
+// Anything else (byte-swapped, misaligned, no unit stride) is packed
+// K-major first.  float operands always pass through the 3xTF32 split,
+// which writes K-major hi / lo copies.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -33,14 +38,24 @@
 
 namespace tpg {
 
-constexpr int GBM = 128, GBN = 256, GBK = 64, GSTAGES = 4;
-constexpr int A_STAGE_BYTES = GBM * GBK * 2;
-constexpr int B_STAGE_BYTES = GBN * GBK * 2;
-constexpr int TMEM_COLS = 256;
+template <int MODE>
+struct Cfg {
+  static constexpr int ESZ = MODE ? 4 : 2;          // operand element bytes
+  static constexpr int BM = 128;
+  static constexpr int BN = MODE ? 128 : 256;
+  static constexpr int BK = 128 / ESZ;              // one 128-B swizzle row
+  static constexpr int STAGES = MODE ? 3 : 4;
+  static constexpr int NPART = MODE ? 2 : 1;        // hi (+ lo)
+  static constexpr int KI = MODE ? 8 : 16;          // K per MMA instruction
+  static constexpr int A_BYTES = BM * BK * ESZ;     // 16 KiB
+  static constexpr int B_BYTES = BN * BK * ESZ;
+  static constexpr int STAGE_BYTES = NPART * (A_BYTES + B_BYTES);
+  static constexpr int TMEM_COLS = BN;              // per accumulator
+  static constexpr size_t SMEM =
+      1024 + (size_t)STAGES * STAGE_BYTES + 4 * 4096 + 8 * (2 * STAGES + 4) + 16;
+};
 constexpr int GEMM_THREADS = 192;
 constexpr int GROUP_M = 16;
-constexpr size_t GEMM_SMEM =
-    1024 + (size_t)GSTAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 4 * 4096 + 8 * (2 * GSTAGES + 4) + 16;
 
 struct Sm100Args {
   char* d;
@@ -49,6 +64,7 @@ struct Sm100Args {
   int ddt;
   int epi;  // 0 generic, 1 column-major (M contiguous), 2 row-major (N contiguous)
   int tiles_m, tiles_n;
+  int amn, bmn;  // operand is MN-major in global memory / shared memory
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -83,25 +99,37 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-// UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row groups 1024 B
-// apart (SBO), version 1 (sm_100).
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+// UMMA shared-memory descriptor, 128B swizzle, version 1 (sm_100).
+//   K-major : rows of 128 B (one K block), 8-row groups 1024 B apart (SBO);
+//             LBO unused.
+//   MN-major: 128 B of M (or N) per K row, K rows 128 B apart in 8-row
+//             groups 1024 B apart (SBO); consecutive 128-B MN atoms LBO
+//             bytes apart (one TMA box = BK rows).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)1 << 16;             // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)(1024 >> 4) << 32;   // SBO
   d |= (uint64_t)1 << 46;             // descriptor version (Blackwell)
   d |= (uint64_t)2 << 61;             // SWIZZLE_128B
   return d;
 }
 
-__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+template <int MODE>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                     uint32_t idesc, uint32_t accumulate) {
+  if constexpr (MODE == 0)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -148,27 +176,46 @@ __device__ __forceinline__ void tile_coords(int t, const Sm100Args& g, int& m_ti
   n_tile = r / gm;
 }
 
+// load one operand tile (ROWS x BK) of part `map` into smem at dst:
+// K-major = one box {BK, ROWS}; MN-major = ROWS*ESZ/128 boxes {128/ESZ, BK}
+template <int MODE, int ROWS>
+__device__ __forceinline__ void load_operand(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                             int kb, int row0, int batch, bool mn) {
+  using G = Cfg<MODE>;
+  if (!mn) {
+    tma_load_3d(dst, map, bar, kb * G::BK, row0, batch);
+  } else {
+    constexpr int ATOM = 128 / G::ESZ;
+#pragma unroll
+    for (int a = 0; a < ROWS / ATOM; ++a)
+      tma_load_3d(dst + a * (G::BK * 128), map, bar, row0 + a * ATOM, kb * G::BK, batch);
+  }
+}
+
 // Persistent: one CTA per SM loops over output tiles.  Two TMEM
-// accumulators (2 x 256 columns) let the epilogue of tile i overlap the
-// mainloop of tile i+1 (tfull/tempty mbarrier pair per accumulator).
+// accumulators let the epilogue of tile i overlap the mainloop of tile i+1
+// (tfull/tempty mbarrier pair per accumulator).
+template <int MODE>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm_sm100(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                 const __grid_constant__ CUtensorMap tma_al, const __grid_constant__ CUtensorMap tma_bl,
                  Sm100Args g, uint32_t idesc, int ntiles) {
+  using G = Cfg<MODE>;
+  constexpr int BM = G::BM, BN = G::BN, BK = G::BK, STAGES = G::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* As = smem;
-  uint8_t* Bs = smem + GSTAGES * A_STAGE_BYTES;
-  uint8_t* epi_stage = Bs + GSTAGES * B_STAGE_BYTES;  // 4 warps x 4 KB
+  // stage s: [A hi][B hi]([A lo][B lo])
+  uint8_t* epi_stage = smem + STAGES * G::STAGE_BYTES;  // 4 warps x 4 KB
   uint64_t* bars = (uint64_t*)(epi_stage + 4 * 4096);
   uint64_t* full = bars;
-  uint64_t* empty = bars + GSTAGES;
-  uint64_t* tfull = bars + 2 * GSTAGES;       // [2]
-  uint64_t* tempty = bars + 2 * GSTAGES + 2;  // [2]
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * GSTAGES + 4);
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;       // [2]
+  uint64_t* tempty = bars + 2 * STAGES + 2;  // [2]
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < GSTAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(su32(&full[s]), 1);
       mbar_init(su32(&empty[s]), 1);
     }
@@ -179,18 +226,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_b) : "memory");
+    if (MODE) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_al) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_bl) : "memory");
+    }
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(tmem_slot)),
-                 "r"(2 * TMEM_COLS));
+                 "r"(2 * G::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const int nk = (g.k + GBK - 1) / GBK;
+  const int nk = (g.k + BK - 1) / BK;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -199,35 +250,60 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         int m_tile, n_tile, batch;
         tile_coords(t, g, m_tile, n_tile, batch);
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % GSTAGES;
-          const uint32_t ph = (it / GSTAGES) & 1;
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(su32(&empty[s]), ph ^ 1);
-          mbar_expect_tx(su32(&full[s]), A_STAGE_BYTES + B_STAGE_BYTES);
-          tma_load_3d(su32(As + s * A_STAGE_BYTES), &tma_a, su32(&full[s]), kb * GBK,
-                      m_tile * GBM, batch);
-          tma_load_3d(su32(Bs + s * B_STAGE_BYTES), &tma_b, su32(&full[s]), kb * GBK,
-                      n_tile * GBN, batch);
+          mbar_expect_tx(su32(&full[s]), G::STAGE_BYTES);
+          const uint32_t st0 = su32(smem + s * G::STAGE_BYTES);
+          load_operand<MODE, BM>(st0, &tma_a, su32(&full[s]), kb, m_tile * BM, batch, g.amn);
+          load_operand<MODE, BN>(st0 + G::A_BYTES, &tma_b, su32(&full[s]), kb, n_tile * BN, batch,
+                                 g.bmn);
+          if (MODE) {
+            const uint32_t st1 = st0 + G::A_BYTES + G::B_BYTES;
+            load_operand<MODE, BM>(st1, &tma_al, su32(&full[s]), kb, m_tile * BM, batch, g.amn);
+            load_operand<MODE, BN>(st1 + G::A_BYTES, &tma_bl, su32(&full[s]), kb, n_tile * BN,
+                                   batch, g.bmn);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
+      // per-instruction K advance inside a stage: K-major +KI*ESZ bytes
+      // along the swizzled row; MN-major +KI rows of 128 B
+      const uint32_t adv_a = g.amn ? G::KI * 128 : G::KI * G::ESZ;
+      const uint32_t adv_b = g.bmn ? G::KI * 128 : G::KI * G::ESZ;
+      const uint32_t lbo_a = g.amn ? BK * 128 : 16, lbo_b = g.bmn ? BK * 128 : 16;
       uint32_t it = 0, lt = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
         const uint32_t b = lt & 1, use = lt >> 1;
         mbar_wait(su32(&tempty[b]), (use & 1) ^ 1);  // accumulator drained
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t acc = tmem + b * TMEM_COLS;
+        const uint32_t acc = tmem + b * G::TMEM_COLS;
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % GSTAGES;
-          const uint32_t ph = (it / GSTAGES) & 1;
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(su32(&full[s]), ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t ad = umma_desc_sw128(su32(As + s * A_STAGE_BYTES));
-          const uint64_t bd = umma_desc_sw128(su32(Bs + s * B_STAGE_BYTES));
+          const uint32_t a0 = su32(smem + s * G::STAGE_BYTES);
+          const uint32_t b0 = a0 + G::A_BYTES;
 #pragma unroll
-          for (int k = 0; k < GBK / 16; ++k)  // +32 B per K16 step inside the swizzle atom
-            umma_f16(acc, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / G::KI; ++k) {
+            const uint64_t ad = umma_desc_sw128(a0 + k * adv_a, lbo_a);
+            const uint64_t bd = umma_desc_sw128(b0 + k * adv_b, lbo_b);
+            const uint32_t accum = (kb | k) != 0;
+            if (MODE == 0) {
+              umma<MODE>(acc, ad, bd, idesc, accum);
+            } else {
+              const uint32_t a1 = a0 + G::A_BYTES + G::B_BYTES, b1 = a1 + G::A_BYTES;
+              const uint64_t adl = umma_desc_sw128(a1 + k * adv_a, lbo_a);
+              const uint64_t bdl = umma_desc_sw128(b1 + k * adv_b, lbo_b);
+              // small terms first
+              umma<MODE>(acc, adl, bd, idesc, accum);
+              umma<MODE>(acc, ad, bdl, idesc, 1);
+              umma<MODE>(acc, ad, bd, idesc, 1);
+            }
+          }
           umma_commit(su32(&empty[s]));
         }
         umma_commit(su32(&tfull[b]));
@@ -244,23 +320,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t b = lt & 1, use = lt >> 1;
       mbar_wait(su32(&tfull[b]), use & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int row = m_tile * GBM + q * 32 + lane;
+      const int row = m_tile * BM + q * 32 + lane;
       char* dbase = g.d + (int64_t)batch * g.dsb;
 #pragma unroll 1
-      for (int c = 0; c < GBN / 32; ++c) {
+      for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
         const uint32_t taddr =
-            tmem + b * TMEM_COLS + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
+            tmem + b * G::TMEM_COLS + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
         TMEM_LD32(taddr, v);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c == GBN / 32 - 1) {
+        if (c == BN / 32 - 1) {
           // accumulator fully read: hand it back to the MMA warp
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(su32(&tempty[b]));
         }
-        const int n0 = n_tile * GBN + c * 32;
-        const int row0 = m_tile * GBM + q * 32;
+        const int n0 = n_tile * BN + c * 32;
+        const int row0 = m_tile * BM + q * 32;
         if (g.epi == 1 && row0 + 32 <= g.m && n0 + 32 <= g.n) {
           // column-major destination: transpose the warp's 32x32 chunk
           // through shared memory so each lane writes 16-B pieces of columns
@@ -336,7 +412,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(2 * TMEM_COLS));
+                 "r"(2 * G::TMEM_COLS));
   }
 }
 
@@ -354,35 +430,70 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-static bool make_map(CUtensorMap* map, int dt, const void* base, int64_t kdim, int64_t rows,
-                     int64_t batch, int64_t row_stride, int64_t batch_stride, int box_rows) {
+// operand view in global memory: rows (M for A, N for B) x k x batch, byte
+// strides; mn = unit stride along rows (MN-major), else along k (K-major)
+struct OpView {
+  const void* base;
+  int64_t rows, k, batch;
+  int64_t rs, ks, bs;  // byte strides
+  bool mn;
+};
+
+template <int MODE>
+static bool make_map(CUtensorMap* map, int dt, const OpView& v, int box_rows) {
+  using G = Cfg<MODE>;
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)kdim, (cuuint64_t)rows, (cuuint64_t)batch};
-  cuuint64_t strides[2] = {(cuuint64_t)row_stride, (cuuint64_t)batch_stride};
-  cuuint32_t box[3] = {GBK, (cuuint32_t)box_rows, 1};
+  const CUtensorMapDataType ty = MODE ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                               : dt == TPG_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  cuuint64_t dims[3], strides[2];
+  cuuint32_t box[3] = {0, 0, 1};
+  if (!v.mn) {
+    dims[0] = v.k; dims[1] = v.rows; dims[2] = v.batch;
+    strides[0] = v.rs; strides[1] = v.bs;
+    box[0] = G::BK; box[1] = box_rows;
+  } else {
+    dims[0] = v.rows; dims[1] = v.k; dims[2] = v.batch;
+    strides[0] = v.ks; strides[1] = v.bs;
+    box[0] = 128 / G::ESZ; box[1] = G::BK;
+  }
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(map, dt == TPG_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                  3, const_cast<void*>(base), dims, strides, box, estr,
+  CUresult r = fn(map, ty, 3, const_cast<void*>(v.base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-// K-major operand view (rows x k) with row stride rs and unit k stride?
-static bool k_major_ok(const tpg_operand* o, int64_t rs, int64_t ks, int64_t bstride, int64_t batch) {
+// TMA-legal in place?  unit stride along k (K-major) or rows (MN-major),
+// 16-B aligned base and outer strides, native byte order
+static bool classify(const tpg_operand* o, int esz, int64_t rows, int64_t k, int64_t batch,
+                     int64_t rs, int64_t ks, int64_t bs, OpView* v) {
   const uintptr_t base = (uintptr_t)o->base + o->offset;
-  return !o->big_endian && ks == 2 && rs > 0 && rs % 16 == 0 && base % 16 == 0 &&
-         (batch == 1 || (bstride > 0 && bstride % 16 == 0));
+  v->base = (const void*)base;
+  v->rows = rows; v->k = k; v->batch = batch;
+  v->rs = rs; v->ks = ks; v->bs = batch == 1 ? 0 : bs;
+  if (o->big_endian || base % 16) return false;
+  if (batch > 1 && (bs <= 0 || bs % 16)) return false;
+  if (ks == esz && rs > 0 && rs % 16 == 0) {
+    v->mn = false;
+    if (batch == 1) v->bs = rs * rows;
+    return true;
+  }
+  if (rs == esz && ks > 0 && ks % 16 == 0) {
+    v->mn = true;
+    if (batch == 1) v->bs = ks * k;
+    return true;
+  }
+  return false;
 }
 
 extern "C" int tpg_unary(tpg_stream stream, int op, const tpg_plan* plan, const tpg_operand* d,
                          const tpg_operand* a, int compute, int mode, int force_complex);
 
-// pack a (rows x k) operand with strides (rs, ks, bs) into a K-major
-// contiguous scratch (row stride kp*2, batch stride rows*kp*2)
+// pack a (rows x k) half/bf16 operand into a K-major contiguous scratch
 static int pack_k_major(Stream* st, const tpg_operand* src, int64_t rows, int64_t k, int64_t batch,
-                        int64_t rs, int64_t ks, int64_t bs, void** out, int64_t* out_rs) {
+                        int64_t rs, int64_t ks, int64_t bs, void** out, OpView* v) {
   const int64_t kp = (k + 7) & ~(int64_t)7;
   const size_t bytes = (size_t)(kp * rows * batch * 2);
   TPG_CUDA_CHECK(cudaMallocAsync(out, bytes ? bytes : 16, st->s));
@@ -396,55 +507,97 @@ static int pack_k_major(Stream* st, const tpg_operand* src, int64_t rows, int64_
   d.base = *out;
   d.dtype = src->dtype;
   int rc = tpg_unary(st, TPG_IDENTITY, &p, &d, src, src->dtype, TPG_STANDARD, 0);
-  *out_rs = kp * 2;
+  v->base = *out;
+  v->rows = rows; v->k = k; v->batch = batch;
+  v->rs = kp * 2; v->ks = 2; v->bs = kp * rows * 2;
+  v->mn = false;
   return rc;
 }
 
-int gemm_sm100(Stream* st, int64_t batch, const tpg_operand* d, const int64_t* ds,
-               const tpg_operand* a, const int64_t* as, const tpg_operand* b, const int64_t* bs,
-               int64_t m, int64_t n, int64_t k, int compute, int mode) {
-  const int adt = a->dtype;
-  if (!(adt == TPG_HALF || adt == TPG_BF16) || b->dtype != adt) return 0;
-  if (!(d->dtype == TPG_HALF || d->dtype == TPG_BF16 || d->dtype == TPG_FLOAT)) return 0;
-  if (dt_kind(compute) != K_FLT || mode != TPG_STANDARD || d->big_endian) return 0;
-  if (m < 128 || n < 128 || k < 64 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) return 0;
-  if (batch * ((m + GBM - 1) / GBM) * ((n + GBN - 1) / GBN) > INT32_MAX) return 0;
-  if (sm_count(st->device) <= 0) return 0;
-  {
-    int major = 0;
-    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, st->device);
-    if (major != 10) return 0;
+// 3xTF32 operand split: for a (rows x k x batch) f32 view with byte strides
+// (rs, ks, bs), write hi = x with the low 13 mantissa bits cleared (exactly
+// a tf32 value, so the tensor core's own operand rounding cannot matter)
+// and lo = x - hi (exact) into contiguous K-major [b][row][k] buffers with a
+// 16-B aligned row pitch.  32x32 tiles through shared memory: the loads
+// run along the source's unit-stride axis (rows when the source is
+// M/N-contiguous), the stores along k, so both sides stay coalesced.
+__global__ void __launch_bounds__(256) k_tf32_split(const char* __restrict__ src, int64_t rows,
+                                                    int64_t k, int64_t rs, int64_t ks, int64_t bs,
+                                                    int rows_fast, int swap, int64_t pitch,
+                                                    float* __restrict__ hi, float* __restrict__ lo) {
+  __shared__ uint32_t tile[32][33];
+  const int64_t b = blockIdx.z;
+  const int64_t r0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const char* sb = src + b * bs;
+#pragma unroll
+  for (int i = 0; i < 32; i += 8) {
+    // (fast, slow) = (row, k) when rows are contiguous in the source
+    const int64_t r = rows_fast ? r0 + tx : r0 + ty + i;
+    const int64_t kk = rows_fast ? k0 + ty + i : k0 + tx;
+    uint32_t u = 0;
+    if (r < rows && kk < k) {
+      u = __ldg((const uint32_t*)(sb + r * rs + kk * ks));
+      if (swap) u = __byte_perm(u, 0, 0x0123);
+    }
+    if (rows_fast) tile[ty + i][tx] = u;  // [k][row]
+    else tile[tx][ty + i] = u;            // [k][row]
   }
-  // A is (m x k): rows = m, row stride as[0], k stride as[1]
-  // B is (k x n): rows = n, row stride bs[1], k stride bs[0]
-  const void* abase = (const char*)a->base + a->offset;
-  const void* bbase = (const char*)b->base + b->offset;
-  int64_t a_rs = as[0], b_rs = bs[1], a_bs = as[2], b_bs = bs[2];
-  void* apack = nullptr;
-  void* bpack = nullptr;
-  int rc;
-  if (!k_major_ok(a, as[0], as[1], as[2], batch)) {
-    rc = pack_k_major(st, a, m, k, batch, as[0], as[1], as[2], &apack, &a_rs);
-    if (rc) return rc;
-    abase = apack;
-    a_bs = a_rs * m;
+  __syncthreads();
+  float* hb = hi + b * rows * pitch;
+  float* lb = lo + b * rows * pitch;
+#pragma unroll
+  for (int i = 0; i < 32; i += 8) {
+    const int64_t r = r0 + ty + i, kk = k0 + tx;
+    if (r < rows && kk < k) {
+      const uint32_t u = tile[tx][ty + i];
+      const float x = __uint_as_float(u);
+      const float h = __uint_as_float(u & 0xffffe000u);
+      hb[r * pitch + kk] = isfinite(x) ? h : x;
+      lb[r * pitch + kk] = isfinite(x) ? __fsub_rn(x, h) : 0.0f;
+    }
   }
-  if (!k_major_ok(b, bs[1], bs[0], bs[2], batch)) {
-    rc = pack_k_major(st, b, n, k, batch, bs[1], bs[0], bs[2], &bpack, &b_rs);
-    if (rc) return rc;
-    bbase = bpack;
-    b_bs = b_rs * n;
-  }
-  if (batch == 1) {
-    a_bs = a_rs * m;
-    b_bs = b_rs * n;
-  }
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, adt, abase, k, m, batch, a_rs, a_bs, GBM) ||
-      !make_map(&mb, adt, bbase, k, n, batch, b_rs, b_bs, GBN)) {
-    if (apack) cudaFreeAsync(apack, st->s);
-    if (bpack) cudaFreeAsync(bpack, st->s);
-    return 0;  // not encodable: SIMT path
+}
+
+static int split_tf32(Stream* st, const tpg_operand* src, int64_t rows, int64_t k, int64_t batch,
+                      int64_t rs, int64_t ks, int64_t bs, void** out, OpView* hi, OpView* lo) {
+  const int64_t kp = (k + 3) & ~(int64_t)3;
+  const int64_t n = kp * rows * batch;
+  TPG_CUDA_CHECK(cudaMallocAsync(out, (size_t)(2 * n * 4 + 16), st->s));
+  float* h = (float*)*out;
+  float* l = h + n;
+  const char* sb = (const char*)src->base + src->offset;
+  const bool rows_fast = (rs == 4 || rs == -4) && ks != 4;
+  const dim3 grid((unsigned)((k + 31) / 32), (unsigned)((rows + 31) / 32), (unsigned)batch);
+  if (grid.y > 65535 || grid.z > 65535) return arg_fail("tf32 split: operand too large");
+  k_tf32_split<<<grid, dim3(32, 8), 0, st->s>>>(sb, rows, k, rs, ks, bs, rows_fast, src->big_endian,
+                                                kp, h, l);
+  TPG_LAUNCH_CHECK("tf32 split");
+  OpView v;
+  v.rows = rows; v.k = k; v.batch = batch;
+  v.mn = false;
+  v.ks = 4; v.rs = kp * 4; v.bs = kp * 4 * rows;
+  *hi = v;
+  *lo = v;
+  hi->base = h;
+  lo->base = l;
+  return TPG_OK;
+}
+
+template <int MODE>
+static int launch_sm100(Stream* st, int64_t batch, const tpg_operand* d, const int64_t* ds,
+                        const OpView* av, const OpView* bv, int64_t m, int64_t n, int64_t k,
+                        int adt) {
+  using G = Cfg<MODE>;
+  CUtensorMap ma, mb, mal, mbl;
+  if (!make_map<MODE>(&ma, adt, av[0], G::BM) || !make_map<MODE>(&mb, adt, bv[0], G::BN))
+    return 0;
+  if (MODE) {
+    if (!make_map<MODE>(&mal, adt, av[1], G::BM) || !make_map<MODE>(&mbl, adt, bv[1], G::BN))
+      return 0;
+  } else {
+    mal = ma;
+    mbl = mb;
   }
   Sm100Args g;
   g.d = (char*)d->base + d->offset;
@@ -459,24 +612,65 @@ int gemm_sm100(Stream* st, int64_t batch, const tpg_operand* d, const int64_t* d
   const bool al = ((uintptr_t)g.d % 16) == 0;
   g.epi = (ds[1] == es && ds[0] % 16 == 0 && al) ? 2
           : (ds[0] == es && ds[1] % 16 == 0 && al && (batch == 1 || ds[2] % 16 == 0)) ? 1 : 0;
-  g.tiles_m = (int)((m + GBM - 1) / GBM);
-  g.tiles_n = (int)((n + GBN - 1) / GBN);
-  const uint32_t fmt = adt == TPG_BF16 ? 1u : 0u;
-  const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(GBN >> 3) << 17) |
-                         ((uint32_t)(GBM >> 4) << 24);
+  g.tiles_m = (int)((m + G::BM - 1) / G::BM);
+  g.tiles_n = (int)((n + G::BN - 1) / G::BN);
+  g.amn = av[0].mn;
+  g.bmn = bv[0].mn;
+  uint32_t fmt = MODE ? 2u : adt == TPG_BF16 ? 1u : 0u;
+  const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)g.amn << 15) |
+                         ((uint32_t)g.bmn << 16) | ((uint32_t)(G::BN >> 3) << 17) |
+                         ((uint32_t)(G::BM >> 4) << 24);
   static bool attr_set[64] = {false};
   if (!attr_set[st->device]) {
-    TPG_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)GEMM_SMEM));
+    TPG_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_sm100<MODE>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
     attr_set[st->device] = true;
   }
   const int ntiles = g.tiles_m * g.tiles_n * (int)batch;
   const int grid = ntiles < sm_count(st->device) ? ntiles : sm_count(st->device);
-  k_gemm_sm100<<<grid, GEMM_THREADS, GEMM_SMEM, st->s>>>(ma, mb, g, idesc, ntiles);
+  k_gemm_sm100<MODE><<<grid, GEMM_THREADS, G::SMEM, st->s>>>(ma, mb, mal, mbl, g, idesc, ntiles);
   TPG_LAUNCH_CHECK("gemm sm100");
-  if (apack) TPG_CUDA_CHECK(cudaFreeAsync(apack, st->s));
-  if (bpack) TPG_CUDA_CHECK(cudaFreeAsync(bpack, st->s));
   return 1;
+}
+
+int gemm_sm100(Stream* st, int64_t batch, const tpg_operand* d, const int64_t* ds,
+               const tpg_operand* a, const int64_t* as, const tpg_operand* b, const int64_t* bs,
+               int64_t m, int64_t n, int64_t k, int compute, int mode) {
+  const int adt = a->dtype;
+  const bool f32 = adt == TPG_FLOAT;
+  if (!(adt == TPG_HALF || adt == TPG_BF16 || f32) || b->dtype != adt) return 0;
+  if (!(d->dtype == TPG_HALF || d->dtype == TPG_BF16 || d->dtype == TPG_FLOAT)) return 0;
+  if (f32 && d->dtype != TPG_FLOAT) return 0;
+  if (dt_kind(compute) != K_FLT || mode != TPG_STANDARD || d->big_endian) return 0;
+  if (m < 128 || n < 128 || k < 64 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) return 0;
+  if (batch * ((m + 127) / 128) * ((n + 127) / 128) > INT32_MAX) return 0;
+  if (sm_count(st->device) <= 0) return 0;
+  {
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, st->device);
+    if (major != 10) return 0;
+  }
+  // A is (m x k): rows = m, row stride as[0], k stride as[1]
+  // B is (k x n): rows = n, row stride bs[1], k stride bs[0]
+  OpView av[2], bv[2];
+  void* apack = nullptr;
+  void* bpack = nullptr;
+  int rc;
+  if (f32) {
+    rc = split_tf32(st, a, m, k, batch, as[0], as[1], as[2], &apack, &av[0], &av[1]);
+    if (rc == TPG_OK) rc = split_tf32(st, b, n, k, batch, bs[1], bs[0], bs[2], &bpack, &bv[0], &bv[1]);
+  } else {
+    rc = TPG_OK;
+    if (!classify(a, 2, m, k, batch, as[0], as[1], as[2], &av[0]))
+      rc = pack_k_major(st, a, m, k, batch, as[0], as[1], as[2], &apack, &av[0]);
+    if (rc == TPG_OK && !classify(b, 2, n, k, batch, bs[1], bs[0], bs[2], &bv[0]))
+      rc = pack_k_major(st, b, n, k, batch, bs[1], bs[0], bs[2], &bpack, &bv[0]);
+  }
+  if (rc == TPG_OK) rc = f32 ? launch_sm100<1>(st, batch, d, ds, av, bv, m, n, k, adt)
+                             : launch_sm100<0>(st, batch, d, ds, av, bv, m, n, k, adt);
+  if (apack) cudaFreeAsync(apack, st->s);
+  if (bpack) cudaFreeAsync(bpack, st->s);
+  return rc;  // 1 handled, 0 not encodable (SIMT path), <0 error
 }
 
 }  // namespace tpg

@@ -951,10 +951,10 @@ __global__ void __launch_bounds__(256, 3) k_red_rows_v(RedParams p, Part* ws, ui
 // and reads one 16-byte vector per row; a block covers NT*VE outputs x one
 // row chunk.  Partials are chunk-major (ws[c * O + o]) so the finalizing
 // block reads them coalesced, 8 chunks in flight per thread.
-template <int OP, typename T>
-__global__ void __launch_bounds__(128, 6) k_red_cols_v(RedParams p, int64_t nob, Part* ws,
-                                                       uint32_t* cnt) {
-  constexpr int VE = Vec16<T>::n, U = 4, NT = 128;
+template <int OP, typename T, int NT>
+__global__ void __launch_bounds__(NT, 768 / NT) k_red_cols_v(RedParams p, int64_t nob, Part* ws,
+                                                             uint32_t* cnt) {
+  constexpr int VE = Vec16<T>::n, U = 4;
   __shared__ int is_last;
   uint32_t st = 0;
   const int tid = threadIdx.x;
@@ -1068,9 +1068,10 @@ int launch_vec(RedParams& p, Stream* st, bool col, bool& done) {
   };
   if (col) {
     if (!cols_vec_ok<T>(p)) return TPG_OK;
-    constexpr int VE = Vec16<T>::n, NT = 128;
+    constexpr int VE = Vec16<T>::n;
+    constexpr int NT = 64;  // 64 x 16 B = 1 KiB of a row per block (measured best)
     const int64_t nob = (p.O + NT * VE - 1) / (NT * VE);
-    const int64_t target = sms * 6 * 2;  // two waves of resident blocks
+    const int64_t target = sms * (768 / NT) * 4;  // four waves of resident blocks
     int64_t C = (target + nob - 1) / nob;
     if (C > p.N / 32) C = p.N / 32;
     if (C > 64) C = 64;
@@ -1079,7 +1080,7 @@ int launch_vec(RedParams& p, Stream* st, bool col, bool& done) {
     p.C = (p.N + p.chunk - 1) / p.chunk;
     if (int rc = scratch(p.O * p.C, nob)) return rc;
     const int64_t work = nob * p.C;
-    k_red_cols_v<OP, T><<<(int)std::min<int64_t>(work, 1 << 30), NT, 0, st->s>>>(p, nob, ws, cnt);
+    k_red_cols_v<OP, T, NT><<<(int)std::min<int64_t>(work, 1 << 30), NT, 0, st->s>>>(p, nob, ws, cnt);
   } else {
     if (!rows_vec_ok<T>(p)) return TPG_OK;
     const int64_t wslots = sms * 3 * 8;  // resident warps

@@ -2,7 +2,8 @@
 
 Tolerance: |C - C_oracle| <= 1e-2 * sum_k |a_ik||b_kj| for
 half / bfloat16 operands (fp32 accumulation in TMEM vs the reference's
-compensated double sum, one rounding each).  Layouts follow SURVEY §8d
+compensated double sum, one rounding each), 1e-5 for float operands (3xTF32
+split products, fp32 accumulation; north_star's fp32 tolerance).  Layouts follow SURVEY §8d
 cfg4: A a transposed column-major base (K-major), B column-major with a
 padded leading dimension, a strided B (pack path), column-major C.
 """
@@ -33,6 +34,8 @@ def _make(rng, dt, rows, cols, pad=0):
     if dt is tp.bfloat16:
         raw = np.asfortranarray((base.view(np.uint32) >> 16).astype(np.uint16))
         t = tp.from_numpy(raw, dtype=tp.bfloat16)
+    elif dt is tp.float:
+        t = tp.from_numpy(np.asfortranarray(base))
     else:
         t = tp.from_numpy(np.asfortranarray(base.astype(np.float16)))
     return tp.apply_index(t, (slice(0, rows), slice(None))) if pad else t
@@ -60,14 +63,15 @@ def _oracle_block(A, B, rows, cols, out_dtype):
     return out, bound
 
 
-def _check(Cg, A, B, rng, samples=48):
+def _check(Cg, A, B, rng, samples=48, tol=None):
+    tol = tol if tol is not None else (1e-5 if A.dtype is tp.float else TOL)
     m, n = Cg.dims
     rows = np.sort(rng.choice(m, min(samples, m), replace=False))
     cols = np.sort(rng.choice(n, min(samples, n), replace=False))
     want, bound = _oracle_block(A, B, rows, cols, Cg.dtype)
     got = _host(Cg)[np.ix_(rows, cols)]
     err = np.abs(got - want)
-    assert np.all(err <= TOL * bound + 1e-6), float((err / (bound + 1e-30)).max())
+    assert np.all(err <= tol * bound + 1e-30), float((err / (bound + 1e-30)).max())
 
 
 @pytest.mark.parametrize("dt", [tp.half, tp.bfloat16])
@@ -123,3 +127,66 @@ def test_gemm_nonfinite_becomes_nan():
     Cg = tp.to_numpy(tp.matmul(tp.from_numpy(np.asfortranarray(a)),
                                tp.from_numpy(np.asfortranarray(b))))
     assert np.isnan(Cg[3]).all() and np.all(Cg[4] == 128)
+
+
+@pytest.mark.parametrize("m,n,k", [(256, 256, 128), (384, 640, 320), (1000, 700, 333),
+                                   (2048, 1024, 4096)])
+def test_gemm_f32_tf32x3(m, n, k):
+    """float x float on tcgen05 kind::tf32 (3xTF32), K-major A and B."""
+    rng = np.random.default_rng(m * 7 + n + k)
+    A = tp.transpose(_make(rng, tp.float, k, m))
+    B = _make(rng, tp.float, k, n, pad=32)
+    Cg = tp.matmul(A, B)
+    assert Cg.dtype is tp.float
+    _check(Cg, A, B, rng)
+
+
+@pytest.mark.parametrize("dt", [tp.half, tp.bfloat16, tp.float])
+def test_gemm_mn_major_operands(dt):
+    """A column-major (M contiguous) and B row-major (N contiguous): both
+    operands are fed MN-major to the tensor cores, no pack."""
+    rng = np.random.default_rng(21)
+    m, n, k = 640, 512, 448
+    A = _make(rng, dt, m, k)                      # M-major
+    B = tp.transpose(_make(rng, dt, n, k))        # N-major
+    _check(tp.matmul(A, B), A, B, rng)
+    Bk = _make(rng, dt, k, n)                     # mixed: A MN-major, B K-major
+    _check(tp.matmul(A, Bk), A, Bk, rng)
+    At = tp.transpose(_make(rng, dt, k, m))       # mixed: A K-major, B MN-major
+    _check(tp.matmul(At, B), At, B, rng)
+
+
+def test_gemm_f32_strided_and_swapped():
+    """f32 operands without a unit stride or byte-swapped go through the
+    generic split; result still within 1e-5 of sum|a||b|."""
+    rng = np.random.default_rng(22)
+    m, n, k = 384, 256, 320
+    Ab = _make(rng, tp.float, 2 * m, k)
+    A = tp.apply_index(Ab, (slice(None, None, 2), slice(None)))
+    B = _make(rng, tp.float, k, n)
+    _check(tp.matmul(A, B), A, B, rng)
+    Bs = _make(rng, tp.float, k, n)
+    want = tp.to_numpy(Bs).copy()
+    tp.byteswap(Bs)
+    Cg = tp.to_numpy(tp.matmul(A, Bs)).astype(np.float64)
+    a = tp.to_numpy(A).astype(np.float64)
+    bound = np.abs(a) @ np.abs(want.astype(np.float64))
+    assert np.all(np.abs(Cg - a @ want.astype(np.float64)) <= 1e-5 * bound)
+
+
+@pytest.mark.parametrize("dt", [tp.half, tp.float])
+def test_gemm_batched_col_major(dt):
+    """SURVEY cfg4 batched layout: A, B, C column-major with batch slowest
+    (A MN-major, B K-major)."""
+    rng = np.random.default_rng(23)
+    m, n, k, nb = 384, 256, 192, 3
+    npd = np.float16 if dt is tp.half else np.float32
+    a = rng.uniform(-1, 1, (m, k, nb)).astype(npd)
+    b = rng.uniform(-1, 1, (k, n, nb)).astype(npd)
+    Cg = tp.to_numpy(tp.matmul_batched(tp.from_numpy(np.asfortranarray(a)),
+                                       tp.from_numpy(np.asfortranarray(b)))).astype(np.float64)
+    tol = TOL if dt is tp.half else 1e-5
+    for i in range(nb):
+        a64, b64 = a[:, :, i].astype(np.float64), b[:, :, i].astype(np.float64)
+        bound = np.abs(a64) @ np.abs(b64)
+        assert np.all(np.abs(Cg[:, :, i] - a64 @ b64) <= tol * bound + 1e-30)

@@ -340,6 +340,11 @@ def cfg5(tp, dev, run):
     run("cfg5_multiply_scalar_f32_2^28", lambda: tp.multiply(Y, k15, dest=Z), nbytes=8 * n5,
         fl=False)
     run("cfg5_add_scalar_f32_2^28", lambda: tp.add(Z, km2, dest=Y), nbytes=8 * n5, fl=False)
+    # the same multiply-then-add as one fused chain:
+    # 8 B/elem moved instead of 16; rate counted on the unfused 16 B/elem
+    # algorithm is 2x this GB/s
+    run("cfg5_chain_mul_add_f32_2^28", lambda: tp.chain(Y, [("multiply", k15), ("add", km2)],
+                                                          dest=Z), nbytes=8 * n5, fl=False)
     del S, Y, Z
     s16 = tp.from_numpy(np.random.default_rng(9).integers(-3000, 3000, n5).astype(">i2"), dev)
     h16 = tp.tensor_create((n5,), tp.half, dev)

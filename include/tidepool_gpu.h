@@ -196,6 +196,27 @@ int tpg_matmul_batched(tpg_stream stream, int64_t batch,
                        const tpg_operand* b, const int64_t b_strides[3],
                        int64_t m, int64_t n, int64_t k, int compute, int mode);
 
+/* Extension: fused elementwise chain x = op_i(x, s_i)
+ * (or op_i(s_i, x) with scalar_first) over one source view in one pass.
+ * Each step has the reference binary semantics with a by-value scalar
+ * (kernels.py:50-81, 213-248): compute in `compute` (widen_for_compute of
+ * the step's result dtype), round once to `dtype`.  The last step's dtype
+ * is the destination dtype.  plan has 2 views (d, a).  Bit-identical to
+ * running the steps as separate tpg_binary calls. */
+typedef struct tpg_chain_step {
+  int32_t op;            /* TPG_ADD .. TPG_MAXIMUM */
+  int32_t dtype;         /* the step's result (rounding) dtype */
+  int32_t compute;       /* widen_for_compute(dtype) */
+  int32_t scalar_first;  /* 1: op(s, x), 0: op(x, s) */
+  int32_t scalar_dtype;  /* dtype of `scalar` */
+  int32_t reserved;
+  uint8_t scalar[16];    /* element bytes, little-endian */
+} tpg_chain_step;
+int tpg_chain(tpg_stream stream, const tpg_plan* plan, const tpg_operand* d,
+              const tpg_operand* a, int nsteps, const tpg_chain_step* steps, int mode);
+int tpg_chain_check(tpg_stream stream, const tpg_plan* plan, const tpg_operand* d,
+                    const tpg_operand* a, int nsteps, const tpg_chain_step* steps, int mode);
+
 /* fill: kernels.fill (kernels.py:343-352); `value` is the packed element
  * (dtype size bytes, already cast and byte-ordered, ops.py:752-758). */
 int tpg_fill(tpg_stream stream, const tpg_plan* plan, const tpg_operand* d,

@@ -18,7 +18,7 @@ from .dtypes import (cast_scalar, implicit_casting, promote, set_implicit_castin
 from .errors import *  # noqa: F401,F403
 from .ops import (absolute, add, arange, arccosine, arcsine, array_equal, byteswap, cast,
                   clear_status, conjugate, copy, cosine, divide, ensure, exponential, fill,
-                  frobenius_norm, get_status, identity, inner, logarithm, matmul, matmul_batched,
+                  frobenius_norm, get_status, identity, inner, logarithm, matmul, matmul_batched, chain,
                   maximum, minimum, multiply, negate, ones, outer, reduce, sine, square_root,
                   subtract, zeros)
 from .plan import IterPlan, build_plan, canonicalize
@@ -30,6 +30,9 @@ from .tensors import (MAX_DIMS, Scalar, Tensor, apply_index, broadcast_to, conti
 
 _dispatch.register_module("core")
 _dispatch.register_device_impl("core", "gpu", table.build_core_table())
+# extension entries beyond the reference's 31 keys (dispatch.add_op,
+# reference dispatch.py:111-117)
+_dispatch.add_op("core", "gpu", "ewise_chain", table.chain_entry)
 
 bool = dtypes.BOOL  # noqa: A001
 int8 = dtypes.INT8

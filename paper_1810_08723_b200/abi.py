@@ -30,6 +30,12 @@ class Operand(C.Structure):
                 ("big_endian", C.c_int32), ("imm", C.c_uint64 * 2)]
 
 
+class ChainStep(C.Structure):
+    _fields_ = [("op", C.c_int32), ("dtype", C.c_int32), ("compute", C.c_int32),
+                ("scalar_first", C.c_int32), ("scalar_dtype", C.c_int32),
+                ("reserved", C.c_int32), ("scalar", C.c_uint8 * 16)]
+
+
 class DeviceProps(C.Structure):
     _fields_ = [("sm_count", C.c_int32), ("cc_major", C.c_int32), ("cc_minor", C.c_int32),
                 ("total_mem", C.c_int64), ("free_mem", C.c_int64), ("l2_bytes", C.c_int32),
@@ -108,6 +114,8 @@ PROTOTYPES = {
                           C.c_int, C.c_int]),
     "tpg_matmul_batched": (_i32, [_vp, _i64, _OP, P(_i64), _OP, P(_i64), _OP, P(_i64), _i64,
                                   _i64, _i64, C.c_int, C.c_int]),
+    "tpg_chain": (_i32, [_vp, _PLAN, _OP, _OP, C.c_int, C.POINTER(ChainStep), C.c_int]),
+    "tpg_chain_check": (_i32, [_vp, _PLAN, _OP, _OP, C.c_int, C.POINTER(ChainStep), C.c_int]),
     "tpg_fill": (_i32, [_vp, _PLAN, _OP, _vp, _i32]),
     "tpg_arange": (_i32, [_vp, _PLAN, _OP]),
     "tpg_byteswap": (_i32, [_vp, _PLAN, _OP]),

@@ -26,7 +26,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
           "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", f"-I{ROOT / 'include'}"]
 # files whose double arithmetic must not be contracted into FMAs (the
 # reference computes every + - * as a separately rounded CPython float op)
-NO_FMA_PREFIX = ("tpg_ewise", "tpg_reduce")
+NO_FMA_PREFIX = ("tpg_ewise", "tpg_reduce", "tpg_chain")
 
 
 def _headers():

@@ -279,6 +279,38 @@ def matmul_batched_entry(batch, d_buf, d_base, d_strides, store, a_buf, a_base, 
                                        dtypes.MODE_CODE[store.mode]), "matmul_batched")
 
 
+class ChainFn:
+    """Descriptor of a fused chain: per step (op, result dtype, compute
+    dtype, scalar Codec, scalar_first)."""
+    __slots__ = ("steps", "mode")
+
+    def __init__(self, steps, mode="standard"):
+        self.steps, self.mode = steps, mode
+
+
+def chain_entry(plan, d_buf, store, a_buf, a_unpack, fn, bases):
+    """Extension entry: one pass for a chain of binary
+    ops with by-value scalars, bit-identical to the ops run one by one."""
+    L = _native.lib()
+    p = plan.to_c()
+    d = dest(d_buf, bases[0], store)
+    a = operand(a_buf, bases[1], a_unpack)
+    n = len(fn.steps)
+    arr = (abi.ChainStep * n)()
+    for i, (op, rdt, comp, codec, sfirst) in enumerate(fn.steps):
+        arr[i].op = abi.BINARY_CODE[op]
+        arr[i].dtype = rdt.code
+        arr[i].compute = comp.code
+        arr[i].scalar_first = 1 if sfirst else 0
+        arr[i].scalar_dtype = codec.dtype.code
+        raw = bytes(codec.imm).ljust(16, b"\0")
+        for j in range(16):
+            arr[i].scalar[j] = raw[j]
+    mode = dtypes.MODE_CODE[store.mode]
+    args = (_sh(), C.byref(p), C.byref(d), C.byref(a), n, arr, mode)
+    _guarded(store.mode, lambda: L.tpg_chain(*args), lambda: L.tpg_chain_check(*args))
+
+
 def fill_entry(plan, buf, pack, value, base):
     L = _native.lib()
     raw = dtypes.pack_value(pack.dtype, value, pack.byteorder)

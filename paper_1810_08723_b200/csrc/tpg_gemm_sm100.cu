@@ -42,9 +42,14 @@ template <int MODE>
 struct Cfg {
   static constexpr int ESZ = MODE ? 4 : 2;          // operand element bytes
   static constexpr int BM = 128;
-  static constexpr int BN = MODE ? 128 : 256;
-  static constexpr int BK = 128 / ESZ;              // one 128-B swizzle row
-  static constexpr int STAGES = MODE ? 3 : 4;
+  static constexpr int BN = 256;
+  // MODE 1 uses 64-B swizzle rows (BK = 16 floats) so that four stages of
+  // four tiles (A/B hi/lo, 48 KiB) fit next to the epilogue staging; N = 256
+  // keeps the shared-memory operand traffic per MMA flop at the f16 level
+  // (ncu: 128-wide tiles left the tensor pipe 61% busy, L1/smem-bound)
+  static constexpr int SWZ = MODE ? 64 : 128;       // swizzle row bytes
+  static constexpr int BK = SWZ / ESZ;
+  static constexpr int STAGES = 4;
   static constexpr int NPART = MODE ? 2 : 1;        // hi (+ lo)
   static constexpr int KI = MODE ? 8 : 16;          // K per MMA instruction
   static constexpr int A_BYTES = BM * BK * ESZ;     // 16 KiB
@@ -105,13 +110,16 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
 //   MN-major: 128 B of M (or N) per K row, K rows 128 B apart in 8-row
 //             groups 1024 B apart (SBO); consecutive 128-B MN atoms LBO
 //             bytes apart (one TMA box = BK rows).
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo) {
+//   64B swizzle (MODE 1, K-major only): rows of 64 B, 8-row groups 512 B
+//   apart.
+template <int SWZ>
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;   // SBO
-  d |= (uint64_t)1 << 46;             // descriptor version (Blackwell)
-  d |= (uint64_t)2 << 61;             // SWIZZLE_128B
+  d |= (uint64_t)((8 * SWZ) >> 4) << 32;        // SBO: 8 swizzle rows
+  d |= (uint64_t)1 << 46;                       // descriptor version (Blackwell)
+  d |= (uint64_t)(SWZ == 128 ? 2 : 4) << 61;    // SWIZZLE_128B / SWIZZLE_64B
   return d;
 }
 
@@ -185,10 +193,10 @@ __device__ __forceinline__ void load_operand(uint32_t dst, const CUtensorMap* ma
   if (!mn) {
     tma_load_3d(dst, map, bar, kb * G::BK, row0, batch);
   } else {
-    constexpr int ATOM = 128 / G::ESZ;
+    constexpr int ATOM = G::SWZ / G::ESZ;
 #pragma unroll
     for (int a = 0; a < ROWS / ATOM; ++a)
-      tma_load_3d(dst + a * (G::BK * 128), map, bar, row0 + a * ATOM, kb * G::BK, batch);
+      tma_load_3d(dst + a * (G::BK * G::SWZ), map, bar, row0 + a * ATOM, kb * G::BK, batch);
   }
 }
 
@@ -271,9 +279,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       // per-instruction K advance inside a stage: K-major +KI*ESZ bytes
       // along the swizzled row; MN-major +KI rows of 128 B
-      const uint32_t adv_a = g.amn ? G::KI * 128 : G::KI * G::ESZ;
-      const uint32_t adv_b = g.bmn ? G::KI * 128 : G::KI * G::ESZ;
-      const uint32_t lbo_a = g.amn ? BK * 128 : 16, lbo_b = g.bmn ? BK * 128 : 16;
+      const uint32_t adv_a = g.amn ? G::KI * G::SWZ : G::KI * G::ESZ;
+      const uint32_t adv_b = g.bmn ? G::KI * G::SWZ : G::KI * G::ESZ;
+      const uint32_t lbo_a = g.amn ? BK * G::SWZ : 16, lbo_b = g.bmn ? BK * G::SWZ : 16;
       uint32_t it = 0, lt = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
         const uint32_t b = lt & 1, use = lt >> 1;
@@ -289,15 +297,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint32_t b0 = a0 + G::A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / G::KI; ++k) {
-            const uint64_t ad = umma_desc_sw128(a0 + k * adv_a, lbo_a);
-            const uint64_t bd = umma_desc_sw128(b0 + k * adv_b, lbo_b);
+            const uint64_t ad = umma_desc<G::SWZ>(a0 + k * adv_a, lbo_a);
+            const uint64_t bd = umma_desc<G::SWZ>(b0 + k * adv_b, lbo_b);
             const uint32_t accum = (kb | k) != 0;
             if (MODE == 0) {
               umma<MODE>(acc, ad, bd, idesc, accum);
             } else {
               const uint32_t a1 = a0 + G::A_BYTES + G::B_BYTES, b1 = a1 + G::A_BYTES;
-              const uint64_t adl = umma_desc_sw128(a1 + k * adv_a, lbo_a);
-              const uint64_t bdl = umma_desc_sw128(b1 + k * adv_b, lbo_b);
+              const uint64_t adl = umma_desc<G::SWZ>(a1 + k * adv_a, lbo_a);
+              const uint64_t bdl = umma_desc<G::SWZ>(b1 + k * adv_b, lbo_b);
               // small terms first
               umma<MODE>(acc, adl, bd, idesc, accum);
               umma<MODE>(acc, ad, bdl, idesc, 1);
@@ -456,11 +464,12 @@ static bool make_map(CUtensorMap* map, int dt, const OpView& v, int box_rows) {
   } else {
     dims[0] = v.rows; dims[1] = v.k; dims[2] = v.batch;
     strides[0] = v.ks; strides[1] = v.bs;
-    box[0] = 128 / G::ESZ; box[1] = G::BK;
+    box[0] = G::SWZ / G::ESZ; box[1] = G::BK;
   }
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, ty, 3, const_cast<void*>(v.base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  G::SWZ == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

@@ -439,8 +439,9 @@ def main():
         base, t = cpu_baseline(max(args.steps // 10, 3))
         line = {"metric": METRIC, "value": base["value"], "unit": "GB/s", "n_gpus": args.gpus,
                 "steps": max(args.steps // 10, 3), "warmup": 1, "ms_per_step": round(t * 1e3, 3),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": config, "impl": "reference", "cpu_baseline": base,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded numpy)", "config": config, "impl": "reference",
+                "cpu_baseline": base,
                 "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)

@@ -24,10 +24,13 @@
 // runtime dtypes (warp-uniform), covering all 15x15 pairs, both byte orders
 // and every op with one kernel per (op class, compute kind, traversal).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <thrust/complex.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "tpg_common.cuh"
 #include "tpg_internal.h"
@@ -653,6 +656,215 @@ __global__ void __launch_bounds__(256, sizeof(TX) >= 4 ? 4 : 5) k_tile_f32(EwPar
   }
 }
 
+// k_tile_tma: the same transposing float kernel fed by TMA (SURVEY cfg2,
+// the headline).  The X operand is a 2-D tensor map over its memory order
+// (reversed plan axes are handled by mirrored coordinates and index
+// flips in shared memory); 64 x 64 X tiles stream through an XS-stage
+// shared-memory ring (one mbarrier per stage, thread 0 issues the bulk
+// tensor copies XS-1 tiles ahead), so a block keeps up to XS-1 tiles of
+// loads in flight without registers.  Phase 1 converts a stage into the
+// XOR-swizzled float tile (transposed), the block barrier then frees the
+// stage for the next TMA, phase 2 writes 16-B coalesced columns.
+constexpr int XS = 4;
+
+__device__ __forceinline__ void tma_mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+
+template <int OP, int NIN, int XI, typename TX, typename TY>
+__global__ void __launch_bounds__(256) k_tile_tma(const __grid_constant__ CUtensorMap xmap,
+                                                  EwParams p, int q, int nt0, int ntq, int ymode,
+                                                  int rev0, int revq) {
+  constexpr int SX = sizeof(TX);
+  constexpr int VX = 16 / SX;          // X elements per 16-B chunk
+  constexpr int LPR = TT * SX / 16;    // lanes per tile row (4, 8 or 16)
+  constexpr int RPW = 32 / LPR;        // tile rows per warp pass
+  constexpr int NLD = TT / (8 * RPW);  // 16-B chunks per thread per tile
+  constexpr int SWM = RPW > 4 ? RPW : 4;
+  constexpr int Y = 3 - XI;
+  constexpr int STAGE = TT * TT * SX;
+  extern __shared__ __align__(128) uint8_t tsm[];
+  uint8_t* xring = tsm;                                   // XS stages
+  float(*sm)[TT] = (float(*)[TT])(tsm + XS * STAGE);      // 16 KiB float tile
+  uint64_t* bar = (uint64_t*)(tsm + XS * STAGE + TT * TT * 4);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane % LPR;
+  const int r0 = warp * RPW + lane / LPR;
+  const int nwork = nt0 * ntq;
+  const char* ys = NIN >= 2 ? p.base[Y] : nullptr;
+  char* ds = p.base[0];
+  const int64_t sdq = p.str[0][q];
+  const int64_t syq = NIN >= 2 ? p.str[Y][q] : 0;
+  float yimm = 0.0f;
+  if (NIN >= 2 && ymode == 0) yimm = to_f<TY>(from_bits<TY>(p.imm[Y].lo));
+  // memory-order tile coordinates of work item w
+  auto issue = [&](int w, int s) {
+    const int t0 = w % nt0, tq = w / nt0;
+    const int mq = revq ? (ntq - 1 - tq) * TT : tq * TT;
+    const int m0 = rev0 ? (nt0 - 1 - t0) * TT : t0 * TT;
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar[s]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(STAGE)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];" ::"r"((uint32_t)__cvta_generic_to_shared(xring + s * STAGE)),
+        "l"((uint64_t)&xmap), "r"(mq), "r"(m0), "r"(b)
+        : "memory");
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < XS; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&xmap) : "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int w = blockIdx.x;
+    for (int s = 0; s < XS - 1 && w < nwork; ++s, w += gridDim.x) issue(w, s);
+  }
+  float yr[VX];
+  auto load_y = [&](int w) {
+    if (NIN >= 2 && ymode == 1) {
+      const int tq = w / nt0;
+#pragma unroll
+      for (int k = 0; k < VX; ++k) {
+        const int jj = revq ? TT - 1 - (c * VX + k) : c * VX + k;
+        yr[k] = to_f<TY>(__ldg((const TY*)(ys + (int64_t)(tq * TT + jj) * syq)));
+      }
+    }
+  };
+  if ((int)blockIdx.x < nwork) load_y(blockIdx.x);
+  int it = 0;
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++it) {
+    const int s = it % XS;
+    tma_mbar_wait((uint32_t)__cvta_generic_to_shared(&bar[s]), (it / XS) & 1);
+    // phase 1: stage (memory order) -> float tile [j][i ^ swz] (plan order)
+    const uint8_t* stg = xring + s * STAGE;
+    const int jb = revq ? TT - 1 - c * VX : c * VX;             // plan j of element 0
+    const int swz1 = (((revq ? (TT - 1 - c * VX) : c * VX) / VX) * SWM) & 31;
+#pragma unroll
+    for (int l = 0; l < NLD; ++l) {
+      const int rm = r0 + l * 8 * RPW;                          // memory row
+      const int i = rev0 ? TT - 1 - rm : rm;
+      const uint4 raw = *(const uint4*)(stg + rm * (TT * SX) + c * 16);
+      const TX* e = (const TX*)&raw;
+#pragma unroll
+      for (int k = 0; k < VX; ++k) {
+        const float x = to_f<TX>(e[k]);
+        float v = x;
+        if (NIN >= 2 && ymode <= 1) {
+          const float y = ymode == 0 ? yimm : yr[k];
+          v = XI == 1 ? fop<OP>(x, y) : fop<OP>(y, x);
+        }
+        sm[revq ? jb - k : jb + k][i ^ swz1] = v;
+      }
+    }
+    __syncthreads();  // stage s fully read; float tile complete
+    if (threadIdx.x == 0) {
+      const int wn = w + (XS - 1) * gridDim.x;
+      if (wn < nwork) issue(wn, (it + XS - 1) % XS);
+    }
+    const int t0 = w % nt0, tq = w / nt0;
+    if (w + (int)gridDim.x < nwork) load_y(w + gridDim.x);
+    // phase 2: float4 columns -> destination
+    const int ig = threadIdx.x % 16;
+    char* db = ds + (int64_t)(t0 * TT + ig * 4) * 4 + (int64_t)(tq * TT) * sdq;
+#pragma unroll
+    for (int pass = 0; pass < 4; ++pass) {
+      const int j = threadIdx.x / 16 + 16 * pass;
+      const int swz = ((j / VX) * SWM) & 31;
+      float4 f = *(const float4*)&sm[j][(ig * 4) ^ swz];
+      if (NIN >= 2 && ymode == 2) {
+        const int64_t sy0 = p.str[Y][0];
+        const char* yb = ys + (int64_t)(t0 * TT + ig * 4) * sy0 + (int64_t)(tq * TT + j) * syq;
+        float y[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) y[u] = to_f<TY>(__ldg((const TY*)(yb + u * sy0)));
+        if (XI == 1) {
+          f.x = fop<OP>(f.x, y[0]); f.y = fop<OP>(f.y, y[1]);
+          f.z = fop<OP>(f.z, y[2]); f.w = fop<OP>(f.w, y[3]);
+        } else {
+          f.x = fop<OP>(y[0], f.x); f.y = fop<OP>(y[1], f.y);
+          f.z = fop<OP>(y[2], f.z); f.w = fop<OP>(y[3], f.w);
+        }
+      }
+      __stcs((float4*)(db + j * sdq), f);
+    }
+    __syncthreads();  // float tile drained before the next phase 1
+  }
+}
+
+template <int SX>
+constexpr size_t tile_tma_smem() {
+  return (size_t)XS * TT * TT * SX + TT * TT * 4 + XS * 8 + 128;
+}
+
+// TMA launch of the cfg2 pattern: 2-D plan, X unit-stride (+-) along q,
+// 16-B multiple row stride, element size <= 4.  Returns false when the
+// layout is not eligible or the map cannot be encoded (caller falls back).
+template <auto K, typename TX>
+bool launch_tile_tma(EwParams& p, Stream* st, int xi, int q, int64_t nt0, int64_t ntq, int ymode) {
+  constexpr int SX = sizeof(TX);
+  if (SX > 4 || p.ndim != 2) return false;
+  const int64_t sq = p.str[xi][q], s0 = p.str[xi][0];
+  if ((sq != SX && sq != -SX) || s0 == 0 || (s0 < 0 ? -s0 : s0) % 16) return false;
+  const int64_t eq = p.ext[q], e0 = p.ext[0];
+  const char* lo = p.base[xi] + (sq < 0 ? (eq - 1) * sq : 0) + (s0 < 0 ? (e0 - 1) * s0 : 0);
+  if ((uintptr_t)lo % 16) return false;
+  auto enc = (PFN_cuTensorMapEncodeTiled_v12000)tensor_map_encoder();
+  if (!enc) return false;
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)eq, (cuuint64_t)e0};
+  cuuint64_t strides[1] = {(cuuint64_t)(s0 < 0 ? -s0 : s0)};
+  cuuint32_t box[2] = {TT, TT};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapDataType ty = SX == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                               : SX == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                         : CU_TENSOR_MAP_DATA_TYPE_UINT32;
+  if (enc(&map, ty, 2, const_cast<char*>(lo), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  constexpr size_t smem = tile_tma_smem<SX>();
+  static int bps = 0;
+  if (!bps) {
+    if (cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return false;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, K, 256, smem) != cudaSuccess || n < 1)
+      n = 1;
+    bps = n;
+  }
+  const int64_t slots = (int64_t)sm_count(st->device) * bps;
+  const int grid = (int)std::min<int64_t>(nt0 * ntq, slots);
+  K<<<grid, 256, smem, st->s>>>(map, p, q, (int)nt0, (int)ntq, ymode, s0 < 0 ? 1 : 0,
+                                sq < 0 ? 1 : 0);
+  return true;
+}
+
+// The TMA-fed variant is opt-in (TPG_TILE_TMA=1): measured on B200 at the
+// cfg2 shape it is slower than the register-prefetch k_tile_f32 (22.0 vs
+// 20.9 us per step, bench.py A/B), see DESIGN.md §4.
+inline bool tile_tma_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TPG_TILE_TMA");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // resident blocks per SM of kernel K at 256 threads (queried once per K)
 template <auto K>
 int blocks_per_sm() {
@@ -900,6 +1112,19 @@ int launch_ew(EwParams& p, Stream* st) {
           if (fast && plain && nrest <= 65535 && nt0 * ntq < (1 << 30)) {
             typedef typename Native<DTA>::T TA;
             typedef typename Native<(NIN >= 2 ? DTB : DTA)>::T TB;
+            if (nrest == 1 && !tile_tma_disabled()) {
+              bool ok;
+              if (NIN == 1)
+                ok = launch_tile_tma<k_tile_tma<0, 1, 1, TA, TA>, TA>(p, st, 1, qa, nt0, ntq, 0);
+              else if (x == 1)
+                ok = launch_tile_tma<k_tile_tma<OP, 2, 1, TA, TB>, TA>(p, st, 1, qa, nt0, ntq, ymode);
+              else
+                ok = launch_tile_tma<k_tile_tma<OP, 2, 2, TB, TA>, TB>(p, st, 2, qa, nt0, ntq, ymode);
+              if (ok) {
+                TPG_LAUNCH_CHECK("tile_tma launch");
+                return TPG_OK;
+              }
+            }
             if (NIN == 1)
               launch_tile_f32<k_tile_f32<0, 1, 1, TA, TA>>(p, st, qa, nt0, ntq, nrest, 0);
             else if (x == 1)

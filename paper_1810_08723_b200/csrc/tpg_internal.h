@@ -18,6 +18,10 @@ struct Stream {
   int64_t ncounters = 0;
 };
 
+// cuTensorMapEncodeTiled from the driver (nullptr if unavailable); cast
+// to PFN_cuTensorMapEncodeTiled_v12000 by the caller
+void* tensor_map_encoder();
+
 // at least n zeroed counters, stream-ordered on st
 uint32_t* stream_counters(Stream* st, int64_t n);
 

@@ -95,6 +95,21 @@ uint32_t* device_flags(int device) {
   return g_flags[device];
 }
 
+void* tensor_map_encoder() {
+  static void* fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = p;
+  }
+  return fn;
+}
+
 uint32_t* stream_counters(Stream* st, int64_t n) {
   if (n <= st->ncounters) return st->counters;
   int64_t cap = st->ncounters ? st->ncounters : 4096;

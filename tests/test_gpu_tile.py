@@ -118,3 +118,39 @@ def test_cfg2_full_size_against_numpy():
     got = tp.to_numpy(tp.add(V, R))
     want = (x16.T[::-1, :].astype(np.float64) + r.astype(np.float64)).astype(np.float32)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("tma", ["0", "1"])
+@pytest.mark.parametrize("d", SRC, ids=[x.name for x in SRC])
+def test_tile_reversals(d, tma, monkeypatch):
+    """Both tile kernels (register prefetch, and the opt-in TMA-fed one that
+    maps reversed plan axes to mirrored tensor-map coordinates): every
+    (axis-0 reversed, unit axis reversed) combination, all three Y modes,
+    against the oracle.  TPG_TILE_TMA is read once per process, so the TMA
+    leg runs in a subprocess."""
+    if tma == "1":
+        import subprocess
+        import sys
+        env = dict(__import__("os").environ, TPG_TILE_TMA="1")
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                            f"{__file__}::test_tile_reversals[{d.name}-0]"],
+                           env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        return
+    rng = np.random.default_rng(300 + SRC.index(d))
+    with ShadowOracle() as so:
+        for r0 in (False, True):
+            for rq in (False, True):
+                base = tp.from_numpy(np.asfortranarray(_arr(rng, d, (192, 256))))
+                v = tp.transpose(base)                    # (256, 192), axis 1 unit
+                v = tp.apply_index(v, (slice(None, None, -1 if r0 else 1),
+                                       slice(None, None, -1 if rq else 1)))
+                row = tp.from_numpy(np.asfortranarray(_arr(rng, D.FLOAT, (1, 192))))
+                col = tp.from_numpy(np.asfortranarray(_arr(rng, D.FLOAT, (256, 192))))
+                tp.add(v, row)
+                tp.multiply(row, v)
+                tp.subtract(v, col)
+                tp.add(v, tp.Scalar(2.5, tp.float))
+                tp.cast(v, tp.float)
+    assert so.calls >= 20
+    assert not so.failures, so.failures[:3]

@@ -58,10 +58,28 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.phys = self._pin_device()
         if self.world > 1:
             import torch.distributed as dist
             dist.init_process_group("gloo")
             self.dist = dist
+
+    def _pin_device(self) -> int:
+        """One GPU per process: under torchrun each rank sees only GPU
+        LOCAL_RANK (mod the GPUs present), so the library initialises one
+        device context per process.  Returns the physical index."""
+        if self.world == 1 or "CUDA_VISIBLE_DEVICES" in os.environ:
+            return 0 if self.world == 1 else self.local
+        try:
+            out = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True,
+                                 timeout=30).stdout
+            n = len([ln for ln in out.splitlines() if ln.startswith("GPU ")])
+        except (OSError, subprocess.TimeoutExpired):
+            return self.local
+        if n > 0:
+            os.environ["CUDA_VISIBLE_DEVICES"] = str(self.local % n)
+            return self.local % n
+        return self.local
 
     def barrier(self):
         if self.world > 1:
@@ -391,6 +409,7 @@ def cpu_baseline(steps: int = 3):
     from oracle import oracle
     from paper_1810_08723_b200 import abi
     L = oracle.lib()
+    oracle.set_threads(len(os.sched_getaffinity(0)))  # every core this process may use
     cols = 512
     x16 = np.asfortranarray(np.random.default_rng(3).integers(-1000, 1000, (N, N),
                                                               endpoint=True).astype(np.int16))
@@ -454,8 +473,8 @@ def main():
     devs = tp.list_devices()
     if not devs:
         raise SystemExit("no CUDA device visible")
-    dev = devs[dist.local % len(devs)]
-    clocks = Clocks(dev.index)
+    dev = devs[dist.local % len(devs)] if len(devs) > 1 else devs[0]
+    clocks = Clocks(dist.phys)
     clocks.start()
     dist.barrier()
     ms, e2e_ms, e2e_wall, h2d, d2h = bench_cfg2(tp, dev, args.steps, args.warmup, L)

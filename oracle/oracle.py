@@ -34,6 +34,7 @@ def lib():
             "tpo_arange": [PL, OP],
             "tpo_byteswap": [PL, OP],
             "tpo_threads": [],
+            "tpo_set_threads": [C.c_int],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -53,3 +54,8 @@ def ptr(buf) -> int:
 
 def threads() -> int:
     return lib().tpo_threads()
+
+
+def set_threads(n: int) -> int:
+    lib().tpo_set_threads(int(n))
+    return threads()

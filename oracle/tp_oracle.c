@@ -788,6 +788,16 @@ int tpo_byteswap(const tpg_plan* plan, const tpg_operand* d) {
   return 0;
 }
 
+/* use n host threads (the reference arm runs with every core the process
+   may use, even under torchrun's OMP_NUM_THREADS=1) */
+int tpo_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#endif
+  (void)n;
+  return 0;
+}
+
 int tpo_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

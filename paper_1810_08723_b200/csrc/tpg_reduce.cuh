@@ -691,12 +691,49 @@ __device__ __forceinline__ Vec16<float> ld_vec<float>(const char* ptr) {
   return v;
 }
 
+// Per-thread accumulator of the vector kernels.  min/max are branch-free
+// and index elements relative to the chunk start (32-bit); the reference's
+// "first element NaN" rule is applied separately by the one thread that
+// owns element 0 (first_nan), so the hot loop never tests for it.
+template <int OP>
+struct VAcc {
+  double hi, lo;
+  int idx;  // min/max: chunk-relative index of the best element, -1 = none
+  bool fnan;
+  double nanv;
+  __device__ __forceinline__ void init() {
+    hi = lo = 0.0;
+    idx = -1;
+    fnan = false;
+    nanv = 0.0;
+  }
+  __device__ __forceinline__ void feed(double v, int jr) {
+    if (OP == TPG_RSUM) {
+      dd_add(hi, lo, v);
+    } else if (OP == TPG_RNORM) {
+      const double m = fabs(v);
+      dd_add(hi, lo, __dmul_rn(m, m));
+    } else {
+      const bool better = OP == TPG_RMIN ? v < hi : v > hi;  // false for NaN
+      const bool take = (v == v) && (idx < 0 || better);
+      hi = take ? v : hi;
+      idx = take ? jr : idx;
+    }
+  }
+  __device__ __forceinline__ void first_nan(double v) {
+    if ((OP == TPG_RMIN || OP == TPG_RMAX) && v != v) {
+      fnan = true;
+      nanv = v;
+    }
+  }
+};
+
 struct __align__(16) Part {
   double hi, lo;
 };
 
 template <int OP>
-__device__ __forceinline__ Part to_part(const FAcc<OP, false>& a) {
+__device__ __forceinline__ Part to_part(const VAcc<OP>& a, int64_t jbase) {
   Part r;
   if (OP == TPG_RSUM || OP == TPG_RNORM) {
     r.hi = a.hi;
@@ -706,7 +743,7 @@ __device__ __forceinline__ Part to_part(const FAcc<OP, false>& a) {
     r.lo = __longlong_as_double(-2ll);
   } else {
     r.hi = a.hi;
-    r.lo = __longlong_as_double(a.idx);
+    r.lo = __longlong_as_double(a.idx < 0 ? -1ll : jbase + a.idx);
   }
   return r;
 }
@@ -800,13 +837,14 @@ __device__ __forceinline__ Part block_part(Part t, Part* sh) {
 // 16-byte alignment, pipelined 16-byte body, scalar tail.  Folds into x[NA]
 // (a lane's feeds reach each accumulator in increasing element order).
 template <int OP, typename T, int NL, int NA, int U>
-__device__ __forceinline__ void stream_range(FAcc<OP, false> (&x)[NA], const char* base, int64_t j0,
+__device__ __forceinline__ void stream_range(VAcc<OP> (&x)[NA], const char* base, int64_t j0,
                                              int64_t j1, int li, double pp) {
   constexpr int VE = Vec16<T>::n;
   const uintptr_t a0 = (uintptr_t)(base + j0 * (int64_t)sizeof(T));
   int64_t ja = j0 + (int64_t)(((16 - (a0 & 15)) & 15) / sizeof(T));
   if (ja > j1) ja = j1;
-  if (j0 + li < ja) x[0].feed(ld_real<T>(base + (j0 + li) * (int64_t)sizeof(T)), j0 + li, pp);
+  if (j0 == 0 && li == 0 && pp >= 0.0) x[0].first_nan(ld_real<T>(base));
+  if (j0 + li < ja) x[0].feed(ld_real<T>(base + (j0 + li) * (int64_t)sizeof(T)), li);
   const int64_t nv = (j1 - ja) / VE;
   const char* vb = base + ja * (int64_t)sizeof(T);
   const int64_t nfull = nv / (NL * U);
@@ -824,7 +862,7 @@ __device__ __forceinline__ void stream_range(FAcc<OP, false> (&x)[NA], const cha
       for (int u = 0; u < U; ++u) {
         const int64_t j = ja + (vi + u * NL) * VE;
 #pragma unroll
-        for (int e = 0; e < VE; ++e) x[u % NA].feed((double)v[u].x[e], j + e, pp);
+        for (int e = 0; e < VE; ++e) x[u % NA].feed((double)v[u].x[e], (int)(j - j0) + e);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = nvv[u];
@@ -835,17 +873,17 @@ __device__ __forceinline__ void stream_range(FAcc<OP, false> (&x)[NA], const cha
     const Vec16<T> v = ld_vec<T>(vb + vi * 16);
     const int64_t j = ja + vi * VE;
 #pragma unroll
-    for (int e = 0; e < VE; ++e) x[0].feed((double)v.x[e], j + e, pp);
+    for (int e = 0; e < VE; ++e) x[0].feed((double)v.x[e], (int)(j - j0) + e);
   }
   const int64_t jt = ja + nv * VE + li;
-  if (jt < j1) x[0].feed(ld_real<T>(base + jt * (int64_t)sizeof(T)), jt, pp);
+  if (jt < j1) x[0].feed(ld_real<T>(base + jt * (int64_t)sizeof(T)), (int)(jt - j0));
 }
 
 template <int OP, int NA>
-__device__ __forceinline__ Part fold_accs(FAcc<OP, false> (&x)[NA]) {
-  Part t = to_part<OP>(x[0]);
+__device__ __forceinline__ Part fold_accs(VAcc<OP> (&x)[NA], int64_t jbase) {
+  Part t = to_part<OP>(x[0], jbase);
 #pragma unroll
-  for (int a = 1; a < NA; ++a) t = part_comb<OP>(t, to_part<OP>(x[a]));
+  for (int a = 1; a < NA; ++a) t = part_comb<OP>(t, to_part<OP>(x[a], jbase));
   return t;
 }
 
@@ -866,11 +904,11 @@ __global__ void __launch_bounds__(256, 3) k_red_rows_wv(RedParams p, Part* ws, u
     outer_offsets(p, o, doff, soff);
     const int64_t j0 = c * p.chunk;
     const int64_t j1 = min(p.N, j0 + p.chunk);
-    FAcc<OP, false> x[NA];
+    VAcc<OP> x[NA];
 #pragma unroll
     for (int a = 0; a < NA; ++a) x[a].init();
     stream_range<OP, T, 32, NA, U>(x, p.sbase + soff, j0, j1, lane, p.p);
-    const Part r = warp_part<OP>(fold_accs<OP, NA>(x));
+    const Part r = warp_part<OP>(fold_accs<OP, NA>(x, j0));
     if (p.C == 1) {
       if (lane == 0) acc_store<OP, K_FLT>(p, part_acc<OP>(r), doff, st);
       continue;
@@ -915,11 +953,11 @@ __global__ void __launch_bounds__(256, 3) k_red_rows_v(RedParams p, Part* ws, ui
     outer_offsets(p, o, doff, soff);
     const int64_t j0 = c * p.chunk;
     const int64_t j1 = min(p.N, j0 + p.chunk);
-    FAcc<OP, false> x[NA];
+    VAcc<OP> x[NA];
 #pragma unroll
     for (int a = 0; a < NA; ++a) x[a].init();
     stream_range<OP, T, NT, NA, U>(x, p.sbase + soff, j0, j1, tid, p.p);
-    const Part r = block_part<OP, NT>(fold_accs<OP, NA>(x), sh);
+    const Part r = block_part<OP, NT>(fold_accs<OP, NA>(x, j0), sh);
     if (p.C == 1) {
       if (tid == 0) acc_store<OP, K_FLT>(p, part_acc<OP>(r), doff, st);
       continue;
@@ -968,11 +1006,21 @@ __global__ void __launch_bounds__(NT, 768 / NT) k_red_cols_v(RedParams p, int64_
     const int64_t j0 = c * p.chunk;
     const int64_t j1 = min(p.N, j0 + p.chunk);
     if (act) {
-      FAcc<OP, false> x[VE];
+      // min/max: two accumulators per output (even / odd rows) halve the
+      // compare-select dependency chain; sum/norm keep one (registers)
+      constexpr int NACC = (OP == TPG_RMIN || OP == TPG_RMAX) ? 2 : 1;
+      VAcc<OP> x[VE][NACC];
 #pragma unroll
-      for (int e = 0; e < VE; ++e) x[e].init();
+      for (int e = 0; e < VE; ++e)
+#pragma unroll
+        for (int a = 0; a < NACC; ++a) x[e][a].init();
       const int64_t s0 = p.si[0];
       const char* ptr = p.sbase + soff + j0 * s0;
+      if (j0 == 0 && p.p >= 0.0) {
+        const Vec16<T> f = ld_vec<T>(ptr);
+#pragma unroll
+        for (int e = 0; e < VE; ++e) x[e][0].first_nan((double)f.x[e]);
+      }
       int64_t jb = j0;
       const int64_t nfull = (j1 - j0) / U;
       if (nfull > 0) {
@@ -987,7 +1035,7 @@ __global__ void __launch_bounds__(NT, 768 / NT) k_red_cols_v(RedParams p, int64_
 #pragma unroll
           for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int e = 0; e < VE; ++e) x[e].feed((double)v[u].x[e], jb + u, p.p);
+            for (int e = 0; e < VE; ++e) x[e][u % NACC].feed((double)v[u].x[e], (int)(jb - j0) + u);
 #pragma unroll
           for (int u = 0; u < U; ++u) v[u] = nvv[u];
           jb += U;
@@ -997,11 +1045,12 @@ __global__ void __launch_bounds__(NT, 768 / NT) k_red_cols_v(RedParams p, int64_
       for (; jb < j1; ++jb, ptr += s0) {
         const Vec16<T> v = ld_vec<T>(ptr);
 #pragma unroll
-        for (int e = 0; e < VE; ++e) x[e].feed((double)v.x[e], jb, p.p);
+        for (int e = 0; e < VE; ++e) x[e][0].feed((double)v.x[e], (int)(jb - j0));
       }
 #pragma unroll
       for (int e = 0; e < VE; ++e) {
-        const Part t = to_part<OP>(x[e]);
+        Part t = to_part<OP>(x[e][0], j0);
+        if (NACC > 1) t = part_comb<OP>(t, to_part<OP>(x[e][NACC - 1], j0));
         if (p.C == 1) acc_store<OP, K_FLT>(p, part_acc<OP>(t), doff + e * p.so_d[0], st);
         else st_part(&ws[c * p.O + o + e], t);
       }

@@ -289,4 +289,36 @@ def register(tidepool_module, count: int | None = None):
         ref_devices._devices.extend(devs)
 
     ref_devices.configure = configure
+
+    # descriptor-based raw gather.  The reference builds
+    # a Python list of (dst, src) byte-offset pairs for every clone,
+    # reshape copy and byte-order-preserving transfer (tensors.py:686-699);
+    # for gpu -> same-gpu moves the plugin replaces that with one
+    # canonical plan and the tpg_gather_plan kernel.  tensors._raw_gather
+    # is looked up at call time by its callers (ops.py:115,195,
+    # tensors.contiguous_clone), so rebinding the module attribute is
+    # enough.  Other device pairs keep the reference path (table "gather").
+    ref_tensors = tp.tensors
+    orig_raw_gather = ref_tensors._raw_gather
+
+    def raw_gather(src, dst):
+        if (dst.device.type is gpu_type and src.device is dst.device
+                and src.dtype.size == dst.dtype.size and src.dims == dst.dims):
+            n = 1
+            for e in dst.dims:
+                n *= e
+            if n == 0:
+                return
+            if src.storage.stream is not dst.storage.stream:
+                src.storage.stream.sync()
+            plan = _plan(ref_tensors.canonicalize(dst, src)).to_c()
+            _native.check(L.tpg_gather_plan(None, C.byref(plan), _Buf(dst.storage.view()).ptr,
+                                            dst.offset, _Buf(src.storage.view()).ptr, src.offset,
+                                            src.dtype.size), "gather")
+            _sync()
+            return
+        return orig_raw_gather(src, dst)
+
+    raw_gather.reference = orig_raw_gather
+    ref_tensors._raw_gather = raw_gather
     return devs

@@ -87,3 +87,22 @@ def test_cross_device_round_trip_and_table_counts(tp):
     assert tp.tensors.read_values(back) == [1, 3, 2, 4]
     stats = tp.dispatch.table_stats("core", "gpu")
     assert len(stats) == 31 and stats["copy"] >= 1
+
+
+def test_descriptor_gather_replaces_pair_lists(tp):
+    """gpu -> same-gpu raw gathers (clones, reshape copies) run through
+    tpg_gather_plan instead of the reference's pair list, byte-exact."""
+    gpu = tp.devices.by_name("gpu0")
+    tz = tp.tensors
+    assert getattr(tz._raw_gather, "reference", None) is not None
+    t = tp.cast(tp.arange(24, tp.int16), device=gpu)
+    v = tp.apply_index(tz.reshape(t, (4, 6)), (slice(None, None, -1), slice(1, None, 2)))
+    before = tp.dispatch.table_stats("core", "gpu").get("gather", 0)
+    c = tz.contiguous_clone(v)
+    assert tp.dispatch.table_stats("core", "gpu").get("gather", 0) == before
+    cpu_v = tp.apply_index(tz.reshape(tp.arange(24, tp.int16), (4, 6)),
+                           (slice(None, None, -1), slice(1, None, 2)))
+    assert tz.read_values(c) == tz.read_values(cpu_v)
+    tp.byteswap(c)
+    c2 = tz.contiguous_clone(c)
+    assert c2.byteorder == "big" and tz.read_values(c2) == tz.read_values(cpu_v)

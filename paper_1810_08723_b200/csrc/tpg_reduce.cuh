@@ -695,14 +695,20 @@ __device__ __forceinline__ Vec16<float> ld_vec<float>(const char* ptr) {
 // and index elements relative to the chunk start (32-bit); the reference's
 // "first element NaN" rule is applied separately by the one thread that
 // owns element 0 (first_nan), so the hot loop never tests for it.
-template <int OP>
+// IDX = false (an accumulator fed strictly in element order, e.g. the
+// column kernel): min/max is one fmin/fmax per element with no index;
+// equal extremes are bit-identical except +-0, so when the extreme is zero
+// the caller rescans its range for the first zero (its sign is the
+// reference's answer); "no element yet" is hi = NaN.
+template <int OP, bool IDX = true>
 struct VAcc {
   double hi, lo;
   int idx;  // min/max: chunk-relative index of the best element, -1 = none
   bool fnan;
   double nanv;
   __device__ __forceinline__ void init() {
-    hi = lo = 0.0;
+    hi = (IDX || OP == TPG_RSUM || OP == TPG_RNORM) ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
+    lo = 0.0;
     idx = -1;
     fnan = false;
     nanv = 0.0;
@@ -713,11 +719,17 @@ struct VAcc {
     } else if (OP == TPG_RNORM) {
       const double m = fabs(v);
       dd_add(hi, lo, __dmul_rn(m, m));
-    } else {
+    } else if (IDX) {
       const bool better = OP == TPG_RMIN ? v < hi : v > hi;  // false for NaN
       const bool take = (v == v) && (idx < 0 || better);
       hi = take ? v : hi;
       idx = take ? jr : idx;
+    } else {
+      // one DMNMX: NaN operands are ignored (hi NaN = empty), so this is the
+      // extreme over the non-NaN elements; the only case where "first of
+      // equal elements" is observable is a +-0 extreme, which the caller
+      // resolves by rescanning (zero_first)
+      hi = OP == TPG_RMIN ? fmin(hi, v) : fmax(hi, v);
     }
   }
   __device__ __forceinline__ void first_nan(double v) {
@@ -732,8 +744,8 @@ struct __align__(16) Part {
   double hi, lo;
 };
 
-template <int OP>
-__device__ __forceinline__ Part to_part(const VAcc<OP>& a, int64_t jbase) {
+template <int OP, bool IDX>
+__device__ __forceinline__ Part to_part(const VAcc<OP, IDX>& a, int64_t jbase) {
   Part r;
   if (OP == TPG_RSUM || OP == TPG_RNORM) {
     r.hi = a.hi;
@@ -741,9 +753,14 @@ __device__ __forceinline__ Part to_part(const VAcc<OP>& a, int64_t jbase) {
   } else if (a.fnan) {
     r.hi = a.nanv;
     r.lo = __longlong_as_double(-2ll);
-  } else {
+  } else if (IDX) {
     r.hi = a.hi;
     r.lo = __longlong_as_double(a.idx < 0 ? -1ll : jbase + a.idx);
+  } else {
+    // in-order accumulator: any index inside the chunk orders it correctly
+    // against the other chunks' partials
+    r.hi = a.hi;
+    r.lo = __longlong_as_double(a.hi == a.hi ? jbase : -1ll);
   }
   return r;
 }
@@ -881,9 +898,9 @@ __device__ __forceinline__ void stream_range(VAcc<OP> (&x)[NA], const char* base
 
 template <int OP, int NA>
 __device__ __forceinline__ Part fold_accs(VAcc<OP> (&x)[NA], int64_t jbase) {
-  Part t = to_part<OP>(x[0], jbase);
+  Part t = to_part(x[0], jbase);
 #pragma unroll
-  for (int a = 1; a < NA; ++a) t = part_comb<OP>(t, to_part<OP>(x[a], jbase));
+  for (int a = 1; a < NA; ++a) t = part_comb<OP>(t, to_part(x[a], jbase));
   return t;
 }
 
@@ -990,7 +1007,7 @@ __global__ void __launch_bounds__(256, 3) k_red_rows_v(RedParams p, Part* ws, ui
 // row chunk.  Partials are chunk-major (ws[c * O + o]) so the finalizing
 // block reads them coalesced, 8 chunks in flight per thread.
 template <int OP, typename T, int NT>
-__global__ void __launch_bounds__(NT, 768 / NT) k_red_cols_v(RedParams p, int64_t nob, Part* ws,
+__global__ void __launch_bounds__(NT, 512 / NT) k_red_cols_v(RedParams p, int64_t nob, Part* ws,
                                                              uint32_t* cnt) {
   constexpr int VE = Vec16<T>::n, U = 4;
   __shared__ int is_last;
@@ -1006,10 +1023,9 @@ __global__ void __launch_bounds__(NT, 768 / NT) k_red_cols_v(RedParams p, int64_
     const int64_t j0 = c * p.chunk;
     const int64_t j1 = min(p.N, j0 + p.chunk);
     if (act) {
-      // min/max: two accumulators per output (even / odd rows) halve the
-      // compare-select dependency chain; sum/norm keep one (registers)
-      constexpr int NACC = (OP == TPG_RMIN || OP == TPG_RMAX) ? 2 : 1;
-      VAcc<OP> x[VE][NACC];
+      // one in-order accumulator per output: min/max need no element index
+      constexpr int NACC = 1;
+      VAcc<OP, false> x[VE][NACC];
 #pragma unroll
       for (int e = 0; e < VE; ++e)
 #pragma unroll
@@ -1022,35 +1038,59 @@ __global__ void __launch_bounds__(NT, 768 / NT) k_red_cols_v(RedParams p, int64_
         for (int e = 0; e < VE; ++e) x[e][0].first_nan((double)f.x[e]);
       }
       int64_t jb = j0;
+      // three rotating batches of U row vectors: two batches (2*U*16 B)
+      // stay in flight while one is folded in, and no register copies
+      // wait on loads
       const int64_t nfull = (j1 - j0) / U;
-      if (nfull > 0) {
-        Vec16<T> v[U], nvv[U];
+      Vec16<T> bA[U], bB[U], bC[U];
+      auto ld = [&](Vec16<T>(&b)[U], int64_t k) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = ld_vec<T>(ptr + u * s0);
-        for (int64_t k = 0; k < nfull; ++k) {
-          if (k + 1 < nfull) {
+        for (int u = 0; u < U; ++u) b[u] = ld_vec<T>(ptr + (k * U + u) * s0);
+      };
+      auto fold = [&](const Vec16<T>(&b)[U], int64_t k) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) nvv[u] = ld_vec<T>(ptr + (U + u) * s0);
-          }
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int e = 0; e < VE; ++e) x[e][u % NACC].feed((double)v[u].x[e], (int)(jb - j0) + u);
-#pragma unroll
-          for (int u = 0; u < U; ++u) v[u] = nvv[u];
-          jb += U;
-          ptr += U * s0;
-        }
+          for (int e = 0; e < VE; ++e) x[e][0].feed((double)b[u].x[e], (int)(k * U + u));
+      };
+      if (nfull > 0) ld(bA, 0);
+      if (nfull > 1) ld(bB, 1);
+      int64_t k = 0;
+      for (; k + 3 <= nfull; k += 3) {
+        if (k + 2 < nfull) ld(bC, k + 2);
+        fold(bA, k);
+        if (k + 3 < nfull) ld(bA, k + 3);
+        fold(bB, k + 1);
+        if (k + 4 < nfull) ld(bB, k + 4);
+        fold(bC, k + 2);
       }
+      if (k < nfull) fold(bA, k);
+      if (k + 1 < nfull) fold(bB, k + 1);
+      jb = j0 + nfull * U;
+      ptr += nfull * U * s0;
       for (; jb < j1; ++jb, ptr += s0) {
         const Vec16<T> v = ld_vec<T>(ptr);
 #pragma unroll
         for (int e = 0; e < VE; ++e) x[e][0].feed((double)v.x[e], (int)(jb - j0));
       }
+      if (OP == TPG_RMIN || OP == TPG_RMAX) {
+        // a +-0 extreme: the sign is that of the first zero in the range
+#pragma unroll 1
+        for (int e = 0; e < VE; ++e) {
+          if (x[e][0].hi != 0.0) continue;
+          const char* q = p.sbase + soff + j0 * s0 + e * (int64_t)sizeof(T);
+          for (int64_t j = j0; j < j1; ++j, q += s0) {
+            const double v = (double)*(const T*)q;
+            if (v == 0.0) {
+              x[e][0].hi = v;
+              break;
+            }
+          }
+        }
+      }
 #pragma unroll
       for (int e = 0; e < VE; ++e) {
-        Part t = to_part<OP>(x[e][0], j0);
-        if (NACC > 1) t = part_comb<OP>(t, to_part<OP>(x[e][NACC - 1], j0));
+        const Part t = to_part(x[e][0], j0);
         if (p.C == 1) acc_store<OP, K_FLT>(p, part_acc<OP>(t), doff + e * p.so_d[0], st);
         else st_part(&ws[c * p.O + o + e], t);
       }
@@ -1120,7 +1160,7 @@ int launch_vec(RedParams& p, Stream* st, bool col, bool& done) {
     constexpr int VE = Vec16<T>::n;
     constexpr int NT = 64;  // 64 x 16 B = 1 KiB of a row per block (measured best)
     const int64_t nob = (p.O + NT * VE - 1) / (NT * VE);
-    const int64_t target = sms * (768 / NT) * 4;  // four waves of resident blocks
+    const int64_t target = sms * (512 / NT) * 4;  // four waves of resident blocks
     int64_t C = (target + nob - 1) / nob;
     if (C > p.N / 32) C = p.N / 32;
     if (C > 64) C = 64;

@@ -79,3 +79,20 @@ def test_reduce_repeatable():
         for _ in range(3):
             b = tp.to_numpy(tp.reduce("sum", X, axes=axes))
             assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def test_signed_zero_ties_keep_first():
+    """min/max ties between -0.0 and +0.0 resolve to the FIRST element in
+    plan order (kernels.py:58-65 via ops.py:527-544), in every kernel."""
+    rng = np.random.default_rng(15)
+    x = -rng.random((2500, 1030))            # all negative ...
+    z = rng.random((2500, 1030)) < 0.5
+    x[:, ::3] = np.where(z[:, ::3], -0.0, 0.0)   # ... some columns all-zero, random signs
+    x[::7, :] = np.where(z[::7, :], -0.0, 0.0)   # ... and some rows
+    with ShadowOracle() as so:
+        for arr in (x, -x):
+            X = tp.from_numpy(np.asfortranarray(arr))
+            for op in ("minimum", "maximum"):
+                for axes in ((0,), (1,), None):
+                    tp.reduce(op, X, axes=axes)
+    assert not so.failures, so.failures[:3]

@@ -866,26 +866,35 @@ __device__ __forceinline__ void stream_range(VAcc<OP> (&x)[NA], const char* base
   const char* vb = base + ja * (int64_t)sizeof(T);
   const int64_t nfull = nv / (NL * U);
   int64_t vi = li;
-  if (nfull > 0) {
-    Vec16<T> v[U], nvv[U];
+  // three rotating batches: two batches of U vectors in flight while one
+  // is folded in (no register copies waiting on loads)
+  Vec16<T> bA[U], bB[U], bC[U];
+  auto ld = [&](Vec16<T>(&b)[U], int64_t k) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = ld_vec<T>(vb + (vi + u * NL) * 16);
-    for (int64_t k = 0; k < nfull; ++k) {
-      if (k + 1 < nfull) {
+    for (int u = 0; u < U; ++u) b[u] = ld_vec<T>(vb + (li + (k * U + u) * NL) * 16);
+  };
+  auto fold = [&](const Vec16<T>(&b)[U], int64_t k) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) nvv[u] = ld_vec<T>(vb + (vi + (U + u) * NL) * 16);
-      }
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = ja + (li + (k * U + u) * NL) * VE;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t j = ja + (vi + u * NL) * VE;
-#pragma unroll
-        for (int e = 0; e < VE; ++e) x[u % NA].feed((double)v[u].x[e], (int)(j - j0) + e);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = nvv[u];
-      vi += NL * U;
+      for (int e = 0; e < VE; ++e) x[u % NA].feed((double)b[u].x[e], (int)(j - j0) + e);
     }
+  };
+  if (nfull > 0) ld(bA, 0);
+  if (nfull > 1) ld(bB, 1);
+  int64_t k = 0;
+  for (; k + 3 <= nfull; k += 3) {
+    if (k + 2 < nfull) ld(bC, k + 2);
+    fold(bA, k);
+    if (k + 3 < nfull) ld(bA, k + 3);
+    fold(bB, k + 1);
+    if (k + 4 < nfull) ld(bB, k + 4);
+    fold(bC, k + 2);
   }
+  if (k < nfull) fold(bA, k);
+  if (k + 1 < nfull) fold(bB, k + 1);
+  vi = li + nfull * U * NL;
   for (; vi < nv; vi += NL) {
     const Vec16<T> v = ld_vec<T>(vb + vi * 16);
     const int64_t j = ja + vi * VE;
@@ -908,7 +917,7 @@ __device__ __forceinline__ Part fold_accs(VAcc<OP> (&x)[NA], int64_t jbase) {
 // outputs, e.g. cfg3 axis 0).  Warps never synchronise with each other, so
 // one warp's drain overlaps the others' streaming.
 template <int OP, typename T>
-__global__ void __launch_bounds__(256, 3) k_red_rows_wv(RedParams p, Part* ws, uint32_t* cnt) {
+__global__ void __launch_bounds__(256, 2) k_red_rows_wv(RedParams p, Part* ws, uint32_t* cnt) {
   constexpr int U = 4, NA = 2;
   uint32_t st = 0;
   const int lane = threadIdx.x & 31;
@@ -957,7 +966,7 @@ __global__ void __launch_bounds__(256, 3) k_red_rows_wv(RedParams p, Part* ws, u
 // Row mode, block granularity: one block per (output, chunk) (few outputs,
 // e.g. full reductions).
 template <int OP, typename T>
-__global__ void __launch_bounds__(256, 3) k_red_rows_v(RedParams p, Part* ws, uint32_t* cnt) {
+__global__ void __launch_bounds__(256, 2) k_red_rows_v(RedParams p, Part* ws, uint32_t* cnt) {
   constexpr int U = 4, NA = 2, NT = 256;
   __shared__ Part sh[NT / 32];
   __shared__ int is_last;
@@ -1172,7 +1181,7 @@ int launch_vec(RedParams& p, Stream* st, bool col, bool& done) {
     k_red_cols_v<OP, T, NT><<<(int)std::min<int64_t>(work, 1 << 30), NT, 0, st->s>>>(p, nob, ws, cnt);
   } else {
     if (!rows_vec_ok<T>(p)) return TPG_OK;
-    const int64_t wslots = sms * 3 * 8;  // resident warps
+    const int64_t wslots = sms * 2 * 8;  // resident warps
     if (p.O >= wslots / 2) {
       // warp items: enough outputs to fill the machine; split each output
       // only as far as needed for about two warp items per slot
@@ -1188,7 +1197,7 @@ int launch_vec(RedParams& p, Stream* st, bool col, bool& done) {
       const int64_t warps = std::min<int64_t>(p.O * p.C, wslots);
       k_red_rows_wv<OP, T><<<(int)((warps + 7) / 8), 256, 0, st->s>>>(p, ws, cnt);
     } else {
-      const int64_t target = sms * 3 * 2;  // two waves of resident blocks
+      const int64_t target = sms * 2 * 2;  // two waves of resident blocks
       int64_t C = (target + p.O - 1) / p.O;
       const int64_t minchunk = 16384;
       if (C > (p.N + minchunk - 1) / minchunk) C = (p.N + minchunk - 1) / minchunk;

@@ -568,6 +568,37 @@ __global__ void __launch_bounds__(256) k_tf32_split(const char* __restrict__ src
   }
 }
 
+// K-contiguous, 16-B aligned source rows: straight 16-B vector pass
+__global__ void __launch_bounds__(256) k_tf32_split_vec(const char* __restrict__ src, int64_t rows,
+                                                        int64_t k4, int64_t rs, int64_t bs,
+                                                        int64_t batch, int swap, int64_t pitch,
+                                                        float* __restrict__ hi,
+                                                        float* __restrict__ lo) {
+  const int64_t total = rows * k4 * batch;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = e % k4, r = e / k4;
+    const int64_t row = r % rows, b = r / rows;
+    uint4 u = __ldcs((const uint4*)(src + b * bs + row * rs) + v);
+    if (swap) {
+      u.x = __byte_perm(u.x, 0, 0x0123); u.y = __byte_perm(u.y, 0, 0x0123);
+      u.z = __byte_perm(u.z, 0, 0x0123); u.w = __byte_perm(u.w, 0, 0x0123);
+    }
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    float h[4], l[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float x = __uint_as_float(w[i]);
+      const float hh = __uint_as_float(w[i] & 0xffffe000u);
+      h[i] = isfinite(x) ? hh : x;
+      l[i] = isfinite(x) ? __fsub_rn(x, hh) : 0.0f;
+    }
+    const int64_t d = (b * rows + row) * pitch + v * 4;
+    __stcs((float4*)(hi + d), make_float4(h[0], h[1], h[2], h[3]));
+    __stcs((float4*)(lo + d), make_float4(l[0], l[1], l[2], l[3]));
+  }
+}
+
 static int split_tf32(Stream* st, const tpg_operand* src, int64_t rows, int64_t k, int64_t batch,
                       int64_t rs, int64_t ks, int64_t bs, void** out, OpView* hi, OpView* lo) {
   const int64_t kp = (k + 3) & ~(int64_t)3;
@@ -577,10 +608,18 @@ static int split_tf32(Stream* st, const tpg_operand* src, int64_t rows, int64_t 
   float* l = h + n;
   const char* sb = (const char*)src->base + src->offset;
   const bool rows_fast = (rs == 4 || rs == -4) && ks != 4;
-  const dim3 grid((unsigned)((k + 31) / 32), (unsigned)((rows + 31) / 32), (unsigned)batch);
-  if (grid.y > 65535 || grid.z > 65535) return arg_fail("tf32 split: operand too large");
-  k_tf32_split<<<grid, dim3(32, 8), 0, st->s>>>(sb, rows, k, rs, ks, bs, rows_fast, src->big_endian,
-                                                kp, h, l);
+  if (ks == 4 && k % 4 == 0 && rs % 16 == 0 && (batch == 1 || bs % 16 == 0) && rs > 0 &&
+      (uintptr_t)sb % 16 == 0) {
+    const int64_t total = rows * (k / 4) * batch;
+    const int g = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count(st->device) * 8);
+    k_tf32_split_vec<<<g, 256, 0, st->s>>>(sb, rows, k / 4, rs, bs, batch, src->big_endian, kp,
+                                           h, l);
+  } else {
+    const dim3 grid((unsigned)((k + 31) / 32), (unsigned)((rows + 31) / 32), (unsigned)batch);
+    if (grid.y > 65535 || grid.z > 65535) return arg_fail("tf32 split: operand too large");
+    k_tf32_split<<<grid, dim3(32, 8), 0, st->s>>>(sb, rows, k, rs, ks, bs, rows_fast,
+                                                  src->big_endian, kp, h, l);
+  }
   TPG_LAUNCH_CHECK("tf32 split");
   OpView v;
   v.rows = rows; v.k = k; v.batch = batch;

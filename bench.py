@@ -403,6 +403,64 @@ def cfg4(tp, dev, run):
     del Ab, Bb, Cb
 
 
+def sharded_extras(tp, dev, L, dist, steps=5, warmup=3):
+    """N>1: the sharded paths of SURVEY §8e measured across all ranks (max
+    over ranks of device time per step, whole-job aggregate bytes):
+    cfg3 full sum of the f64 8192^2 matrix split along axis 1 (local
+    single-pass reduction + ONE NCCL all-reduce over NVLink), and cfg5's
+    fused multiply-add chain on 2^30 f32 elements split into slabs."""
+    from paper_1810_08723_b200.sharded import NcclComm, Sharded
+    import torch.distributed as tdist
+    res = {}
+    stream = dev.default_stream()
+
+    def share(uid):
+        if dist.world == 1:
+            return uid
+        obj = [uid]
+        tdist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def timed(step):
+        for _ in range(warmup):
+            step()
+        stream.sync()
+        dist.barrier()
+        ms = timed_steps(L, stream, step, steps, None, gate=False)
+        dist.barrier()
+        return dist.max(statistics.median(ms))
+
+    try:
+        comm = NcclComm(dev, dist.rank, dist.world, share)
+        n = 8192
+        cols = np.random.default_rng(5).random((n, n))  # same matrix on every rank
+        S = Sharded.from_numpy(cols, dist.rank, dist.world, dev, axis=1)
+        del cols
+        total = {}
+
+        def red():
+            total["v"] = S.reduce_full("sum", comm)
+        m = timed(red)
+        res[f"cfg3_sum_full_f64_8192^2_sharded_{dist.world}gpu_nccl"] = {
+            "ms": round(m, 4), "GB/s": round(n * n * 8 / m / 1e6, 1)}
+        comm.close()
+    except Exception as exc:  # pragma: no cover - reported, not fatal
+        res["cfg3_sharded_error"] = repr(exc)[:200]
+    try:
+        per = (1 << 30) // dist.world
+        Y = tp.tensor_create((per,), tp.float, dev)
+        tp.fill(Y, 1.25)
+        Z = tp.tensor_create((per,), tp.float, dev)
+        k15, km2 = tp.Scalar(1.5, tp.float), tp.Scalar(-2.0, tp.float)
+        m = timed(lambda: tp.chain(Y, [("multiply", k15), ("add", km2)], dest=Z))
+        res[f"cfg5_chain_f32_2^30_sharded_{dist.world}gpu"] = {
+            "ms": round(m, 4), "GB/s": round(dist.world * per * 8 / m / 1e6, 1)}
+        del Y, Z
+    except Exception as exc:  # pragma: no cover
+        res["cfg5_sharded_error"] = repr(exc)[:200]
+    return res
+
+
 def cpu_baseline(steps: int = 3):
     """Reference CPU implementation (oracle/tp_oracle.c, all host threads)
     on a bounded cfg2 sample: 512 of the 4096 columns (2,097,152 elements)."""
@@ -488,6 +546,8 @@ def main():
     work = {}
     if dist.rank == 0 and dist.world == 1 and not args.no_extras:
         work = extras(tp, dev, L)
+    elif dist.world > 1 and not args.no_extras:
+        work = sharded_extras(tp, dev, L, dist)
     clk = clocks.stop()
     if dist.rank == 0:
         traffic = None

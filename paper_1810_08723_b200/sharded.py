@@ -88,6 +88,12 @@ class NcclComm:
         s.sync()
         return out
 
+    def allreduce_device(self, ptr: int, count: int, op: int, stream) -> None:
+        """In-place all-reduce of `count` doubles already on this device,
+        enqueued on `stream` (no host round trip)."""
+        _native.check(_native.lib().tpg_nccl_allreduce(stream.handle, ptr, count, 11, op),
+                      "allreduce")
+
     def close(self):
         _native.lib().tpg_nccl_destroy()
 
@@ -153,6 +159,22 @@ class Sharded:
         from . import tensors as tz
         t = self.local
         has = t.nelem > 0
+        if op in ("sum", "norm") and hasattr(comm, "allreduce_device") and (op == "sum" or p == 2.0):
+            # device-resident finish: the local kernel writes its partial to
+            # a device double, NCCL sums it in place, one read at the end
+            dst = _scalar_double(t)
+            if has:
+                if op == "sum":
+                    ops.reduce("sum", t, dest=dst)
+                else:
+                    ops.reduce("norm", t, dest=dst, p=2.0)
+                    ops.multiply(dst, dst, dest=dst)  # |x|_2^2, exact enough (1 ulp)
+            else:
+                ops.fill(dst, 0.0)
+            st = dst.storage.stream
+            comm.allreduce_device(dst.storage.ptr + dst.offset, 1, SUM, st)
+            s = float(dst.item())
+            return s if op == "sum" else math.sqrt(s)
         if op in ("sum", "norm"):
             part = (_local_sum(t) if op == "sum" else _local_power_sum(t, p)) if has else 0.0
             return combine_partials(op, part, comm, p=p)

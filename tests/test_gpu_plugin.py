@@ -106,3 +106,43 @@ def test_descriptor_gather_replaces_pair_lists(tp):
     tp.byteswap(c)
     c2 = tz.contiguous_clone(c)
     assert c2.byteorder == "big" and tz.read_values(c2) == tz.read_values(cpu_v)
+
+
+def _program2(tp, seed, device):
+    """Mixed dtypes, byte order, reductions over each axis, casts: the
+    reference's own pipeline (promotion, implicit casts, aliasing clones)
+    with the gpu table underneath."""
+    tz = tp.tensors
+    st = random.Random(1000 + seed)
+    dts = [tp.int8, tp.int16, tp.int32, tp.uint8, tp.float, tp.double, tp.half]
+    out = []
+    a = tp.tensor_create((5, 4), st.choice(dts), device)
+    b = tp.tensor_create((5, 4), st.choice(dts), device)
+    for t in (a, b):
+        _, pack = tp.dtypes.codec(t.dtype, t.byteorder)
+        buf = t.storage.view()
+        for off in tz.iter_offsets(t):
+            v = st.randint(-20, 20)
+            if t.dtype is tp.uint8:
+                v = abs(v)
+            pack(buf, off, float(v) if t.dtype in (tp.float, tp.double, tp.half) else v)
+    if st.random() < 0.5:
+        tp.byteswap(b)
+    out.append(tp.add(a, b))
+    out.append(tp.multiply(tp.transpose(a), tp.transpose(b)))
+    out.append(tp.maximum(a, tp.apply_index(b, (slice(None, None, -1), slice(None)))))
+    out.append(tp.cast(tp.subtract(a, b), tp.int16))
+    for op in ("sum", "minimum", "maximum"):
+        for axes in ((0,), (1,), None):
+            out.append(tp.reduce(op, a, axes=axes))
+    out.append(tp.cast(a, tp.double))
+    return [(t.dims, t.dtype.name, tz.read_values(t)) for t in out]
+
+
+def test_reference_mixed_dtype_programs_match_on_gpu(tp):
+    gpu = tp.devices.by_name("gpu0")
+    for seed in range(15):
+        for (cd, ct, cv), (gd, gt, gv) in zip(_program2(tp, seed, tp.cpu()),
+                                              _program2(tp, seed, gpu)):
+            assert cd == gd and ct == gt, (seed, ct, gt)
+            assert all(_eq(x, y, 1e-12) for x, y in zip(cv, gv)), (seed, ct, cv, gv)

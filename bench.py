@@ -240,43 +240,39 @@ def bench_cfg2(tp, dev, steps, warmup, L):
         step()
     stream.sync()
     ms = timed_steps(L, stream, step, steps, flush)
-    # end to end through the public API with host buffers: H2D of the
-    # step's inputs from pinned memory, the op, D2H of the result
-    hx = C.c_void_p()
-    hr = C.c_void_p()
-    ho = C.c_void_p()
-    L.tpg_host_alloc(x16.nbytes, C.byref(hx))
-    L.tpg_host_alloc(r.nbytes, C.byref(hr))
-    L.tpg_host_alloc(N * N * 4, C.byref(ho))
-    C.memmove(hx.value, x16.ctypes.data, x16.nbytes)
-    C.memmove(hr.value, r.ctypes.data, r.nbytes)
-
-    # pipelined over NCH row slabs on two streams: H2D of slab i+1, the add
-    # of slab i and the D2H of slab i-1 overlap (PCIe is full duplex).  V's
-    # rows [r0, r1) are X16's columns [N-r1, N-r0): contiguous host bytes;
-    # the output slab is a pitched 2-D copy.
-    from paper_1810_08723_b200 import table as tb
+    # end to end through the public API with host buffers: every step
+    # uploads its inputs from pinned host memory, runs the op and downloads
+    # the result (tp.pinned / tp.upload / tp.download / tp.use_stream),
+    # pipelined over E2E_CHUNKS row slabs on two streams: the upload of
+    # slab i+1, the add of slab i and the download of slab i-1 overlap
+    # (PCIe is full duplex).  V's rows [r0, r1) are X16's columns
+    # [N-r1, N-r0): a contiguous host run; the output slab is pitched.
+    hx = tp.pinned((N, N), np.int16)
+    hx[...] = x16
+    hr = tp.pinned((1, N), np.float32)
+    hr[...] = r
+    ho = tp.pinned((N, N), np.float32)
     pipe = [dev.create_stream(), dev.create_stream()]
     rows = N // E2E_CHUNKS
     vch = [tp.apply_index(V, (slice(i * rows, (i + 1) * rows), slice(None)))
            for i in range(E2E_CHUNKS)]
     och = [tp.apply_index(out, (slice(i * rows, (i + 1) * rows), slice(None)))
            for i in range(E2E_CHUNKS)]
+    xch = [tp.apply_index(X, (slice(None), slice(N - (i + 1) * rows, N - i * rows)))
+           for i in range(E2E_CHUNKS)]
 
     def e2e_step():
         for s in pipe:
             s.wait_for(stream)
-        L.tpg_memcpy_h2d(R.storage.ptr, hr.value, r.nbytes, pipe[0].handle)
+        tp.upload(hr, R, pipe[0])
         pipe[1].wait_for(pipe[0])
         for i in range(E2E_CHUNKS):
             s = pipe[i % 2]
             c0 = N - (i + 1) * rows
-            L.tpg_memcpy_h2d(X.storage.ptr + c0 * N * 2, hx.value + c0 * N * 2, rows * N * 2,
-                             s.handle)
-            with tb.use_stream(s):
+            tp.upload(hx[:, c0:c0 + rows], xch[i], s)
+            with tp.use_stream(s):
                 tp.add(vch[i], R, dest=och[i])
-            L.tpg_memcpy2d(ho.value + i * rows * 4, N * 4, out.storage.ptr + i * rows * 4, N * 4,
-                           rows * 4, N, s.handle)
+            tp.download(och[i], ho[i * rows:(i + 1) * rows, :], s)
         for s in pipe:
             stream.wait_for(s)
 
@@ -288,11 +284,8 @@ def bench_cfg2(tp, dev, steps, warmup, L):
     e2e_ms = timed_steps(L, stream, e2e_step, e2e_steps, None, gate=False)
     wall = (time.perf_counter() - t0) * 1e3 / e2e_steps
     # correctness spot check against the host result of the same bytes
-    got = np.frombuffer((C.c_char * (N * N * 4)).from_address(ho.value), dtype=np.float32)
     want = (x16.T[::-1, :].astype(np.float64) + r.astype(np.float64)).astype(np.float32)
-    assert np.array_equal(got.reshape((N, N), order="F"), want), "cfg2 e2e result mismatch"
-    for h in (hx, hr, ho):
-        L.tpg_host_free(h.value)
+    assert np.array_equal(ho, want), "cfg2 e2e result mismatch"
     dev.release(flush_buf, stream)
     return ms, e2e_ms, wall, x16.nbytes + r.nbytes, N * N * 4
 

@@ -21,7 +21,8 @@ from .ops import (absolute, add, arange, arccosine, arcsine, array_equal, bytesw
                   frobenius_norm, get_status, identity, inner, logarithm, matmul, matmul_batched, chain,
                   maximum, minimum, multiply, negate, ones, outer, reduce, sine, square_root,
                   subtract, zeros)
-from . import profiling  # noqa: F401
+from . import profiling, transfer  # noqa: F401
+from .transfer import download, pinned, upload, use_stream
 from .otp1 import load_otp1, save_otp1, save_otp1_bytes
 from .plan import IterPlan, build_plan, canonicalize
 from .tensors import (MAX_DIMS, Scalar, Tensor, apply_index, broadcast_to, contiguous_clone,

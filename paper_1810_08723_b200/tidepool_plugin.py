@@ -90,6 +90,17 @@ class _Cudart:
         self.lib.cudaDeviceSynchronize()
         self.lib.cudaFree(self.C.c_void_p(ptr))
 
+    def place_on_device(self, ptr: int, n: int, device: int) -> None:
+        """Preferred location = the GPU and migrate there now, so the first
+        kernel touching a fresh buffer does not page-fault it over
+        (cudaMemAdviseSetPreferredLocation = 3, SetAccessedBy = 5 for the
+        host reads the reference does)."""
+        C = self.C
+        self.lib.cudaMemAdvise(C.c_void_p(ptr), C.c_size_t(n), C.c_int(3), C.c_int(device))
+        self.lib.cudaMemAdvise(C.c_void_p(ptr), C.c_size_t(n), C.c_int(5), C.c_int(-1))
+        self.lib.cudaMemPrefetchAsync(C.c_void_p(ptr), C.c_size_t(n), C.c_int(device), None)
+        self.lib.cudaGetLastError()
+
     def is_device_accessible(self, ptr: int) -> bool:
         """True for device / managed / pinned memory (cudaPointerGetAttributes)."""
         C = self.C
@@ -139,9 +150,20 @@ def register(tidepool_module, count: int | None = None):
             if nbytes < 0:
                 raise tp.errors.AllocationError("negative allocation size")
             self.alloc_count += 1
-            ptr = rt.malloc_managed(nbytes)
-            arr = (C.c_ubyte * max(nbytes, 1)).from_address(ptr)
-            arr._tpg_free = _Free(ptr)  # freed with the last reference
+            size = max(nbytes, 1)
+            # caching: every op allocates its result (and the pipeline its
+            # converted intermediates); reuse managed blocks of the same size
+            # released earlier (the plugin syncs after each table call, so a
+            # released block has no kernel in flight)
+            pool = _cache.setdefault((self.index, size), [])
+            if pool:
+                ptr = pool.pop()
+            else:
+                ptr = rt.malloc_managed(size)
+                if size >= (1 << 20):
+                    rt.place_on_device(ptr, size, self.index)
+            arr = (C.c_ubyte * size).from_address(ptr)
+            arr._tpg_free = _Free(ptr, (self.index, size))  # back to the cache with the last ref
             return arr
 
         @property
@@ -150,13 +172,21 @@ def register(tidepool_module, count: int | None = None):
             props.update(tb_props(self.index))
             return props
 
+    _cache: dict = {}
+    _cache_limit = 64  # blocks kept per (device, size)
+
     class _Free:
-        def __init__(self, ptr):
+        def __init__(self, ptr, key=None):
             self.ptr = ptr
+            self.key = key
 
         def __del__(self):
             try:
-                rt.free(self.ptr)
+                pool = _cache.get(self.key) if self.key is not None else None
+                if pool is not None and len(pool) < _cache_limit:
+                    pool.append(self.ptr)
+                else:
+                    rt.free(self.ptr)
             except Exception:
                 pass
 

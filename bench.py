@@ -341,25 +341,38 @@ def extras(tp, dev, L, warmup=3, steps=5, only=None):
 
 
 def cfg5(tp, dev, run):
-    n5 = 1 << 28  # a quarter of cfg5's 2^30 per step keeps extras short
-    s = np.random.default_rng(8).uniform(-1e3, 1e3, n5).astype(">f8")
-    S = tp.from_numpy(s, dev)
+    """SURVEY cfg5 at its full 2^30 elements: the f64 big-endian source is
+    built on the device from four copies of a 2^28 host-generated slab
+    (keeps host memory at 2 GiB)."""
+    n5 = 1 << 30
+    q = n5 // 4
+    chunk = tp.from_numpy(np.random.default_rng(8).uniform(-1e3, 1e3, q).astype(">f8"), dev)
+    S = tp.tensor_create((n5,), tp.double, dev)
+    S.byteorder = "big"
+    for i in range(4):
+        tp.copy(chunk, tp.apply_index(S, (slice(i * q, (i + 1) * q),)))
+    del chunk
     Y = tp.tensor_create((n5,), tp.float, dev)
-    run("cfg5_cast_f64BE_to_f32_2^28", lambda: tp.copy(S, Y), nbytes=12 * n5, fl=False)
+    run("cfg5_cast_f64BE_to_f32_2^30", lambda: tp.copy(S, Y), nbytes=12 * n5, fl=False)
+    del S
     Z = tp.tensor_create((n5,), tp.float, dev)
     k15, km2 = tp.Scalar(1.5, tp.float), tp.Scalar(-2.0, tp.float)
-    run("cfg5_multiply_scalar_f32_2^28", lambda: tp.multiply(Y, k15, dest=Z), nbytes=8 * n5,
+    run("cfg5_multiply_scalar_f32_2^30", lambda: tp.multiply(Y, k15, dest=Z), nbytes=8 * n5,
         fl=False)
-    run("cfg5_add_scalar_f32_2^28", lambda: tp.add(Z, km2, dest=Y), nbytes=8 * n5, fl=False)
+    run("cfg5_add_scalar_f32_2^30", lambda: tp.add(Z, km2, dest=Y), nbytes=8 * n5, fl=False)
     # the same multiply-then-add as one fused chain (SURVEY §8f item 2):
-    # 8 B/elem moved instead of 16; rate counted on the unfused 16 B/elem
-    # algorithm is 2x this GB/s
-    run("cfg5_chain_mul_add_f32_2^28", lambda: tp.chain(Y, [("multiply", k15), ("add", km2)],
+    # 8 B/elem moved instead of 16
+    run("cfg5_chain_mul_add_f32_2^30", lambda: tp.chain(Y, [("multiply", k15), ("add", km2)],
                                                           dest=Z), nbytes=8 * n5, fl=False)
-    del S, Y, Z
-    s16 = tp.from_numpy(np.random.default_rng(9).integers(-3000, 3000, n5).astype(">i2"), dev)
+    del Y, Z
+    c16 = tp.from_numpy(np.random.default_rng(9).integers(-3000, 3000, q).astype(">i2"), dev)
+    s16 = tp.tensor_create((n5,), tp.int16, dev)
+    s16.byteorder = "big"
+    for i in range(4):
+        tp.copy(c16, tp.apply_index(s16, (slice(i * q, (i + 1) * q),)))
+    del c16
     h16 = tp.tensor_create((n5,), tp.half, dev)
-    run("cfg5_cast_i16BE_to_f16_2^28", lambda: tp.copy(s16, h16), nbytes=4 * n5, fl=False)
+    run("cfg5_cast_i16BE_to_f16_2^30", lambda: tp.copy(s16, h16), nbytes=4 * n5, fl=False)
     del s16, h16
 
 

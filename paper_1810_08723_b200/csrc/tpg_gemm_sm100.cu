@@ -200,6 +200,109 @@ __device__ __forceinline__ void load_operand(uint32_t dst, const CUtensorMap* ma
   }
 }
 
+// Epilogue of one output tile for one CTA: warp (2..5) reads TMEM lanes
+// [32*(warp%4), +32) of accumulator `acc` (BN fp32 columns), converts and
+// stores rows [row_base + 32*(warp%4), +32) x columns [n0, n0 + BN) of D.
+// After the last TMEM read the warp arrives on `tempty` (a shared::cluster
+// address: the local CTA's barrier or the pair leader's).
+template <int BN>
+__device__ __forceinline__ void epilogue_tile(const Sm100Args& g, uint32_t acc, int row_base,
+                                              int n_tile, int batch, int warp, int lane,
+                                              uint8_t* epi_stage, uint32_t tempty, bool remote) {
+  const int q = warp & 3;
+  const int es = dt_size(g.ddt);
+  const int row = row_base + q * 32 + lane;
+  char* dbase = g.d + (int64_t)batch * g.dsb;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t v[32];
+    const uint32_t taddr = acc + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
+    TMEM_LD32(taddr, v);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (c == BN / 32 - 1) {
+      // accumulator fully read: hand it back to the MMA warp
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        if (remote)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty)
+                       : "memory");
+        else
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty) : "memory");
+      }
+    }
+    const int n0 = n_tile * BN + c * 32;
+    const int row0 = row_base + q * 32;
+    if (g.epi == 1 && row0 + 32 <= g.m && n0 + 32 <= g.n) {
+      // column-major destination: transpose the warp's 32x32 chunk
+      // through shared memory so each lane writes 16-B pieces of columns
+      uint8_t* stg = epi_stage;  // this warp's 4 KiB staging slice
+      if (es == 2) {
+        uint16_t* s16 = (uint16_t*)stg;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          s16[j * 32 + lane] = (uint16_t)cvt_out(g.ddt, __uint_as_float(v[j]));
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int j = lane / 4 + 8 * it, part = lane % 4;
+          const uint4 val = *(const uint4*)(s16 + j * 32 + part * 8);
+          *(uint4*)(dbase + (int64_t)(row0 + part * 8) * 2 + (int64_t)(n0 + j) * g.ds1) = val;
+        }
+      } else {
+        uint32_t* s32 = (uint32_t*)stg;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) s32[j * 32 + lane] = cvt_out(g.ddt, __uint_as_float(v[j]));
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int j = lane / 8 + 4 * it, part = lane % 8;
+          const uint4 val = *(const uint4*)(s32 + j * 32 + part * 4);
+          *(uint4*)(dbase + (int64_t)(row0 + part * 4) * 4 + (int64_t)(n0 + j) * g.ds1) = val;
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    if (row < g.m) {
+      char* rp = dbase + (int64_t)row * g.ds0;
+      if (g.epi == 2 && n0 + 32 <= g.n) {
+        // row-major destination: 32 contiguous values per thread
+        if (es == 2) {
+          uint32_t w[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            w[j] = cvt_out(g.ddt, __uint_as_float(v[2 * j])) |
+                   (cvt_out(g.ddt, __uint_as_float(v[2 * j + 1])) << 16);
+          uint4* dst = (uint4*)(rp + (int64_t)n0 * 2);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+        } else {
+          uint4* dst = (uint4*)(rp + (int64_t)n0 * 4);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_uint4(cvt_out(g.ddt, __uint_as_float(v[4 * j])),
+                                cvt_out(g.ddt, __uint_as_float(v[4 * j + 1])),
+                                cvt_out(g.ddt, __uint_as_float(v[4 * j + 2])),
+                                cvt_out(g.ddt, __uint_as_float(v[4 * j + 3])));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = n0 + j;
+          if (n < g.n) {
+            const uint32_t o = cvt_out(g.ddt, __uint_as_float(v[j]));
+            char* pp = rp + (int64_t)n * g.ds1;
+            if (es == 2) *(uint16_t*)pp = (uint16_t)o;
+            else *(uint32_t*)pp = o;
+          }
+        }
+      }
+    }
+  }
+}
+
 // Persistent: one CTA per SM loops over output tiles.  Two TMEM
 // accumulators let the epilogue of tile i overlap the mainloop of tile i+1
 // (tfull/tempty mbarrier pair per accumulator).
@@ -318,9 +421,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else {
-    // epilogue: warp w reads TMEM lanes [32*(w%4), 32*(w%4)+32)
-    const int q = warp & 3;
-    const int es = dt_size(g.ddt);
+    // epilogue warps 2..5
     uint32_t lt = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
       int m_tile, n_tile, batch;
@@ -328,91 +429,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t b = lt & 1, use = lt >> 1;
       mbar_wait(su32(&tfull[b]), use & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int row = m_tile * BM + q * 32 + lane;
-      char* dbase = g.d + (int64_t)batch * g.dsb;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        const uint32_t taddr =
-            tmem + b * G::TMEM_COLS + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
-        TMEM_LD32(taddr, v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c == BN / 32 - 1) {
-          // accumulator fully read: hand it back to the MMA warp
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(su32(&tempty[b]));
-        }
-        const int n0 = n_tile * BN + c * 32;
-        const int row0 = m_tile * BM + q * 32;
-        if (g.epi == 1 && row0 + 32 <= g.m && n0 + 32 <= g.n) {
-          // column-major destination: transpose the warp's 32x32 chunk
-          // through shared memory so each lane writes 16-B pieces of columns
-          uint8_t* stg = epi_stage + (warp - 2) * 4096;
-          if (es == 2) {
-            uint16_t* s16 = (uint16_t*)stg;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              s16[j * 32 + lane] = (uint16_t)cvt_out(g.ddt, __uint_as_float(v[j]));
-            __syncwarp();
-#pragma unroll
-            for (int it = 0; it < 4; ++it) {
-              const int j = lane / 4 + 8 * it, part = lane % 4;
-              const uint4 val = *(const uint4*)(s16 + j * 32 + part * 8);
-              *(uint4*)(dbase + (int64_t)(row0 + part * 8) * 2 + (int64_t)(n0 + j) * g.ds1) = val;
-            }
-          } else {
-            uint32_t* s32 = (uint32_t*)stg;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) s32[j * 32 + lane] = cvt_out(g.ddt, __uint_as_float(v[j]));
-            __syncwarp();
-#pragma unroll
-            for (int it = 0; it < 8; ++it) {
-              const int j = lane / 8 + 4 * it, part = lane % 8;
-              const uint4 val = *(const uint4*)(s32 + j * 32 + part * 4);
-              *(uint4*)(dbase + (int64_t)(row0 + part * 4) * 4 + (int64_t)(n0 + j) * g.ds1) = val;
-            }
-          }
-          __syncwarp();
-          continue;
-        }
-        if (row < g.m) {
-          char* rp = dbase + (int64_t)row * g.ds0;
-          if (g.epi == 2 && n0 + 32 <= g.n) {
-            // row-major destination: 32 contiguous values per thread
-            if (es == 2) {
-              uint32_t w[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                w[j] = cvt_out(g.ddt, __uint_as_float(v[2 * j])) |
-                       (cvt_out(g.ddt, __uint_as_float(v[2 * j + 1])) << 16);
-              uint4* dst = (uint4*)(rp + (int64_t)n0 * 2);
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
-            } else {
-              uint4* dst = (uint4*)(rp + (int64_t)n0 * 4);
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                dst[j] = make_uint4(cvt_out(g.ddt, __uint_as_float(v[4 * j])),
-                                    cvt_out(g.ddt, __uint_as_float(v[4 * j + 1])),
-                                    cvt_out(g.ddt, __uint_as_float(v[4 * j + 2])),
-                                    cvt_out(g.ddt, __uint_as_float(v[4 * j + 3])));
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int n = n0 + j;
-              if (n < g.n) {
-                const uint32_t o = cvt_out(g.ddt, __uint_as_float(v[j]));
-                char* pp = rp + (int64_t)n * g.ds1;
-                if (es == 2) *(uint16_t*)pp = (uint16_t)o;
-                else *(uint32_t*)pp = o;
-              }
-            }
-          }
-        }
-      }
+      epilogue_tile<BN>(g, tmem + b * G::TMEM_COLS, m_tile * BM, n_tile, batch, warp, lane,
+                        epi_stage + (warp - 2) * 4096, su32(&tempty[b]), false);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -33,6 +33,9 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "tpg_common.cuh"
 #include "tpg_internal.h"
 
@@ -541,6 +544,197 @@ static int pack_k_major(Stream* st, const tpg_operand* src, int64_t rows, int64_
   return rc;
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant for half / bfloat16 (tcgen05.mma.cta_group::2): a cluster
+// of 2 CTAs on one TPC computes a 256 x 256 tile.  Each CTA loads its 128
+// rows of A and its 128-row half of B (K-major or MN-major, 128-B swizzle)
+// into its own shared memory, signalling the LEADER's full barrier; the
+// leader's single thread issues M256 N256 K16 MMAs that read both CTAs'
+// operands and write each CTA's 128 accumulator rows into its own TMEM;
+// tcgen05.commit multicasts stage releases / accumulator-ready to both CTAs,
+// and both CTAs' epilogue warps hand the accumulator back by arriving on the
+// leader's tempty barrier.  Per CTA a stage is 32 KiB (vs 48 KiB for the
+// single-CTA 128 x 256 tile), so 6 stages fit.
+constexpr int P_STAGES = 6;
+constexpr int P_HALF = 128 * 64 * 2;  // one CTA's A rows or B half per stage (16 KiB)
+constexpr size_t P_SMEM = 1024 + (size_t)P_STAGES * 2 * P_HALF + 4 * 4096 + 8 * (2 * P_STAGES + 4) + 16;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                 int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void load_half_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                               int kb, int row0, int batch, bool mn) {
+  if (!mn) {
+    tma_load_3d_pair(dst, map, bar, kb * 64, row0, batch);
+  } else {
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+      tma_load_3d_pair(dst + a * (64 * 128), map, bar, row0 + a * 64, kb * 64, batch);
+  }
+}
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+  const uint16_t mask = 0x3;
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(bar), "h"(mask)
+      : "memory");
+}
+
+// tile t of the pair grid: (m256 tile, n256 tile, batch), grouped raster
+__device__ __forceinline__ void pair_tile(int t, const Sm100Args& g, int& m2, int& n2, int& batch) {
+  const int tm = (g.tiles_m + 1) / 2;  // 256-row tiles
+  const int per_batch = tm * g.tiles_n;
+  batch = t / per_batch;
+  t -= batch * per_batch;
+  const int per_group = (GROUP_M / 2) * g.tiles_n;
+  const int group = t / per_group;
+  const int first = group * (GROUP_M / 2);
+  const int gm = min(tm - first, GROUP_M / 2);
+  const int r = t - group * per_group;
+  m2 = first + r % gm;
+  n2 = r / gm;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    k_gemm_sm100_pair(const __grid_constant__ CUtensorMap tma_a,
+                      const __grid_constant__ CUtensorMap tma_b, Sm100Args g, uint32_t idesc,
+                      int ntiles) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* epi_stage = smem + P_STAGES * 2 * P_HALF;
+  uint64_t* bars = (uint64_t*)(epi_stage + 4 * 4096);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + P_STAGES;
+  uint64_t* tfull = bars + 2 * P_STAGES;
+  uint64_t* tempty = bars + 2 * P_STAGES + 2;
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * P_STAGES + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(su32(&full[s]), 1);
+      mbar_init(su32(&empty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(su32(&tfull[b]), 1);
+      mbar_init(su32(&tempty[b]), 8);  // 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_b) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const int nk = (g.k + 63) / 64;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // both CTAs: load own A rows and own B half, complete on the leader's barrier
+      uint32_t it = 0;
+      for (int t = pair; t < ntiles; t += npairs) {
+        int m2, n2, batch;
+        pair_tile(t, g, m2, n2, batch);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % P_STAGES;
+          const uint32_t ph = (it / P_STAGES) & 1;
+          mbar_wait(su32(&empty[s]), ph ^ 1);
+          const uint32_t fb = map_to_rank(su32(&full[s]), 0);
+          if (rank == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                             su32(&full[s])),
+                         "r"(4 * P_HALF)
+                         : "memory");
+          }
+          const uint32_t st0 = su32(smem + s * 2 * P_HALF);
+          load_half_pair(st0, &tma_a, fb, kb, m2 * 256 + rank * 128, batch, g.amn);
+          load_half_pair(st0 + P_HALF, &tma_b, fb, kb, n2 * 256 + rank * 128, batch, g.bmn);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      const uint32_t adv_a = g.amn ? 16 * 128 : 32, adv_b = g.bmn ? 16 * 128 : 32;
+      const uint32_t lbo_a = g.amn ? 64 * 128 : 16, lbo_b = g.bmn ? 64 * 128 : 16;
+      uint32_t it = 0, lt = 0;
+      for (int t = pair; t < ntiles; t += npairs, ++lt) {
+        const uint32_t b = lt & 1, use = lt >> 1;
+        mbar_wait(su32(&tempty[b]), (use & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + b * 256;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % P_STAGES;
+          const uint32_t ph = (it / P_STAGES) & 1;
+          mbar_wait(su32(&full[s]), ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a0 = su32(smem + s * 2 * P_HALF), b0 = a0 + P_HALF;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_pair(acc, umma_desc<128>(a0 + k * adv_a, lbo_a), umma_desc<128>(b0 + k * adv_b, lbo_b),
+                      idesc, (kb | k) != 0);
+          umma_commit_pair(su32(&empty[s]));
+        }
+        umma_commit_pair(su32(&tfull[b]));
+      }
+    }
+  } else {
+    uint32_t lt = 0;
+    const uint32_t te0 = map_to_rank(su32(&tempty[0]), 0), te1 = map_to_rank(su32(&tempty[1]), 0);
+    for (int t = pair; t < ntiles; t += npairs, ++lt) {
+      int m2, n2, batch;
+      pair_tile(t, g, m2, n2, batch);
+      const uint32_t b = lt & 1, use = lt >> 1;
+      mbar_wait(su32(&tfull[b]), use & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      epilogue_tile<256>(g, tmem + b * 256, m2 * 256 + (int)rank * 128, n2, batch, warp, lane,
+                         epi_stage + (warp - 2) * 4096, b ? te1 : te0, true);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 // 3xTF32 operand split: for a (rows x k x batch) f32 view with byte strides
 // (rs, ks, bs), write hi = x with the low 13 mantissa bits cleared (exactly
 // a tf32 value, so the tensor core's own operand rounding cannot matter)
@@ -699,6 +893,56 @@ static int launch_sm100(Stream* st, int64_t batch, const tpg_operand* d, const i
   return 1;
 }
 
+// CTA-pair launch (half / bfloat16); TPG_GEMM_PAIR=0 forces the 1-CTA kernel
+static bool pair_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TPG_GEMM_PAIR");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static int launch_pair(Stream* st, int64_t batch, const tpg_operand* d, const int64_t* ds,
+                       const OpView* av, const OpView* bv, int64_t m, int64_t n, int64_t k,
+                       int adt) {
+  using G = Cfg<0>;
+  CUtensorMap ma, mb;
+  if (!make_map<0>(&ma, adt, av[0], 128) || !make_map<0>(&mb, adt, bv[0], 128)) return 0;
+  Sm100Args g;
+  g.d = (char*)d->base + d->offset;
+  g.ds0 = ds[0];
+  g.ds1 = ds[1];
+  g.dsb = ds[2];
+  g.m = (int)m;
+  g.n = (int)n;
+  g.k = (int)k;
+  g.ddt = d->dtype;
+  const int es = dt_size(d->dtype);
+  const bool al = ((uintptr_t)g.d % 16) == 0;
+  g.epi = (ds[1] == es && ds[0] % 16 == 0 && al) ? 2
+          : (ds[0] == es && ds[1] % 16 == 0 && al && (batch == 1 || ds[2] % 16 == 0)) ? 1 : 0;
+  g.tiles_m = (int)((m + G::BM - 1) / G::BM);
+  g.tiles_n = (int)((n + 255) / 256);
+  g.amn = av[0].mn;
+  g.bmn = bv[0].mn;
+  const uint32_t fmt = adt == TPG_BF16 ? 1u : 0u;
+  const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)g.amn << 15) |
+                         ((uint32_t)g.bmn << 16) | ((uint32_t)(256 >> 3) << 17) |
+                         ((uint32_t)(256 >> 4) << 24);
+  static bool attr_set[64] = {false};
+  if (!attr_set[st->device]) {
+    TPG_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_sm100_pair,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P_SMEM));
+    attr_set[st->device] = true;
+  }
+  const int ntiles = ((g.tiles_m + 1) / 2) * g.tiles_n * (int)batch;
+  const int pairs = std::min(ntiles, sm_count(st->device) / 2);
+  k_gemm_sm100_pair<<<2 * pairs, GEMM_THREADS, P_SMEM, st->s>>>(ma, mb, g, idesc, ntiles);
+  TPG_LAUNCH_CHECK("gemm sm100 pair");
+  return 1;
+}
+
 int gemm_sm100(Stream* st, int64_t batch, const tpg_operand* d, const int64_t* ds,
                const tpg_operand* a, const int64_t* as, const tpg_operand* b, const int64_t* bs,
                int64_t m, int64_t n, int64_t k, int compute, int mode) {
@@ -732,8 +976,11 @@ int gemm_sm100(Stream* st, int64_t batch, const tpg_operand* d, const int64_t* d
     if (rc == TPG_OK && !classify(b, 2, n, k, batch, bs[1], bs[0], bs[2], &bv[0]))
       rc = pack_k_major(st, b, n, k, batch, bs[1], bs[0], bs[2], &bpack, &bv[0]);
   }
-  if (rc == TPG_OK) rc = f32 ? launch_sm100<1>(st, batch, d, ds, av, bv, m, n, k, adt)
-                             : launch_sm100<0>(st, batch, d, ds, av, bv, m, n, k, adt);
+  if (rc == TPG_OK) {
+    if (f32) rc = launch_sm100<1>(st, batch, d, ds, av, bv, m, n, k, adt);
+    else if (pair_enabled() && m >= 256) rc = launch_pair(st, batch, d, ds, av, bv, m, n, k, adt);
+    else rc = launch_sm100<0>(st, batch, d, ds, av, bv, m, n, k, adt);
+  }
   if (apack) cudaFreeAsync(apack, st->s);
   if (bpack) cudaFreeAsync(bpack, st->s);
   return rc;  // 1 handled, 0 not encodable (SIMT path), <0 error

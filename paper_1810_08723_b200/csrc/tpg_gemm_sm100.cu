@@ -555,9 +555,11 @@ static int pack_k_major(Stream* st, const tpg_operand* src, int64_t rows, int64_
 // and both CTAs' epilogue warps hand the accumulator back by arriving on the
 // leader's tempty barrier.  Per CTA a stage is 32 KiB (vs 48 KiB for the
 // single-CTA 128 x 256 tile), so 6 stages fit.
+// MODE 1 (3xTF32) uses the same pair structure with four 8 KiB tiles per
+// CTA and stage (A hi/lo rows, B hi/lo half; 64-B swizzle, K = 16 floats).
 constexpr int P_STAGES = 6;
-constexpr int P_HALF = 128 * 64 * 2;  // one CTA's A rows or B half per stage (16 KiB)
-constexpr size_t P_SMEM = 1024 + (size_t)P_STAGES * 2 * P_HALF + 4 * 4096 + 8 * (2 * P_STAGES + 4) + 16;
+constexpr int P_STAGE = 32768;  // bytes per CTA and stage, both modes
+constexpr size_t P_SMEM = 1024 + (size_t)P_STAGES * P_STAGE + 4 * 4096 + 8 * (2 * P_STAGES + 4) + 16;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -581,23 +583,34 @@ __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap
       "l"((uint64_t)map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+template <int MODE>
 __device__ __forceinline__ void load_half_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                                int kb, int row0, int batch, bool mn) {
+  using G = Cfg<MODE>;
   if (!mn) {
-    tma_load_3d_pair(dst, map, bar, kb * 64, row0, batch);
+    tma_load_3d_pair(dst, map, bar, kb * G::BK, row0, batch);
   } else {
+    constexpr int ATOM = G::SWZ / G::ESZ;
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
-      tma_load_3d_pair(dst + a * (64 * 128), map, bar, row0 + a * 64, kb * 64, batch);
+    for (int a = 0; a < 128 / ATOM; ++a)
+      tma_load_3d_pair(dst + a * (G::BK * G::SWZ), map, bar, row0 + a * ATOM, kb * G::BK, batch);
   }
 }
+template <int MODE>
 __device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                           uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  if constexpr (MODE == 0)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
   const uint16_t mask = 0x3;
@@ -622,13 +635,19 @@ __device__ __forceinline__ void pair_tile(int t, const Sm100Args& g, int& m2, in
   n2 = r / gm;
 }
 
+template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     k_gemm_sm100_pair(const __grid_constant__ CUtensorMap tma_a,
-                      const __grid_constant__ CUtensorMap tma_b, Sm100Args g, uint32_t idesc,
+                      const __grid_constant__ CUtensorMap tma_b,
+                      const __grid_constant__ CUtensorMap tma_al,
+                      const __grid_constant__ CUtensorMap tma_bl, Sm100Args g, uint32_t idesc,
                       int ntiles) {
+  using G = Cfg<MODE>;
+  constexpr int TILE = 128 * G::BK * G::ESZ;  // one 128-row operand tile (16 / 8 KiB)
+  static_assert(TILE * 2 * G::NPART == P_STAGE, "pair stage layout");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* epi_stage = smem + P_STAGES * 2 * P_HALF;
+  uint8_t* epi_stage = smem + P_STAGES * P_STAGE;
   uint64_t* bars = (uint64_t*)(epi_stage + 4 * 4096);
   uint64_t* full = bars;
   uint64_t* empty = bars + P_STAGES;
@@ -650,6 +669,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_b) : "memory");
+    if (MODE) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_al) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_bl) : "memory");
+    }
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -662,7 +685,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   cluster_sync_all();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const int nk = (g.k + 63) / 64;
+  const int nk = (g.k + G::BK - 1) / G::BK;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -679,19 +702,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           if (rank == 0) {
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                              su32(&full[s])),
-                         "r"(4 * P_HALF)
+                         "r"(2 * P_STAGE)
                          : "memory");
           }
-          const uint32_t st0 = su32(smem + s * 2 * P_HALF);
-          load_half_pair(st0, &tma_a, fb, kb, m2 * 256 + rank * 128, batch, g.amn);
-          load_half_pair(st0 + P_HALF, &tma_b, fb, kb, n2 * 256 + rank * 128, batch, g.bmn);
+          const uint32_t st0 = su32(smem + s * P_STAGE);
+          const int ra = m2 * 256 + rank * 128, rb = n2 * 256 + rank * 128;
+          load_half_pair<MODE>(st0, &tma_a, fb, kb, ra, batch, g.amn);
+          load_half_pair<MODE>(st0 + TILE, &tma_b, fb, kb, rb, batch, g.bmn);
+          if (MODE) {
+            load_half_pair<MODE>(st0 + 2 * TILE, &tma_al, fb, kb, ra, batch, g.amn);
+            load_half_pair<MODE>(st0 + 3 * TILE, &tma_bl, fb, kb, rb, batch, g.bmn);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      const uint32_t adv_a = g.amn ? 16 * 128 : 32, adv_b = g.bmn ? 16 * 128 : 32;
-      const uint32_t lbo_a = g.amn ? 64 * 128 : 16, lbo_b = g.bmn ? 64 * 128 : 16;
+      const uint32_t adv_a = g.amn ? G::KI * G::SWZ : G::KI * G::ESZ;
+      const uint32_t adv_b = g.bmn ? G::KI * G::SWZ : G::KI * G::ESZ;
+      const uint32_t lbo_a = g.amn ? G::BK * G::SWZ : 16, lbo_b = g.bmn ? G::BK * G::SWZ : 16;
       uint32_t it = 0, lt = 0;
       for (int t = pair; t < ntiles; t += npairs, ++lt) {
         const uint32_t b = lt & 1, use = lt >> 1;
@@ -703,11 +732,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           const uint32_t ph = (it / P_STAGES) & 1;
           mbar_wait(su32(&full[s]), ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t a0 = su32(smem + s * 2 * P_HALF), b0 = a0 + P_HALF;
+          const uint32_t a0 = su32(smem + s * P_STAGE), b0 = a0 + TILE;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_pair(acc, umma_desc<128>(a0 + k * adv_a, lbo_a), umma_desc<128>(b0 + k * adv_b, lbo_b),
-                      idesc, (kb | k) != 0);
+          for (int k = 0; k < G::BK / G::KI; ++k) {
+            const uint64_t ad = umma_desc<G::SWZ>(a0 + k * adv_a, lbo_a);
+            const uint64_t bd = umma_desc<G::SWZ>(b0 + k * adv_b, lbo_b);
+            const uint32_t accum = (kb | k) != 0;
+            if (MODE == 0) {
+              umma_pair<MODE>(acc, ad, bd, idesc, accum);
+            } else {
+              const uint64_t adl = umma_desc<G::SWZ>(a0 + 2 * TILE + k * adv_a, lbo_a);
+              const uint64_t bdl = umma_desc<G::SWZ>(a0 + 3 * TILE + k * adv_b, lbo_b);
+              umma_pair<MODE>(acc, adl, bd, idesc, accum);  // small terms first
+              umma_pair<MODE>(acc, ad, bdl, idesc, 1);
+              umma_pair<MODE>(acc, ad, bd, idesc, 1);
+            }
+          }
           umma_commit_pair(su32(&empty[s]));
         }
         umma_commit_pair(su32(&tfull[b]));
@@ -903,12 +943,19 @@ static bool pair_enabled() {
   return v == 1;
 }
 
+template <int MODE>
 static int launch_pair(Stream* st, int64_t batch, const tpg_operand* d, const int64_t* ds,
                        const OpView* av, const OpView* bv, int64_t m, int64_t n, int64_t k,
                        int adt) {
-  using G = Cfg<0>;
-  CUtensorMap ma, mb;
-  if (!make_map<0>(&ma, adt, av[0], 128) || !make_map<0>(&mb, adt, bv[0], 128)) return 0;
+  using G = Cfg<MODE>;
+  CUtensorMap ma, mb, mal, mbl;
+  if (!make_map<MODE>(&ma, adt, av[0], 128) || !make_map<MODE>(&mb, adt, bv[0], 128)) return 0;
+  if (MODE) {
+    if (!make_map<MODE>(&mal, adt, av[1], 128) || !make_map<MODE>(&mbl, adt, bv[1], 128)) return 0;
+  } else {
+    mal = ma;
+    mbl = mb;
+  }
   Sm100Args g;
   g.d = (char*)d->base + d->offset;
   g.ds0 = ds[0];
@@ -926,19 +973,20 @@ static int launch_pair(Stream* st, int64_t batch, const tpg_operand* d, const in
   g.tiles_n = (int)((n + 255) / 256);
   g.amn = av[0].mn;
   g.bmn = bv[0].mn;
-  const uint32_t fmt = adt == TPG_BF16 ? 1u : 0u;
+  const uint32_t fmt = MODE ? 2u : adt == TPG_BF16 ? 1u : 0u;
   const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)g.amn << 15) |
                          ((uint32_t)g.bmn << 16) | ((uint32_t)(256 >> 3) << 17) |
                          ((uint32_t)(256 >> 4) << 24);
   static bool attr_set[64] = {false};
   if (!attr_set[st->device]) {
-    TPG_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_sm100_pair,
+    TPG_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_sm100_pair<MODE>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P_SMEM));
     attr_set[st->device] = true;
   }
   const int ntiles = ((g.tiles_m + 1) / 2) * g.tiles_n * (int)batch;
   const int pairs = std::min(ntiles, sm_count(st->device) / 2);
-  k_gemm_sm100_pair<<<2 * pairs, GEMM_THREADS, P_SMEM, st->s>>>(ma, mb, g, idesc, ntiles);
+  k_gemm_sm100_pair<MODE><<<2 * pairs, GEMM_THREADS, P_SMEM, st->s>>>(ma, mb, mal, mbl, g, idesc,
+                                                                      ntiles);
   TPG_LAUNCH_CHECK("gemm sm100 pair");
   return 1;
 }
@@ -977,9 +1025,11 @@ int gemm_sm100(Stream* st, int64_t batch, const tpg_operand* d, const int64_t* d
       rc = pack_k_major(st, b, n, k, batch, bs[1], bs[0], bs[2], &bpack, &bv[0]);
   }
   if (rc == TPG_OK) {
-    if (f32) rc = launch_sm100<1>(st, batch, d, ds, av, bv, m, n, k, adt);
-    else if (pair_enabled() && m >= 256) rc = launch_pair(st, batch, d, ds, av, bv, m, n, k, adt);
-    else rc = launch_sm100<0>(st, batch, d, ds, av, bv, m, n, k, adt);
+    const bool pair = pair_enabled() && m >= 256;
+    if (f32) rc = pair ? launch_pair<1>(st, batch, d, ds, av, bv, m, n, k, adt)
+                       : launch_sm100<1>(st, batch, d, ds, av, bv, m, n, k, adt);
+    else rc = pair ? launch_pair<0>(st, batch, d, ds, av, bv, m, n, k, adt)
+                   : launch_sm100<0>(st, batch, d, ds, av, bv, m, n, k, adt);
   }
   if (apack) cudaFreeAsync(apack, st->s);
   if (bpack) cudaFreeAsync(bpack, st->s);

@@ -12,7 +12,9 @@ timeout 600 python bench.py --steps 50 --warmup 5 > gpurun_out/bench.json 2> gpu
 echo "bench rc=$?" >> gpurun_out/bench.err
 timeout 300 python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err
 if [ "${NCU:-1}" = "1" ]; then
-timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 > gpurun_out/ncu_bench.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_cfg2.csv python bench.py --steps 5 --warmup 3 --no-extras > gpurun_out/ncu_bench_cfg2.log 2>&1
+echo "ncu rc=$?" >> gpurun_out/ncu_bench_cfg2.log
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 > gpurun_out/ncu_bench.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_bench.log
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_tile -s 3 -c 1 -o gpurun_out/prof_cfg2 -f python bench.py --steps 3 --warmup 3 --no-extras > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?" >> gpurun_out/ncu_full.log

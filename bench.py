@@ -38,7 +38,8 @@ METRIC = "elementwise/reduce HBM GB/s vs ~8 TB/s; gemm TFLOP/s; at 1/2/4/8 B200"
 N = 4096
 CFG2_BYTES = N * N * (2 + 4) + N * 4
 FLUSH_BYTES = 256 << 20
-E2E_CHUNKS = 8  # row slabs of the pipelined host-to-host e2e step
+E2E_CHUNKS = int(os.environ.get("TPG_E2E_CHUNKS", "8"))  # slabs of the pipelined e2e step
+E2E_SPLIT = os.environ.get("TPG_E2E_SPLIT", "cols")  # "rows" | "cols" of the cfg2 result
 
 
 def peaks():
@@ -243,38 +244,55 @@ def bench_cfg2(tp, dev, steps, warmup, L):
     # end to end through the public API with host buffers: every step
     # uploads its inputs from pinned host memory, runs the op and downloads
     # the result (tp.pinned / tp.upload / tp.download / tp.use_stream),
-    # pipelined over E2E_CHUNKS row slabs on two streams: the upload of
-    # slab i+1, the add of slab i and the download of slab i-1 overlap
-    # (PCIe is full duplex).  V's rows [r0, r1) are X16's columns
-    # [N-r1, N-r0): a contiguous host run; the output slab is pitched.
+    # pipelined over E2E_CHUNKS slabs on three streams -- one per copy
+    # engine direction plus one for the kernels -- chained by per-slab
+    # waits: uploads run back to back on the H2D engine, downloads back to
+    # back on the D2H engine (PCIe is full duplex), so the step costs about
+    # one slab upload + the whole download (E2E_SPLIT picks the slab shape).
     hx = tp.pinned((N, N), np.int16)
     hx[...] = x16
     hr = tp.pinned((1, N), np.float32)
     hr[...] = r
     ho = tp.pinned((N, N), np.float32)
-    pipe = [dev.create_stream(), dev.create_stream()]
+    up, comp, down = dev.create_stream(), dev.create_stream(), dev.create_stream()
     rows = N // E2E_CHUNKS
-    vch = [tp.apply_index(V, (slice(i * rows, (i + 1) * rows), slice(None)))
-           for i in range(E2E_CHUNKS)]
-    och = [tp.apply_index(out, (slice(i * rows, (i + 1) * rows), slice(None)))
-           for i in range(E2E_CHUNKS)]
-    xch = [tp.apply_index(X, (slice(None), slice(N - (i + 1) * rows, N - i * rows)))
-           for i in range(E2E_CHUNKS)]
+    if E2E_SPLIT == "rows":
+        # V's rows [r0, r1) = X16's columns [N-r1, N-r0): contiguous upload,
+        # pitched download
+        vch = [tp.apply_index(V, (slice(i * rows, (i + 1) * rows), slice(None)))
+               for i in range(E2E_CHUNKS)]
+        och = [tp.apply_index(out, (slice(i * rows, (i + 1) * rows), slice(None)))
+               for i in range(E2E_CHUNKS)]
+        xch = [tp.apply_index(X, (slice(None), slice(N - (i + 1) * rows, N - i * rows)))
+               for i in range(E2E_CHUNKS)]
+        hxs = [hx[:, N - (i + 1) * rows:N - i * rows] for i in range(E2E_CHUNKS)]
+        hos = [ho[i * rows:(i + 1) * rows, :] for i in range(E2E_CHUNKS)]
+        rch = [R] * E2E_CHUNKS
+    else:
+        # V's columns [c0, c1) = X16's rows [c0, c1): pitched upload,
+        # contiguous download (the larger direction)
+        vch = [tp.apply_index(V, (slice(None), slice(i * rows, (i + 1) * rows)))
+               for i in range(E2E_CHUNKS)]
+        och = [tp.apply_index(out, (slice(None), slice(i * rows, (i + 1) * rows)))
+               for i in range(E2E_CHUNKS)]
+        xch = [tp.apply_index(X, (slice(i * rows, (i + 1) * rows), slice(None)))
+               for i in range(E2E_CHUNKS)]
+        hxs = [hx[i * rows:(i + 1) * rows, :] for i in range(E2E_CHUNKS)]
+        hos = [ho[:, i * rows:(i + 1) * rows] for i in range(E2E_CHUNKS)]
+        rch = [tp.apply_index(R, (slice(None), slice(i * rows, (i + 1) * rows)))
+               for i in range(E2E_CHUNKS)]
 
     def e2e_step():
-        for s in pipe:
-            s.wait_for(stream)
-        tp.upload(hr, R, pipe[0])
-        pipe[1].wait_for(pipe[0])
+        up.wait_for(stream)
+        tp.upload(hr, R, up)
         for i in range(E2E_CHUNKS):
-            s = pipe[i % 2]
-            c0 = N - (i + 1) * rows
-            tp.upload(hx[:, c0:c0 + rows], xch[i], s)
-            with tp.use_stream(s):
-                tp.add(vch[i], R, dest=och[i])
-            tp.download(och[i], ho[i * rows:(i + 1) * rows, :], s)
-        for s in pipe:
-            stream.wait_for(s)
+            tp.upload(hxs[i], xch[i], up)
+            comp.wait_for(up)
+            with tp.use_stream(comp):
+                tp.add(vch[i], rch[i], dest=och[i])
+            down.wait_for(comp)
+            tp.download(och[i], hos[i], down)
+        stream.wait_for(down)
 
     for _ in range(2):
         e2e_step()
@@ -286,8 +304,16 @@ def bench_cfg2(tp, dev, steps, warmup, L):
     # correctness spot check against the host result of the same bytes
     want = (x16.T[::-1, :].astype(np.float64) + r.astype(np.float64)).astype(np.float32)
     assert np.array_equal(ho, want), "cfg2 e2e result mismatch"
+    # the PCIe bound of the e2e step on this box: the step's whole download
+    # (67 MB, one contiguous copy) and whole upload, each timed alone
+    d2h_ms = statistics.median(timed_steps(
+        L, stream, lambda: tp.download(out, ho, stream), 5, None, gate=False))
+    h2d_ms = statistics.median(timed_steps(
+        L, stream, lambda: tp.upload(hx, X, stream), 5, None, gate=False))
+    pcie = {"d2h_GBps": round(ho.nbytes / d2h_ms / 1e6, 1), "h2d_GBps": round(hx.nbytes / h2d_ms / 1e6, 1),
+            "bound_ms": round(max(d2h_ms, h2d_ms), 3)}
     dev.release(flush_buf, stream)
-    return ms, e2e_ms, wall, x16.nbytes + r.nbytes, N * N * 4
+    return ms, e2e_ms, wall, x16.nbytes + r.nbytes, N * N * 4, pcie
 
 
 def extras(tp, dev, L, warmup=3, steps=5, only=None):
@@ -541,7 +567,7 @@ def main():
     clocks = Clocks(dist.phys)
     clocks.start()
     dist.barrier()
-    ms, e2e_ms, e2e_wall, h2d, d2h = bench_cfg2(tp, dev, args.steps, args.warmup, L)
+    ms, e2e_ms, e2e_wall, h2d, d2h, pcie = bench_cfg2(tp, dev, args.steps, args.warmup, L)
     dist.barrier()
     total = dist.max(sum(ms))
     e2e_total = dist.max(sum(e2e_ms))
@@ -571,7 +597,7 @@ def main():
                          "kernel": "tpg::k_tile_f32<add, i16 -> f32, f32 row> (fused cast + broadcast add)"},
             "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_total / len(e2e_ms), 3),
-                    "wall_ms_per_step": round(e2e_wall, 3)},
+                    "wall_ms_per_step": round(e2e_wall, 3), "pcie": pcie},
             "gpu_launches": args.steps + 1 + len(e2e_ms) * E2E_CHUNKS,
             "clocks": clk,
         }

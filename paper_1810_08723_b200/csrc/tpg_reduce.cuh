@@ -1056,11 +1056,23 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_red_cols_v(RedParams p, int64_
 #pragma unroll
         for (int u = 0; u < U; ++u) b[u] = ld_vec<T>(ptr + (k * U + u) * s0);
       };
+      // min/max fold into plain doubles (fmin/fmax: NaN operands ignored,
+      // NaN = empty), which keeps the compiler from copying batch registers
+      // whose loads are still in flight
+      constexpr bool MM = OP == TPG_RMIN || OP == TPG_RMAX;
+      double mm[VE];
+#pragma unroll
+      for (int e = 0; e < VE; ++e) mm[e] = x[e][0].hi;
       auto fold = [&](const Vec16<T>(&b)[U], int64_t k) {
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-          for (int e = 0; e < VE; ++e) x[e][0].feed((double)b[u].x[e], (int)(k * U + u));
+          for (int e = 0; e < VE; ++e) {
+            if constexpr (MM)
+              mm[e] = OP == TPG_RMIN ? fmin(mm[e], (double)b[u].x[e]) : fmax(mm[e], (double)b[u].x[e]);
+            else
+              x[e][0].feed((double)b[u].x[e], (int)(k * U + u));
+          }
       };
       if (nfull > 0) ld(bA, 0);
       if (nfull > 1) ld(bB, 1);
@@ -1075,6 +1087,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_red_cols_v(RedParams p, int64_
       }
       if (k < nfull) fold(bA, k);
       if (k + 1 < nfull) fold(bB, k + 1);
+      if constexpr (MM) {
+#pragma unroll
+        for (int e = 0; e < VE; ++e) x[e][0].hi = mm[e];
+      }
       jb = j0 + nfull * U;
       ptr += nfull * U * s0;
       for (; jb < j1; ++jb, ptr += s0) {
@@ -1084,7 +1100,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_red_cols_v(RedParams p, int64_
       }
       if (OP == TPG_RMIN || OP == TPG_RMAX) {
         // a +-0 extreme: the sign is that of the first zero in the range
-#pragma unroll 1
+#pragma unroll
         for (int e = 0; e < VE; ++e) {
           if (x[e][0].hi != 0.0) continue;
           const char* q = p.sbase + soff + j0 * s0 + e * (int64_t)sizeof(T);
@@ -1112,19 +1128,26 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_red_cols_v(RedParams p, int64_
     if (is_last) {
       __threadfence();
       if (act) {
-#pragma unroll 1
-        for (int e = 0; e < VE; ++e) {
-          Part y = part_none<OP>();
-          for (int64_t c0 = 0; c0 < p.C; c0 += 8) {
-            Part q[8];
+        // all VE outputs at once, FB chunks per batch: 8 partial loads in
+        // flight per thread (chunk order per output is kept)
+        constexpr int FB = 8 / VE;
+        Part y[VE];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-              q[u] = c0 + u < p.C ? ld_part(&ws[(c0 + u) * p.O + o + e]) : part_none<OP>();
+        for (int e = 0; e < VE; ++e) y[e] = part_none<OP>();
+        for (int64_t c0 = 0; c0 < p.C; c0 += FB) {
+          Part q[FB][VE];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) y = part_comb<OP>(y, q[u]);
-          }
-          acc_store<OP, K_FLT>(p, part_acc<OP>(y), doff + e * p.so_d[0], st);
+          for (int u = 0; u < FB; ++u)
+#pragma unroll
+            for (int e = 0; e < VE; ++e)
+              q[u][e] = c0 + u < p.C ? ld_part(&ws[(c0 + u) * p.O + o + e]) : part_none<OP>();
+#pragma unroll
+          for (int u = 0; u < FB; ++u)
+#pragma unroll
+            for (int e = 0; e < VE; ++e) y[e] = part_comb<OP>(y[e], q[u][e]);
         }
+#pragma unroll
+        for (int e = 0; e < VE; ++e) acc_store<OP, K_FLT>(p, part_acc<OP>(y[e]), doff + e * p.so_d[0], st);
       }
       if (tid == 0) cnt[ob] = 0;
     }
@@ -1169,8 +1192,14 @@ int launch_vec(RedParams& p, Stream* st, bool col, bool& done) {
     constexpr int VE = Vec16<T>::n;
     constexpr int NT = 64;  // 64 x 16 B = 1 KiB of a row per block (measured best)
     const int64_t nob = (p.O + NT * VE - 1) / (NT * VE);
-    const int64_t target = sms * (512 / NT) * 4;  // four waves of resident blocks
-    int64_t C = (target + nob - 1) / nob;
+    // one wave of resident blocks: the last-arriver finalize of each output
+    // block reads C partials per output after the streaming ends, so C is
+    // kept as small as filling the machine allows, rounded down to whole
+    // finalize batches of 8 / VE chunks (cfg3 axis 1: C = 16; C = 64 cost
+    // 20 us of finalize tail on max, 10 us on sum; C = 18 3 us more than 16)
+    const int64_t slots = sms * (512 / NT);
+    int64_t C = slots / nob;
+    if (C > 8 / VE) C -= C % (8 / VE);
     if (C > p.N / 32) C = p.N / 32;
     if (C > 64) C = 64;
     if (C < 1) C = 1;

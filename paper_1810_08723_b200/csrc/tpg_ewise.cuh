@@ -1075,7 +1075,26 @@ int launch_ew(EwParams& p, Stream* st) {
       constexpr int SA = DTA >= 0 ? dt_size(DTA) : 1;
       constexpr int SB = DTB >= 0 ? dt_size(DTB) : 1;
       const int64_t n = p.ext[0];
-      const int g = grid_for((n / CV + 255) / 256, dev, 16);
+      // grid: one CV-element chunk per thread (no grid-stride loop) when a
+      // thread moves >= 48 B, else a persistent grid of 8 waves of resident
+      // blocks (occupancy calculator).  Measured on cfg5 2^30 (r01d,
+      // profiles/r01d_contig_grid.md): cast f64-BE -> f32 5.9 -> 7.0 TB/s,
+      // scalar multiply / add 5.7 -> 6.2 TB/s one chunk per thread; int16-BE
+      // -> half (16 B in, 16 B out per thread) is best persistent
+      constexpr int TB = (SD + (NIN >= 1 ? SA : 0) + (NIN >= 2 ? SB : 0)) * CV;
+      const int64_t chunks = (n / CV + 255) / 256;
+      int g;
+      if (TB >= 48) {
+        g = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, 1 << 30));
+      } else {
+        static int occ = 0;
+        if (!occ) {
+          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_contig<F, NIN, SD, SA, SB>, 256, 0) !=
+                  cudaSuccess || occ < 1)
+            occ = 1;
+        }
+        g = grid_for(chunks, dev, occ * 8);
+      }
       k_contig<F, NIN, SD, SA, SB><<<g, 256, 0, st->s>>>(p, n);
     }
   } else if (c.kind == 1) {

@@ -96,3 +96,26 @@ def test_signed_zero_ties_keep_first():
                 for axes in ((0,), (1,), None):
                     tp.reduce(op, X, axes=axes)
     assert not so.failures, so.failures[:3]
+
+
+@pytest.mark.parametrize("shape", [(256, 20000), (3000, 700), (160000, 40)])
+def test_column_chunking_regimes(shape):
+    """Column mode (outputs unit-stride) across its row-chunk regimes:
+    few outputs / long rows (C capped at 64), C rounded down to whole
+    finalize batches, and many outputs (C = 1, no finalize); NaN in a
+    chunk's first row, ties and signed zeros straddling chunk edges."""
+    rng = np.random.default_rng(16)
+    x = rng.uniform(-2, 2, shape)
+    o, n = shape
+    x[3, :] = 0.0
+    x[3, n // 2:] = -0.0                 # a zero extreme whose sign is set by the first zero
+    x[5, n // 3] = np.nan                # inner NaN (skipped by min/max)
+    x[7, 0] = np.nan                     # first element NaN: NaN result
+    x[9, n - 1] = x[9, :].max()          # tie at the last row
+    with ShadowOracle() as so:
+        for dt in (np.float64, np.float32):
+            X = tp.from_numpy(np.asfortranarray(x.astype(dt)))
+            for op in OPS:
+                tp.reduce(op, X, axes=(1,))
+    assert so.calls >= 8
+    assert not so.failures, so.failures[:3]

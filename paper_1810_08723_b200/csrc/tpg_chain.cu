@@ -34,13 +34,16 @@ struct ChainParams {
 // steps are unrolled at compile time (NS = 0: runtime count, up to 8).
 struct FScal {
   double w[MAX_STEPS];
-  int op[MAX_STEPS], sf[MAX_STEPS];
+  float wf[MAX_STEPS];
+  int op[MAX_STEPS], sf[MAX_STEPS], ex[MAX_STEPS];
 };
 __device__ __forceinline__ FScal chain_scalars(const ChainParams& c) {
   FScal f;
 #pragma unroll
   for (int i = 0; i < MAX_STEPS; ++i) {
     f.w[i] = i < c.n ? dec_flt(c.step[i].sdt, c.step[i].s) : 0.0;
+    f.wf[i] = (float)f.w[i];
+    f.ex[i] = (double)f.wf[i] == f.w[i];
     f.op[i] = c.step[i].op;
     f.sf[i] = c.step[i].sfirst;
   }
@@ -50,7 +53,14 @@ __device__ __forceinline__ float rnd_f32(double r, uint32_t* fl) {
   return __uint_as_float((uint32_t)enc_from_flt(TPG_FLOAT, r, fl).lo);
 }
 // apply the chain to V values: the (warp-uniform) op switch runs once per
-// step, each case is a tight loop over the V values
+// step, each case is a tight loop over the V values.
+// + - * with a scalar that is exactly a float run in float arithmetic: for
+// float operands, rounding the exact result to double and then to float
+// equals rounding it to float once (double has >= 2*24+2 significand bits,
+// so the double rounding is innocuous for + - * /), which is what the
+// reference's compute-in-double-then-narrow store does (ops.py:145-152,
+// dtypes.py:270-278) -- and it keeps the f32<->f64 conversions (the
+// 16/clk XU pipe, 67% busy on the double path) off the chain
 template <int NS, int V>
 __device__ __forceinline__ void chain_f32(const FScal& f, int n, float (&x)[V], uint32_t* fl) {
   constexpr int M = NS ? NS : MAX_STEPS;
@@ -59,6 +69,25 @@ __device__ __forceinline__ void chain_f32(const FScal& f, int n, float (&x)[V], 
     if (NS == 0 && i >= n) break;
     const double w = f.w[i];
     const bool sf = f.sf[i];
+    if (f.ex[i]) {
+      const float wf = f.wf[i];
+      const int op = f.op[i];
+      if (op == TPG_ADD) {
+#pragma unroll
+        for (int e = 0; e < V; ++e) x[e] = __fadd_rn(x[e], wf);
+        continue;
+      }
+      if (op == TPG_MULTIPLY) {
+#pragma unroll
+        for (int e = 0; e < V; ++e) x[e] = __fmul_rn(x[e], wf);
+        continue;
+      }
+      if (op == TPG_SUBTRACT) {
+#pragma unroll
+        for (int e = 0; e < V; ++e) x[e] = sf ? __fsub_rn(wf, x[e]) : __fsub_rn(x[e], wf);
+        continue;
+      }
+    }
     switch (f.op[i]) {
       case TPG_ADD:
 #pragma unroll

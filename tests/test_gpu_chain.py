@@ -90,3 +90,40 @@ def test_chain_error_mode_raises_without_writing():
     with pytest.raises(tp.DomainError):
         tp.chain(x, [("divide", tp.Scalar(0, tp.int32))], dest=d, mode="error")
     assert np.all(tp.to_numpy(d) == 0)
+
+
+def test_f32_chain_float_arithmetic_edges():
+    """The all-float chain computes + - * with float-exact scalars in float
+    arithmetic; that must equal the reference's compute-in-double, round
+    once to float (ops.py:145-152, dtypes.py:270-278) on the edges where
+    double rounding could show: subnormals, results that overflow to inf,
+    signed zeros, inf / NaN operands and ties at the float rounding point."""
+    rng = np.random.default_rng(41)
+    fmax = np.finfo(np.float32).max
+    tiny = np.finfo(np.float32).tiny
+    edge = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, fmax, -fmax, tiny, -tiny, tiny / 3,
+                     -tiny / 7, 1.0 + 2.0 ** -23, 1.0 + 2.0 ** -24, 3.0 * 2.0 ** -25, 16777217.0,
+                     -16777215.0], np.float64).astype(np.float32)
+    body = rng.standard_normal((1 << 16) + 3).astype(np.float32) * np.float32(
+        2.0) ** rng.integers(-140, 127, (1 << 16) + 3).astype(np.float32)
+    y = np.concatenate([np.tile(edge, 64), body]).astype(np.float32)
+    Y = tp.from_numpy(y)
+    scal = [tp.Scalar(v, tp.float) for v in (1.5, -2.0, 2.0 ** -24, 3.0e38, -0.0, 1.0 + 2.0 ** -23)]
+    chains = [[("multiply", scal[0]), ("add", scal[1])],
+              [("add", scal[2]), ("multiply", scal[3])],
+              [("subtract", scal[4]), ("multiply", scal[5]), ("add", scal[2])],
+              [("multiply", scal[3]), ("subtract", scal[1])]]
+    for ch in chains:
+        Z = tp.chain(Y, ch)
+        seq = Y
+        want = y.astype(np.float64)
+        for op, s in ch:
+            seq = getattr(tp, op)(seq, s)
+            w = float(np.float32(s.value))
+            with np.errstate(all="ignore"):
+                want = {"add": want + w, "subtract": want - w, "multiply": want * w}[op]
+                want = want.astype(np.float32).astype(np.float64)
+        z = tp.to_numpy(Z)
+        for ref in (tp.to_numpy(seq), want.astype(np.float32)):
+            same = (z.view(np.uint32) == ref.view(np.uint32)) | (np.isnan(z) & np.isnan(ref))
+            assert same.all(), (ch, np.flatnonzero(~same)[:5])

@@ -71,6 +71,7 @@ struct Sm100Args {
   int m, n, k;
   int ddt;
   int epi;  // 0 generic, 1 column-major (M contiguous), 2 row-major (N contiguous)
+  int tma_d;  // column-major 16-bit D written by TMA bulk tensor stores
   int tiles_m, tiles_n;
   int amn, bmn;  // operand is MN-major in global memory / shared memory
 };
@@ -211,7 +212,8 @@ __device__ __forceinline__ void load_operand(uint32_t dst, const CUtensorMap* ma
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const Sm100Args& g, uint32_t acc, int row_base,
                                               int n_tile, int batch, int warp, int lane,
-                                              uint8_t* epi_stage, uint32_t tempty, bool remote) {
+                                              uint8_t* epi_stage, uint32_t tempty, bool remote,
+                                              const CUtensorMap* dmap) {
   const int q = warp & 3;
   const int es = dt_size(g.ddt);
   const int row = row_base + q * 32 + lane;
@@ -236,6 +238,36 @@ __device__ __forceinline__ void epilogue_tile(const Sm100Args& g, uint32_t acc, 
     }
     const int n0 = n_tile * BN + c * 32;
     const int row0 = row_base + q * 32;
+    if (g.tma_d && g.epi == 1 && row0 + 32 <= g.m && n0 + 32 <= g.n) {
+      // column-major 16-bit destination: the warp's 32x32 chunk is
+      // transposed into a 2 KiB staging half ([column][row], exactly the
+      // TMA box layout) and written by one bulk tensor store; the two
+      // halves alternate, so a half is reused only after the store issued
+      // two chunks earlier has read it
+      uint8_t* stg = epi_stage + (c & 1) * 2048;
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncwarp();
+      uint16_t* s16 = (uint16_t*)stg;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        s16[j * 32 + lane] = (uint16_t)cvt_out(g.ddt, __uint_as_float(v[j]));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile(
+            "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                (uint64_t)dmap),
+            "r"(row0), "r"(n0), "r"(batch), "r"(su32(stg))
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      continue;
+    }
+    if (g.tma_d) {
+      // the staging slice may still be read by an in-flight bulk store
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+    }
     if (g.epi == 1 && row0 + 32 <= g.m && n0 + 32 <= g.n) {
       // column-major destination: transpose the warp's 32x32 chunk
       // through shared memory so each lane writes 16-B pieces of columns
@@ -313,7 +345,7 @@ template <int MODE>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm_sm100(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_al, const __grid_constant__ CUtensorMap tma_bl,
-                 Sm100Args g, uint32_t idesc, int ntiles) {
+                 const __grid_constant__ CUtensorMap tma_d, Sm100Args g, uint32_t idesc, int ntiles) {
   using G = Cfg<MODE>;
   constexpr int BM = G::BM, BN = G::BN, BK = G::BK, STAGES = G::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -433,8 +465,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(su32(&tfull[b]), use & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       epilogue_tile<BN>(g, tmem + b * G::TMEM_COLS, m_tile * BM, n_tile, batch, warp, lane,
-                        epi_stage + (warp - 2) * 4096, su32(&tempty[b]), false);
+                        epi_stage + (warp - 2) * 4096, su32(&tempty[b]), false, &tma_d);
     }
+    if (g.tma_d && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -493,6 +526,26 @@ static bool make_map(CUtensorMap* map, int dt, const OpView& v, int box_rows) {
                   G::SWZ == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// D map for the bulk-store epilogue: column-major 16-bit D (rows unit
+// stride), 32 x 32 boxes, no swizzle (the staging half is [column][row]).
+// Returns false (plain-store epilogue) when D does not qualify.
+static bool make_dmap(CUtensorMap* map, const Sm100Args& g, int64_t batch) {
+  if (g.epi != 1 || dt_size(g.ddt) != 2) return false;
+  if ((uintptr_t)g.d % 16 || g.ds1 % 16 || g.ds1 <= 0) return false;
+  if (batch > 1 && (g.dsb % 16 || g.dsb <= 0)) return false;
+  if (getenv("TPG_GEMM_TMA_STORE") && atoi(getenv("TPG_GEMM_TMA_STORE")) == 0) return false;
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)g.m, (cuuint64_t)g.n, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)g.ds1,
+                           (cuuint64_t)(batch > 1 ? g.dsb : g.ds1 * (int64_t)g.n)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, g.d, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // TMA-legal in place?  unit stride along k (K-major) or rows (MN-major),
@@ -640,7 +693,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     k_gemm_sm100_pair(const __grid_constant__ CUtensorMap tma_a,
                       const __grid_constant__ CUtensorMap tma_b,
                       const __grid_constant__ CUtensorMap tma_al,
-                      const __grid_constant__ CUtensorMap tma_bl, Sm100Args g, uint32_t idesc,
+                      const __grid_constant__ CUtensorMap tma_bl,
+                      const __grid_constant__ CUtensorMap tma_d, Sm100Args g, uint32_t idesc,
                       int ntiles) {
   using G = Cfg<MODE>;
   constexpr int TILE = 128 * G::BK * G::ESZ;  // one 128-row operand tile (16 / 8 KiB)
@@ -763,8 +817,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(su32(&tfull[b]), use & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       epilogue_tile<256>(g, tmem + b * 256, m2 * 256 + (int)rank * 128, n2, batch, warp, lane,
-                         epi_stage + (warp - 2) * 4096, b ? te1 : te0, true);
+                         epi_stage + (warp - 2) * 4096, b ? te1 : te0, true, &tma_d);
     }
+    if (g.tma_d && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -928,7 +983,11 @@ static int launch_sm100(Stream* st, int64_t batch, const tpg_operand* d, const i
   }
   const int ntiles = g.tiles_m * g.tiles_n * (int)batch;
   const int grid = ntiles < sm_count(st->device) ? ntiles : sm_count(st->device);
-  k_gemm_sm100<MODE><<<grid, GEMM_THREADS, G::SMEM, st->s>>>(ma, mb, mal, mbl, g, idesc, ntiles);
+  CUtensorMap md;
+  g.tma_d = make_dmap(&md, g, batch);
+  if (!g.tma_d) md = ma;
+  k_gemm_sm100<MODE><<<grid, GEMM_THREADS, G::SMEM, st->s>>>(ma, mb, mal, mbl, md, g, idesc,
+                                                             ntiles);
   TPG_LAUNCH_CHECK("gemm sm100");
   return 1;
 }
@@ -985,8 +1044,11 @@ static int launch_pair(Stream* st, int64_t batch, const tpg_operand* d, const in
   }
   const int ntiles = ((g.tiles_m + 1) / 2) * g.tiles_n * (int)batch;
   const int pairs = std::min(ntiles, sm_count(st->device) / 2);
-  k_gemm_sm100_pair<MODE><<<2 * pairs, GEMM_THREADS, P_SMEM, st->s>>>(ma, mb, mal, mbl, g, idesc,
-                                                                      ntiles);
+  CUtensorMap md;
+  g.tma_d = make_dmap(&md, g, batch);
+  if (!g.tma_d) md = ma;
+  k_gemm_sm100_pair<MODE><<<2 * pairs, GEMM_THREADS, P_SMEM, st->s>>>(ma, mb, mal, mbl, md, g,
+                                                                      idesc, ntiles);
   TPG_LAUNCH_CHECK("gemm sm100 pair");
   return 1;
 }

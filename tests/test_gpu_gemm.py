@@ -190,3 +190,44 @@ def test_gemm_batched_col_major(dt):
         a64, b64 = a[:, :, i].astype(np.float64), b[:, :, i].astype(np.float64)
         bound = np.abs(a64) @ np.abs(b64)
         assert np.all(np.abs(Cg[:, :, i] - a64 @ b64) <= tol * bound + 1e-30)
+
+
+@pytest.mark.parametrize("dt", [tp.half, tp.bfloat16])
+@pytest.mark.parametrize("m,n,k,nb,ldpad", [(1000, 700, 333, 1, 0), (256, 288, 64, 1, 8),
+                                             (330, 260, 96, 3, 0), (300, 300, 80, 1, 3)])
+def test_gemm_col_major_dest_every_element(dt, m, n, k, nb, ldpad):
+    """Column-major 16-bit destinations, checked element by element: whole
+    32 x 32 chunks go through the bulk-tensor-store epilogue, ragged edge
+    chunks through the plain-store path of the same tile, and a leading
+    dimension that is not a multiple of 16 bytes (ldpad 3) takes the plain
+    path throughout."""
+    rng = np.random.default_rng(m + n + k + nb + ldpad)
+    npd = np.float16
+    a = rng.uniform(-1, 1, (m, k, nb)).astype(np.float32)
+    b = rng.uniform(-1, 1, (k, n, nb)).astype(np.float32)
+    if dt is tp.bfloat16:
+        a = (a.view(np.uint32) & 0xffff0000).view(np.float32)
+        b = (b.view(np.uint32) & 0xffff0000).view(np.float32)
+
+    def dev(x):
+        if dt is tp.bfloat16:
+            raw = (np.asfortranarray(x).view(np.uint32) >> 16).astype(np.uint16)
+            return tp.from_numpy(np.asfortranarray(raw), dtype=tp.bfloat16)
+        return tp.from_numpy(np.asfortranarray(x.astype(npd)))
+
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    if dt is tp.half:
+        a64, b64 = a.astype(npd).astype(np.float64), b.astype(npd).astype(np.float64)
+    base = tp.tensor_create((m + ldpad, n, nb), dt)
+    Cv = tp.apply_index(base, (slice(0, m), slice(None), slice(None)))
+    if nb == 1:
+        A = tp.apply_index(dev(a), (slice(None), slice(None), 0))
+        B = tp.apply_index(dev(b), (slice(None), slice(None), 0))
+        tp.matmul(A, B, dest=tp.apply_index(Cv, (slice(None), slice(None), 0)))
+    else:
+        tp.matmul_batched(dev(a), dev(b), dest=Cv)
+    got = _host(Cv).reshape(m, n, nb, order="F")
+    for i in range(nb):
+        want = a64[:, :, i] @ b64[:, :, i]
+        bound = np.abs(a64[:, :, i]) @ np.abs(b64[:, :, i])
+        assert np.all(np.abs(got[:, :, i] - want) <= TOL * bound + 1e-6), i

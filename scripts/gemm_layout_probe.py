@@ -51,3 +51,13 @@ Ak = tz.permute_axes(f16((n, n, nb)), (1, 0, 2))
 run("batched 64x2048^3 A K-major", lambda: tp.matmul_batched(Ak, Bb, dest=Cb), 2 * nb * n ** 3)
 Bm = tz.permute_axes(f16((n, n, nb)), (1, 0, 2))
 run("batched 64x2048^3 A K-major B MN-major", lambda: tp.matmul_batched(Ak, Bm, dest=Cb), 2 * nb * n ** 3)
+# row-major destination (epilogue writes each thread's 32 contiguous values)
+Cr = tz.permute_axes(tp.tensor_create((n, n, nb), tp.half, dev), (1, 0, 2))
+run("batched 64x2048^3 A K-major, row-major C", lambda: tp.matmul_batched(Ak, Bb, dest=Cr),
+    2 * nb * n ** 3)
+m = 8192
+del Ak, Bb, Cb, Bm, Cr
+Ak = tp.transpose(f16((m, m)))
+B = f16((m, m))
+Cr = tp.transpose(tp.tensor_create((m, m), tp.half, dev))
+run("8192^3 A K-major, row-major C", lambda: tp.matmul(Ak, B, dest=Cr), 2 * m ** 3)

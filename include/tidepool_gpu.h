@@ -114,6 +114,7 @@ const char* tpg_version(void);
 /* Stream-ordered caching allocator (devices.py:149-160 allocate/release). */
 int tpg_malloc(int device, size_t nbytes, void** ptr);
 int tpg_free(int device, void* ptr, tpg_stream stream);  /* deferred past stream */
+int tpg_malloc_on(tpg_stream stream, size_t nbytes, void** ptr);  /* ordered on stream */
 int tpg_host_alloc(size_t nbytes, void** ptr);            /* pinned host memory */
 int tpg_host_free(void* ptr);
 int tpg_mem_stats(int device, int64_t* in_use, int64_t* cached, int64_t* n_alloc);
@@ -140,9 +141,23 @@ int tpg_memset(void* dst, int value, size_t n, tpg_stream stream);
 int tpg_memcpy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
                  size_t height, tpg_stream stream);
 
-/* Sticky status word (ops._status) in host-mapped memory, OR-ed by kernels. */
+/* Sticky status word (ops._status, ops.py:27-38) per device, OR-ed by
+ * kernels.  tpg_flags_get / tpg_flags_clear wait for the whole device;
+ * tpg_flags_take atomically reads-and-clears it in `stream` order and waits
+ * for that stream only (the drop-in's Stream.sync, devices.py:93-98). */
 int tpg_flags_get(int device, uint32_t* flags);
 int tpg_flags_clear(int device);
+int tpg_flags_take(tpg_stream stream, uint32_t* flags);
+
+/* Host-addressable device storage for the drop-in plugin: the reference
+ * object model reads and writes storage bytes on the host (storage.py:38-39,
+ * tensors.py:313-318), so its gpu buffers are CUDA managed allocations
+ * (preferred location: the GPU).  Devices.allocate (devices.py:149-160). */
+int tpg_malloc_managed(int device, size_t nbytes, void** ptr);
+int tpg_free_managed(void* ptr);
+/* completion tracking for recycled blocks: 0 = complete, 1 = pending */
+int tpg_event_create_untimed(tpg_event* ev);
+int tpg_event_query(tpg_event ev);
 
 /* Measurement helper: write then re-read `n` bytes of `scratch` (> L2) on
    `stream`, leaving the L2 full of clean unrelated lines. */

@@ -82,6 +82,7 @@ PROTOTYPES = {
     "tpg_version": (C.c_char_p, []),
     "tpg_malloc": (_i32, [C.c_int, C.c_size_t, P(_vp)]),
     "tpg_free": (_i32, [C.c_int, _vp, _vp]),
+    "tpg_malloc_on": (_i32, [_vp, C.c_size_t, P(_vp)]),
     "tpg_host_alloc": (_i32, [C.c_size_t, P(_vp)]),
     "tpg_host_free": (_i32, [_vp]),
     "tpg_mem_stats": (_i32, [C.c_int, P(_i64), P(_i64), P(_i64)]),
@@ -103,6 +104,11 @@ PROTOTYPES = {
     "tpg_memcpy2d": (_i32, [_vp, C.c_size_t, _vp, C.c_size_t, C.c_size_t, C.c_size_t, _vp]),
     "tpg_flags_get": (_i32, [C.c_int, P(C.c_uint32)]),
     "tpg_flags_clear": (_i32, [C.c_int]),
+    "tpg_flags_take": (_i32, [_vp, P(C.c_uint32)]),
+    "tpg_malloc_managed": (_i32, [C.c_int, C.c_size_t, P(_vp)]),
+    "tpg_free_managed": (_i32, [_vp]),
+    "tpg_event_create_untimed": (_i32, [P(_vp)]),
+    "tpg_event_query": (_i32, [_vp]),
     "tpg_l2_flush": (_i32, [_vp, C.c_size_t, _vp]),
     "tpg_gate_arm": (_i32, [_vp]),
     "tpg_gate_release": (_i32, []),

@@ -175,6 +175,16 @@ int tpg_malloc(int device, size_t nbytes, void** ptr) {
   return TPG_OK;
 }
 
+int tpg_malloc_on(tpg_stream stream, size_t nbytes, void** ptr) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  if (nbytes == 0) nbytes = 1;
+  nbytes = (nbytes + 255) & ~(size_t)255;
+  cudaError_t e = cudaMallocAsync(ptr, nbytes, st->s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  return TPG_OK;
+}
+
 int tpg_free(int device, void* ptr, tpg_stream stream) {
   if (ptr == nullptr) return TPG_OK;
   if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
@@ -408,13 +418,85 @@ int tpg_gate_release(void) {
 int tpg_flags_get(int device, uint32_t* flags) {
   if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
   TPG_CUDA_CHECK(cudaSetDevice(device));
+  // every stream of the device (the kernels run on non-blocking streams
+  // that a legacy-stream cudaMemcpy would not wait for)
+  TPG_CUDA_CHECK(cudaDeviceSynchronize());
   TPG_CUDA_CHECK(cudaMemcpy(flags, g_flags[device], sizeof(uint32_t), cudaMemcpyDeviceToHost));
   return TPG_OK;
+}
+
+// Stream-ordered read-and-clear of the sticky status word: one thread swaps
+// the word with 0 (atomicExch, so a bit OR-ed by a kernel on another stream
+// of the same device is never lost between a read and a clear), the old
+// value lands in pinned host memory, and the host waits for `stream` only.
+__global__ void k_flags_take(uint32_t* flags, uint32_t* out) { *out = atomicExch(flags, 0u); }
+
+int tpg_flags_take(tpg_stream stream, uint32_t* flags) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  static thread_local uint32_t* host_word = nullptr;
+  if (!host_word) TPG_CUDA_CHECK(cudaHostAlloc((void**)&host_word, 64, cudaHostAllocPortable));
+  uint32_t* dev_word = g_flags[st->device] + 8;  // scratch slot next to the sticky word
+  k_flags_take<<<1, 1, 0, st->s>>>(g_flags[st->device], dev_word);
+  TPG_LAUNCH_CHECK("flags take");
+  TPG_CUDA_CHECK(cudaMemcpyAsync(host_word, dev_word, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                 st->s));
+  TPG_CUDA_CHECK(cudaStreamSynchronize(st->s));
+  *flags = *host_word;
+  return TPG_OK;
+}
+
+// CUDA managed memory for storages the host also addresses (the drop-in
+// plugin: the reference reads and writes storage bytes through memoryviews).
+// Preferred location is the GPU; large blocks are migrated there up front so
+// the first kernel does not fault them over page by page.
+int tpg_malloc_managed(int device, size_t nbytes, void** ptr) {
+  if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
+  TPG_CUDA_CHECK(cudaSetDevice(device));
+  if (nbytes == 0) nbytes = 1;
+  TPG_CUDA_CHECK(cudaMallocManaged(ptr, nbytes, cudaMemAttachGlobal));
+  if (nbytes >= (1u << 20)) {
+    cudaMemLocation loc;
+    loc.type = cudaMemLocationTypeDevice;
+    loc.id = device;
+    cudaMemAdvise_v2(*ptr, nbytes, cudaMemAdviseSetPreferredLocation, loc);
+    cudaMemLocation host;
+    host.type = cudaMemLocationTypeHost;
+    host.id = 0;
+    cudaMemAdvise_v2(*ptr, nbytes, cudaMemAdviseSetAccessedBy, host);
+    cudaMemPrefetchAsync_v2(*ptr, nbytes, loc, 0, g_default[device]->s);
+    cudaGetLastError();  // advice is best effort
+  }
+  return TPG_OK;
+}
+
+int tpg_free_managed(void* ptr) {
+  if (ptr == nullptr) return TPG_OK;
+  TPG_CUDA_CHECK(cudaFree(ptr));
+  return TPG_OK;
+}
+
+int tpg_event_create_untimed(tpg_event* ev) {
+  cudaEvent_t e;
+  TPG_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  *ev = (tpg_event)e;
+  return TPG_OK;
+}
+
+int tpg_event_query(tpg_event ev) {
+  cudaError_t e = cudaEventQuery((cudaEvent_t)ev);
+  if (e == cudaSuccess) return 0;
+  if (e == cudaErrorNotReady) {
+    cudaGetLastError();
+    return 1;
+  }
+  return cuda_fail(e, "cudaEventQuery");
 }
 
 int tpg_flags_clear(int device) {
   if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
   TPG_CUDA_CHECK(cudaSetDevice(device));
+  TPG_CUDA_CHECK(cudaDeviceSynchronize());
   TPG_CUDA_CHECK(cudaMemset(g_flags[device], 0, sizeof(uint32_t)));
   return TPG_OK;
 }

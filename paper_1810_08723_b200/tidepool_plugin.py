@@ -1,25 +1,70 @@
-"""Drop-in adapter: the gpu table for an UNMODIFIED reference `tidepool`.
-
-The reference hands Python closures across its function table (SURVEY.md
-§8b): `store` (ops._make_store, ops.py:145-152), codec `unpack` functions
-(dtypes.codec, dtypes.py:357-391), scalar `fn`s (kernels.py:50-158) and
-reduction (init, step, fin) triples (ops.py:522-556).  This module recovers
-the descriptors those closures encode (dtype, byte order, mode, op, compute
-dtype, norm order) by introspection, so the same C-ABI kernels serve the
-reference's own pipeline:
+"""Drop-in adapter: the ("core", "gpu") table for an UNMODIFIED reference
+`tidepool` (the north_star boundary).
 
     import tidepool
     from paper_1810_08723_b200 import tidepool_plugin
     tidepool_plugin.register(tidepool)      # adds device type "gpu"
-    x = tidepool.cast(t, device=tidepool.devices.by_name("gpu0"))
+    g = tidepool.devices.by_name("gpu0")
+    x = tidepool.cast(t, device=g)          # H2D through the gpu `copy` entry
+    y = tidepool.add(x, 1.5)                # the reference pipeline, B200 kernels
 
-The decoding helpers are also used by tests/golden/make_golden.py to turn
+What the reference hands across its function table are Python closures
+(`store` = ops._make_store, ops.py:145-152; codec `unpack`/`pack`,
+dtypes.py:357-391; scalar `fn`s, kernels.py:50-158; reduction (init, step,
+fin) triples, ops.py:522-556).  This module recovers the descriptors those
+closures encode (dtype, byte order, mode, CastContext, status set, norm
+order) by introspection and makes one C-ABI call per entry.
+
+All arithmetic, cast and status semantics stay the reference's:
+
+* status: the device's sticky flag word is drained, in stream order, into
+  the `status` set the reference's scalar functions close over
+  (kernels.py:72-78, 151-156 -> ops._status, ops.py:27-38) whenever a gpu
+  stream synchronises; `tidepool.get_status()` drains every gpu stream first,
+  so flags are visible exactly as on the synchronous cpu device;
+* cast loss (error / warning mode): reported through the store's own
+  `CastContext.domain_loss` (dtypes.py:233-255), so error mode raises the
+  reference's `tidepool.errors.DomainError` before anything is written and
+  warning mode warns once through the reference's handler (`ctx.flush()` in
+  ops.py:284-285);
+* native failures raise the reference's `DeviceError` / `AllocationError`.
+
+B200 mechanics:
+
+* storage = CUDA managed memory (the reference reads and writes storage bytes
+  on the host through memoryviews), preferred on the GPU, recycled through a
+  bounded per-device cache; a recycled block is handed out only after the
+  GPU work that last used it has completed;
+* entries enqueue asynchronously on the storage's gpu stream (a
+  `devices.Stream` subclass whose `sync()` synchronises the CUDA stream);
+  nothing synchronises per entry in standard mode;
+* lazy casts: a lossless dtype-converting gpu->gpu `copy`
+  (the reference's `_dtype_convert`, ops.py:121-124) is recorded instead of
+  launched; a binary entry reading its result converts on load from the
+  original source (cfg2: one 6 B/element pass instead of 14 B/element), any
+  other consumer, writer or synchronisation materialises it first;
+* descriptor transfers: `tensors._raw_gather` (gpu->gpu,
+  cpu->gpu, gpu->cpu) and the cpu `copy` entry for gpu sources run as one
+  plan-driven kernel plus one bulk PCIe copy instead of the reference's
+  per-element Python pair list (tensors.py:686-699).
+
+The closure decoders are also used by tests/golden/make_golden.py to turn
 captured reference table calls into golden vectors.
 """
 
 from __future__ import annotations
 
+import collections
+import ctypes as C
+import threading
 
+MODE_CODE = {"standard": 0, "warning": 1, "error": 2, "complex": 3}
+FLAG_DOMAIN, FLAG_INT_DIV0, FLAG_CAST_LOSS = 1, 2, 4
+
+
+# ---------------------------------------------------------------------------
+# closure decoding
+# ---------------------------------------------------------------------------
 def _cells(fn) -> dict:
     code = getattr(fn, "__code__", None)
     if code is None or fn.__closure__ is None:
@@ -36,7 +81,8 @@ def decode_codec(ref_dtypes, fn):
 
 
 def prime_codecs(ref_dtypes) -> None:
-    """Populate every (dtype, byteorder) codec so reverse lookups succeed."""
+    """Populate every (dtype, byteorder) codec so reverse lookups succeed
+    (the cache never evicts, dtypes.py:354-391)."""
     for d in ref_dtypes.ALL_DTYPES:
         for order in ("little", "big"):
             ref_dtypes.codec(d, order)
@@ -55,6 +101,18 @@ def decode_store(ref_dtypes, store):
     raise LookupError("unrecognised store closure")
 
 
+def decode_ctx(store):
+    """The CastContext a store closure reports cast loss to (or None)."""
+    return _cells(store).get("ctx")
+
+
+def decode_status(fn):
+    """The status set a scalar function records flags into (kernels.py:72-78,
+    151-156); None for functions that never flag."""
+    s = _cells(fn).get("status")
+    return s if isinstance(s, set) else None
+
+
 def unary_forces_complex(fn) -> bool:
     """unary_scalar_fn returns `lambda v: complex_fn(complex(v))` for the
     complex branch (kernels.py:145-146)."""
@@ -63,245 +121,688 @@ def unary_forces_complex(fn) -> bool:
 
 
 def norm_order(step) -> float:
-    cells = _cells(step)
-    return float(cells.get("p", 2.0))
+    return float(_cells(step).get("p", 2.0))
+
+
+# ---------------------------------------------------------------------------
+# plan helpers (reference IterPlan: .extents, .strides, .total)
+# ---------------------------------------------------------------------------
+def _span(extents, strides, base, size):
+    """[lo, hi) byte range one plan view touches."""
+    lo = hi = base
+    for e, s in zip(extents, strides):
+        if e > 1:
+            if s < 0:
+                lo += (e - 1) * s
+            else:
+                hi += (e - 1) * s
+    return lo, hi + size
+
+
+def _is_dense(extents, strides, size):
+    """True when the view enumerates [0, total*size) exactly once in
+    column-major order (a fresh tensor_create layout)."""
+    step = size
+    for e, s in zip(extents, strides):
+        if e == 1:
+            continue
+        if s != step:
+            return False
+        step *= e
+    return True
+
+
+def _fuse_strides(copy_plan, bin_ext, bin_str, a_base, size):
+    """Re-express a binary operand that reads the (dense) destination of a
+    recorded copy as a view of the copy's SOURCE.  Returns (src strides per
+    binary axis, src byte offset relative to the copy's source offset) or
+    None when the binary view does not map axis-for-axis onto the copy plan
+    (the caller then materialises the copy)."""
+    E = copy_plan.extents
+    T, S = copy_plan.strides[0], copy_plan.strides[1]
+    if a_base % size:
+        return None
+    # the operand's base offset as copy-plan digits (mixed radix E)
+    lin, digits = a_base // size, []
+    for e in E:
+        lin, d = divmod(lin, e) if e else (lin, 0)
+        digits.append(d)
+    if lin:
+        return None
+    out, used = [], set()
+    for f, b in zip(bin_ext, bin_str):
+        if f == 1 or b == 0:
+            out.append(0)
+            continue
+        for j, (e, t) in enumerate(zip(E, T)):
+            if t == b and e == f and digits[j] == 0 and j not in used:
+                used.add(j)
+                out.append(S[j])
+                break
+        else:
+            return None
+    return out, sum(d * s for d, s in zip(digits, S))
 
 
 # ---------------------------------------------------------------------------
 # registration into the reference
 # ---------------------------------------------------------------------------
-class _Cudart:
-    """Minimal libcudart access for managed allocations and pointer kinds."""
+class _Block:
+    """One managed allocation behind a gpu storage; returns itself to the
+    device cache when the storage's buffer object is garbage collected."""
+    __slots__ = ("rt", "ptr", "cap", "device", "events", "__weakref__")
 
-    def __init__(self):
-        import ctypes as C
-        self.C = C
-        self.lib = C.CDLL("libcudart.so.12", mode=C.RTLD_GLOBAL)
+    def __init__(self, rt, ptr, cap, device):
+        self.rt, self.ptr, self.cap, self.device = rt, ptr, cap, device
+        self.events = ()
 
-    def malloc_managed(self, n: int) -> int:
-        C = self.C
-        ptr = C.c_void_p()
-        rc = self.lib.cudaMallocManaged(C.byref(ptr), C.c_size_t(max(n, 1)), C.c_uint(1))
-        if rc != 0:
-            raise MemoryError(f"cudaMallocManaged({n}) failed ({rc})")
-        return ptr.value
-
-    def free(self, ptr: int) -> None:
-        self.lib.cudaDeviceSynchronize()
-        self.lib.cudaFree(self.C.c_void_p(ptr))
-
-    def place_on_device(self, ptr: int, n: int, device: int) -> None:
-        """Preferred location = the GPU and migrate there now, so the first
-        kernel touching a fresh buffer does not page-fault it over
-        (cudaMemAdviseSetPreferredLocation = 3, SetAccessedBy = 5 for the
-        host reads the reference does)."""
-        C = self.C
-        self.lib.cudaMemAdvise(C.c_void_p(ptr), C.c_size_t(n), C.c_int(3), C.c_int(device))
-        self.lib.cudaMemAdvise(C.c_void_p(ptr), C.c_size_t(n), C.c_int(5), C.c_int(-1))
-        self.lib.cudaMemPrefetchAsync(C.c_void_p(ptr), C.c_size_t(n), C.c_int(device), None)
-        self.lib.cudaGetLastError()
-
-    def is_device_accessible(self, ptr: int) -> bool:
-        """True for device / managed / pinned memory (cudaPointerGetAttributes)."""
-        C = self.C
-
-        class Attr(C.Structure):
-            _fields_ = [("type", C.c_int), ("device", C.c_int), ("devicePointer", C.c_void_p),
-                        ("hostPointer", C.c_void_p)]
-
-        a = Attr()
-        rc = self.lib.cudaPointerGetAttributes(C.byref(a), C.c_void_p(ptr))
-        if rc != 0:
-            self.lib.cudaGetLastError()
-            return False
-        return a.type in (1, 2, 3)
+    def __del__(self):
+        try:
+            self.rt._release(self)
+        except Exception:
+            pass
 
 
-def register(tidepool_module, count: int | None = None):
+import numpy as _np  # noqa: E402
+
+
+class _DevBytes(_np.ndarray):
+    """Host view of a managed block; carries the block for the pointer
+    registry and its lifetime."""
+
+
+def _size_class(n: int) -> int:
+    if n <= (1 << 20):
+        return (max(n, 1) + 511) & ~511
+    return (n + (2 << 20) - 1) & ~((2 << 20) - 1)
+
+
+class _Runtime:
+    """Per-registration state: devices, streams, block cache, lazy casts."""
+
+    CACHE_BYTES = 8 << 30  # per device; beyond this released blocks are freed
+
+    def __init__(self, tp, L):
+        self.tp, self.L = tp, L
+        self.errors = tp.errors
+        self.lock = threading.RLock()
+        self.tls = threading.local()
+        self.cache: dict = {}         # (device, cap) -> [block ptr + events]
+        self.cached_bytes: dict = {}  # device -> bytes
+        self.blocks: dict = {}        # ptr -> (device, cap) of live managed blocks
+        self.streams: dict = {}       # device -> [GpuStream] (for free tracking)
+        self.lazy: dict = {}          # dst ptr -> _Lazy
+        self.lazy_by_src: dict = {}   # src ptr -> {dst ptr}
+        self.status_sink = tp.ops._status
+        self.event_pool: list = []
+        self.stats = collections.Counter()  # lazy / fused / materialised / transfer paths
+
+    # -- errors --------------------------------------------------------------
+    def check(self, rc, what):
+        if rc == 0:
+            return
+        msg = f"{what}: {self.L.tpg_last_error().decode()}"
+        if rc == -2:
+            raise self.errors.AllocationError(msg)
+        raise self.errors.DeviceError(msg)
+
+    # -- memory --------------------------------------------------------------
+    def allocate(self, device, nbytes):
+        cap = _size_class(nbytes)
+        key = (device, cap)
+        with self.lock:
+            pool = self.cache.get(key)
+            ent = pool.pop() if pool else None
+            if ent is not None:
+                self.cached_bytes[device] -= cap
+        if ent is not None:
+            ptr, events = ent
+            for ev in events:  # the block's last GPU use must be complete
+                if self.L.tpg_event_query(ev) != 0:
+                    self.check(self.L.tpg_event_sync(ev), "event sync")
+                self.event_pool.append(ev)
+        else:
+            p = C.c_void_p()
+            rc = self.L.tpg_malloc_managed(device, cap, C.byref(p))
+            if rc == -2:
+                self.trim(device, 0)
+                rc = self.L.tpg_malloc_managed(device, cap, C.byref(p))
+            self.check(rc, f"managed allocation of {nbytes} bytes")
+            ptr = p.value
+        blk = _Block(self, ptr, cap, device)
+        with self.lock:
+            self.blocks[ptr] = (device, cap)
+        # a uint8 ndarray over the block: its memoryview has format "B", so
+        # the reference's struct packing and slice assignment work on it
+        arr = _np.ctypeslib.as_array((C.c_ubyte * max(nbytes, 1)).from_address(ptr))
+        arr = arr.view(_DevBytes)
+        arr._tpg_block = blk
+        return arr
+
+    def _release(self, blk):
+        ptr = blk.ptr
+        with self.lock:
+            self.blocks.pop(ptr, None)
+            self._drop_lazy_locked(ptr)
+        events = []
+        for st in self.streams.get(blk.device, ()):
+            ev = self.event_pool.pop() if self.event_pool else self._new_event()
+            self.L.tpg_event_record(ev, st.handle)
+            events.append(ev)
+        with self.lock:
+            self.cache.setdefault((blk.device, blk.cap), []).append((ptr, events))
+            self.cached_bytes[blk.device] = self.cached_bytes.get(blk.device, 0) + blk.cap
+            over = self.cached_bytes[blk.device] > self.CACHE_BYTES
+        if over:
+            self.trim(blk.device, self.CACHE_BYTES // 2)
+
+    def _new_event(self):
+        ev = C.c_void_p()
+        self.check(self.L.tpg_event_create_untimed(C.byref(ev)), "event create")
+        return ev.value
+
+    def trim(self, device, keep_bytes):
+        """Free cached blocks of `device` until at most keep_bytes remain."""
+        with self.lock:
+            victims = []
+            for key in list(self.cache):
+                if key[0] != device:
+                    continue
+                pool = self.cache[key]
+                while pool and self.cached_bytes.get(device, 0) > keep_bytes:
+                    victims.append(pool.pop(0))
+                    self.cached_bytes[device] -= key[1]
+        for ptr, events in victims:
+            for ev in events:
+                self.L.tpg_event_sync(ev)
+                self.event_pool.append(ev)
+            self.L.tpg_free_managed(C.c_void_p(ptr))
+
+    # -- pointers --------------------------------------------------------------
+    @staticmethod
+    def address(mv):
+        """Raw address of a storage memoryview (read-only views included)."""
+        obj = mv.obj
+        blk = getattr(obj, "_tpg_block", None)
+        if blk is not None:
+            return blk.ptr
+        if len(mv) == 0:
+            return 0
+        import numpy as np
+        return int(np.frombuffer(mv, dtype=np.uint8).ctypes.data)
+
+    def is_gpu(self, ptr) -> bool:
+        return ptr in self.blocks
+
+    # -- streams ----------------------------------------------------------------
+    def current(self, device):
+        st = getattr(self.tls, "stream", None)
+        if st is not None and st.device.index == device:
+            return st
+        return self.devices[device].default_stream()
+
+    def drain(self, st):
+        """Stream-ordered read-and-clear of the device's status word; status
+        bits go to the reference's status set."""
+        f = C.c_uint32(0)
+        self.check(self.L.tpg_flags_take(st.handle, C.byref(f)), "status flags")
+        bits = f.value
+        kernels = self.tp.kernels
+        if bits & FLAG_DOMAIN:
+            self.status_sink.add(kernels.STATUS_DOMAIN)
+        if bits & FLAG_INT_DIV0:
+            self.status_sink.add(kernels.STATUS_INT_DIV_ZERO)
+        return bits
+
+    # -- lazy casts -------------------------------------------------------------
+    def _drop_lazy_locked(self, dst_ptr):
+        lz = self.lazy.pop(dst_ptr, None)
+        if lz is not None:
+            srcs = self.lazy_by_src.get(lz.src_ptr)
+            if srcs is not None:
+                srcs.discard(dst_ptr)
+                if not srcs:
+                    del self.lazy_by_src[lz.src_ptr]
+        return lz
+
+    def materialize(self, dst_ptr):
+        with self.lock:
+            lz = self._drop_lazy_locked(dst_ptr)
+        if lz is not None:
+            self.stats["materialized"] += 1
+            lz.launch(self)
+
+    def before_read(self, ptr):
+        if ptr in self.lazy:
+            self.materialize(ptr)
+
+    def before_write(self, ptr):
+        if ptr in self.lazy:
+            self.materialize(ptr)
+        srcs = self.lazy_by_src.get(ptr)
+        if srcs:
+            for d in list(srcs):
+                self.materialize(d)
+
+    def materialize_device(self, device):
+        with self.lock:
+            todo = [p for p, lz in self.lazy.items() if lz.device == device]
+        for p in todo:
+            self.materialize(p)
+
+
+class _Lazy:
+    """A recorded dtype-converting gpu->gpu copy (ops._dtype_convert)."""
+    __slots__ = ("device", "plan", "dst_ptr", "dst_op", "src_ptr", "src_op", "keep", "src_dtype",
+                 "dst_dtype", "src_order")
+
+    def launch(self, rt):
+        st = rt.current(self.device)
+        p = rt.abi.make_plan(self.plan.extents, self.plan.strides)
+        rt.check(rt.L.tpg_unary(st.handle, 10, C.byref(p), C.byref(self.dst_op),
+                                C.byref(self.src_op), self.src_op.dtype, 0, 0), "copy")
+
+
+def register(tidepool_module, count: int | None = None, lib=None):
     """Attach B200 gpu devices and the ("core", "gpu") table to `tidepool`.
 
-    Storage of gpu tensors must stay host-addressable in the reference object
-    model (storage.view() memoryviews), so buffers are CUDA
-    managed allocations exposed as ctypes arrays that kernels read and write
-    in place.  Host (cpu-device) source buffers are staged into managed
-    memory for the duration of one call.  Returns the registered devices.
-    """
-    import ctypes as C
-
+    Returns the registered devices (gpu0, gpu1, ...).  `lib` is a test hook
+    (tests/fake_native.py); the product always uses libtidepool_gpu.so."""
     import numpy as np
 
-    from . import _native
-    from . import dtypes as D
-    from . import table as tb
-    from .plan import IterPlan
+    from . import _native, abi
 
     tp = tidepool_module
     ref_devices, ref_dispatch, ref_dtypes = tp.devices, tp.dispatch, tp.dtypes
+    ref_tensors, ref_ops = tp.tensors, tp.ops
+    errors = tp.errors
     prime_codecs(ref_dtypes)
-    L = _native.lib()
-    rt = _Cudart()
+    try:
+        L = lib if lib is not None else _native.lib()
+    except Exception as exc:  # no library / no device: the reference's own error class
+        raise errors.DeviceError(f"gpu device module unavailable: {exc}") from exc
+    rt = _Runtime(tp, L)
+    rt.abi = abi
     gpu_type = ref_devices.DeviceType("gpu", supports_byteswapped=True, async_capable=False)
+    codec_of = {}
+    for (d, order), pair in ref_dtypes._CODEC_CACHE.items():
+        codec_of[pair[0]] = codec_of[pair[1]] = (d, order)
+
+    # -- devices and streams ------------------------------------------------------
+    class GpuStream(ref_devices.Stream):
+        """A reference Stream bound to one CUDA stream.  Work is enqueued by
+        the calling thread (submit runs the task inline, which only launches
+        kernels); sync() waits for the CUDA stream and drains its status."""
+
+        def __init__(self, device, handle=None):
+            super().__init__(device)
+            if handle is None:
+                h = C.c_void_p()
+                rt.check(L.tpg_stream_create(device.index, C.byref(h)), "stream create")
+                handle = h.value
+            self.handle = handle
+            rt.streams.setdefault(device.index, []).append(self)
+
+        def submit(self, task) -> None:
+            prev = getattr(rt.tls, "stream", None)
+            rt.tls.stream = self
+            try:
+                task()
+            finally:
+                rt.tls.stream = prev
+
+        def sync(self) -> None:
+            rt.materialize_device(self.device.index)
+            rt.drain(self)
+            super().sync()
 
     class GpuDevice(ref_devices.Device):
         def __init__(self, index):
             super().__init__(gpu_type, index)
 
+        def default_stream(self):
+            with self._lock:
+                if self._default_stream is None:
+                    h = C.c_void_p()
+                    rt.check(L.tpg_default_stream(self.index, C.byref(h)), "default stream")
+                    self._default_stream = GpuStream(self, h.value)
+                return self._default_stream
+
         def allocate(self, nbytes):
             if nbytes < 0:
-                raise tp.errors.AllocationError("negative allocation size")
-            self.alloc_count += 1
-            size = max(nbytes, 1)
-            # caching: every op allocates its result (and the pipeline its
-            # converted intermediates); reuse managed blocks of the same size
-            # released earlier (the plugin syncs after each table call, so a
-            # released block has no kernel in flight)
-            pool = _cache.setdefault((self.index, size), [])
-            if pool:
-                ptr = pool.pop()
-            else:
-                ptr = rt.malloc_managed(size)
-                if size >= (1 << 20):
-                    rt.place_on_device(ptr, size, self.index)
-            arr = (C.c_ubyte * size).from_address(ptr)
-            arr._tpg_free = _Free(ptr, (self.index, size))  # back to the cache with the last ref
-            return arr
+                raise errors.AllocationError("negative allocation size")
+            with self._lock:
+                self.alloc_count += 1
+            return rt.allocate(self.index, nbytes)
 
         @property
         def properties(self):
             props = super().properties
-            props.update(tb_props(self.index))
+            p = abi.DeviceProps()
+            rt.check(L.tpg_device_props_get(self.index, C.byref(p)), "device properties")
+            props.update({"name": p.name.decode(), "processor-count": str(p.sm_count),
+                          "free-memory": str(p.free_mem), "total-memory": str(p.total_mem)})
             return props
 
-    _cache: dict = {}
-    _cache_limit = 64  # blocks kept per (device, size)
+        def synchronize(self):
+            for st in list(rt.streams.get(self.index, ())):
+                st.sync()
 
-    class _Free:
-        def __init__(self, ptr, key=None):
-            self.ptr = ptr
-            self.key = key
+    # -- operands ---------------------------------------------------------------------
+    class _Temps:
+        """Device staging for host-resident operands of one entry; freed in
+        stream order after the entry's kernel."""
 
-        def __del__(self):
-            try:
-                pool = _cache.get(self.key) if self.key is not None else None
-                if pool is not None and len(pool) < _cache_limit:
-                    pool.append(self.ptr)
-                else:
-                    rt.free(self.ptr)
-            except Exception:
-                pass
+        def __init__(self, st):
+            self.st, self.ptrs = st, []
 
-    def tb_props(index):
-        from . import abi
-        p = abi.DeviceProps()
-        L.tpg_device_props_get(index, C.byref(p))
-        return {"name": p.name.decode(), "processor-count": str(p.sm_count),
-                "free-memory": str(p.free_mem)}
+        def stage(self, host_ptr, lo, hi):
+            n = hi - lo
+            p = C.c_void_p()
+            rt.check(L.tpg_malloc_on(self.st.handle, n, C.byref(p)), "staging")
+            self.ptrs.append(p.value)
+            rt.stats["staged"] += 1
+            # pageable source: returns once the bytes are consumed
+            rt.check(L.tpg_memcpy_h2d(p.value, host_ptr + lo, n, self.st.handle), "H2D")
+            return p.value - lo
 
-    class _Buf:
-        """Device-visible pointer for a reference memoryview (staged when
-        the buffer is ordinary host memory)."""
-        __slots__ = ("ptr", "_tmp")
-
-        def __init__(self, mv):
-            self._tmp = None
-            if mv is None:
-                self.ptr = None
-                return
-            n = len(mv)
-            host = int(np.frombuffer(mv, dtype=np.uint8).ctypes.data) if n else 0
-            if n == 0 or rt.is_device_accessible(host):
-                self.ptr = host
-            else:
-                self._tmp = _Free(rt.malloc_managed(n))
-                C.memmove(self._tmp.ptr, host, n)
-                self.ptr = self._tmp.ptr
+        def done(self):
+            for p in self.ptrs:
+                L.tpg_free(self.st.device.index, p, self.st.handle)
 
     def _codec(fn):
-        name, order = decode_codec(ref_dtypes, fn)
-        return tb.Codec(D.by_name(name), order)
+        try:
+            return codec_of[fn]
+        except KeyError:
+            d, order = decode_codec(ref_dtypes, fn)
+            return ref_dtypes.by_name(d), order
 
     def _store(store):
-        name, order, mode = decode_store(ref_dtypes, store)
-        return tb.Store(D.by_name(name), order, mode)
+        cells = _cells(store)
+        pack = cells.get("pack")
+        if pack is None:
+            raise errors.DeviceError("gpu table: unrecognised store closure")
+        d, order = _codec(pack)
+        return d, order, cells.get("mode", "standard"), cells.get("ctx")
 
-    def _plan(pl):
-        return IterPlan(pl.extents, pl.strides)
+    def _operand(ptr, base, d, order, temps, extents=None, strides=None):
+        """tpg_operand for a storage pointer; host memory is staged."""
+        if ptr and not rt.is_gpu(ptr):
+            if extents is None:
+                raise errors.DeviceError("gpu table: host operand without a plan")
+            lo, hi = _span(extents, strides, base, d.size)
+            if hi > lo:
+                ptr = temps.stage(ptr, lo, hi)
+        return abi.make_operand(ptr, base, d.wire_code, order == "big")
 
-    def _sync():
-        _native.check(L.tpg_stream_sync(None), "sync")
+    def _plan(pl, strides=None):
+        return abi.make_plan(pl.extents, strides if strides is not None else pl.strides)
 
+    def _loss_message(d):
+        return f"value cannot be represented as {d.name}"
+
+    def _run(st, mode, ctx, to, launch, check=None):
+        """Launch with the reference's mode semantics (cast loss -> ctx)."""
+        if mode in ("standard", "complex"):
+            rt.check(launch(), "kernel")
+            return
+        rt.drain(st)
+        if mode == "error" and check is not None:
+            rt.check(check(), "kernel check")
+            bits = rt.drain(st)
+            if bits & FLAG_INT_DIV0:
+                raise errors.DomainError("integer division by zero")
+            if bits & FLAG_CAST_LOSS:
+                if ctx is not None:
+                    ctx.domain_loss(_loss_message(to))
+                raise errors.DomainError(_loss_message(to))
+            rt.check(launch(), "kernel")
+            return
+        rt.check(launch(), "kernel")
+        bits = rt.drain(st)
+        if bits & FLAG_CAST_LOSS:
+            if ctx is not None:
+                ctx.domain_loss(_loss_message(to))   # error: raises; warning: recorded
+            elif mode == "error":
+                raise errors.DomainError(_loss_message(to))
+
+    def _sink(fn):
+        s = decode_status(fn)
+        if s is not None:
+            rt.status_sink = s
+
+    # -- entries (SURVEY §8b signatures) -------------------------------------------
     def binary(op):
-        entry = tb.binary_entry(op)
+        code = abi.BINARY_CODE[op]
 
         def h(plan, d_buf, store, a_buf, a_unpack, b_buf, b_unpack, fn, bases):
-            ca = _codec(a_unpack)
-            entry(_plan(plan), _Buf(d_buf), _store(store), _Buf(a_buf), ca, _Buf(b_buf),
-                  _codec(b_unpack), tb.BinaryFn(op, D.widen_for_compute(ca.dtype)), bases)
-            _sync()
+            dd, dord, mode, ctx = _store(store)
+            da, aord = _codec(a_unpack)
+            db, bord = _codec(b_unpack)
+            dptr, aptr, bptr = rt.address(d_buf), rt.address(a_buf), rt.address(b_buf)
+            dev = rt.blocks[dptr][0]
+            st = rt.current(dev)
+            _sink(fn)
+            compute = ref_dtypes.widen_for_compute(da).wire_code
+            temps = _Temps(st)
+            ops, strides = [], [list(plan.strides[0])]
+            for ptr, d, order, base, v in ((aptr, da, aord, bases[1], 1),
+                                           (bptr, db, bord, bases[2], 2)):
+                fused = None
+                lz = rt.lazy.get(ptr)
+                if lz is not None and lz.src_ptr != dptr:
+                    fused = _fuse_strides(lz.plan, plan.extents, plan.strides[v], base, d.size)
+                if fused is not None:
+                    s, off = fused
+                    with rt.lock:
+                        keep = rt.lazy.get(ptr) is lz
+                    if keep:
+                        rt.stats["fused"] += 1
+                        o = abi.make_operand(lz.src_op.base, lz.src_op.offset + off,
+                                             lz.src_op.dtype, lz.src_op.big_endian)
+                        ops.append(o)
+                        strides.append(s)
+                        continue
+                rt.before_read(ptr)
+                ops.append(_operand(ptr, base, d, order, temps, plan.extents, plan.strides[v]))
+                strides.append(list(plan.strides[v]))
+            rt.before_write(dptr)
+            p = abi.make_plan(plan.extents, strides)
+            dop = abi.make_operand(dptr, bases[0], dd.wire_code, dord == "big")
+            args = (st.handle, code, C.byref(p), C.byref(dop), C.byref(ops[0]), C.byref(ops[1]),
+                    compute, MODE_CODE[mode])
+            _run(st, mode, ctx, dd, lambda: L.tpg_binary(*args), lambda: L.tpg_binary_check(*args))
+            temps.done()
+        h.__name__ = f"gpu_{op}"
         return h
 
     def unary(op):
-        entry = tb.unary_entry(op)
+        code = abi.UNARY_CODE[op]
 
         def h(plan, d_buf, store, a_buf, a_unpack, fn, bases):
-            ca = _codec(a_unpack)
-            fc = op != "identity" and unary_forces_complex(fn) and not ca.dtype.is_complex
-            entry(_plan(plan), _Buf(d_buf), _store(store), _Buf(a_buf), ca,
-                  tb.UnaryFn(op, D.widen_for_compute(ca.dtype), "standard", fc), bases)
-            _sync()
+            dd, dord, mode, ctx = _store(store)
+            da, aord = _codec(a_unpack)
+            dptr, aptr = rt.address(d_buf), rt.address(a_buf)
+            dev = rt.blocks[dptr][0]
+            st = rt.current(dev)
+            if op != "identity":
+                _sink(fn)
+            if op == "identity" and _try_lazy(plan, dptr, dd, dord, mode, aptr, da, aord, bases,
+                                             a_buf, dev):
+                return
+            rt.before_read(aptr)
+            rt.before_write(dptr)
+            temps = _Temps(st)
+            a = _operand(aptr, bases[1], da, aord, temps, plan.extents, plan.strides[1])
+            dop = abi.make_operand(dptr, bases[0], dd.wire_code, dord == "big")
+            p = _plan(plan)
+            if op == "identity":
+                comp, fc = da.wire_code, 0
+            else:
+                comp = ref_dtypes.widen_for_compute(da).wire_code
+                fc = int(unary_forces_complex(fn) and not da.is_complex)
+            args = (st.handle, code, C.byref(p), C.byref(dop), C.byref(a), comp, MODE_CODE[mode],
+                    fc)
+            _run(st, mode, ctx, dd, lambda: L.tpg_unary(*args), lambda: L.tpg_unary_check(*args))
+            temps.done()
+        h.__name__ = f"gpu_{op}"
         return h
 
+    def _try_lazy(plan, dptr, dd, dord, mode, aptr, da, aord, bases, a_buf, dev):
+        """Record a lossless gpu->gpu dtype conversion into a fresh dense
+        tensor instead of launching it (ops._dtype_convert, ops.py:121-124)."""
+        if (mode != "standard" or da is dd or bases[0] != 0 or not rt.is_gpu(aptr)
+                or aptr == dptr or rt.blocks[aptr][0] != dev or aptr in rt.lazy
+                or not ref_dtypes.lossless_castable(da, dd)
+                or not _is_dense(plan.extents, plan.strides[0], dd.size)
+                or plan.total == 0):
+            return False
+        lz = _Lazy()
+        lz.device, lz.plan = dev, plan
+        lz.dst_ptr, lz.src_ptr = dptr, aptr
+        lz.dst_op = abi.make_operand(dptr, 0, dd.wire_code, dord == "big")
+        lz.src_op = abi.make_operand(aptr, bases[1], da.wire_code, aord == "big")
+        lz.keep = a_buf  # the source storage stays alive while the copy is pending
+        lz.src_dtype, lz.dst_dtype, lz.src_order = da, dd, aord
+        rt.before_write(dptr)
+        rt.stats["lazy"] += 1
+        with rt.lock:
+            rt.lazy[dptr] = lz
+            rt.lazy_by_src.setdefault(aptr, set()).add(dptr)
+        return True
+
     def reduce_(op):
-        entry = tb.reduce_entry(op)
+        code = abi.REDUCE_CODE[op]
 
         def h(outer, inner, d_buf, store, a_buf, a_unpack, init, step, fin, bases):
-            ca = _codec(a_unpack)
+            dd, dord, mode, ctx = _store(store)
+            da, aord = _codec(a_unpack)
+            dptr, aptr = rt.address(d_buf), rt.address(a_buf)
+            dev = rt.blocks[dptr][0]
+            st = rt.current(dev)
             p = norm_order(step) if op == "norm" else 2.0
-            acc = tb.ReduceAcc(op, D.widen_for_compute(ca.dtype), p)
-            entry(_plan(outer), _plan(inner), _Buf(d_buf), _store(store), _Buf(a_buf), ca,
-                  acc, acc, acc, bases)
-            _sync()
+            rt.before_read(aptr)
+            rt.before_write(dptr)
+            temps = _Temps(st)
+            if aptr and not rt.is_gpu(aptr):
+                ext = tuple(outer.extents) + tuple(inner.extents)
+                strd = tuple(outer.strides[1]) + tuple(inner.strides[0])
+                a = _operand(aptr, bases[1], da, aord, temps, ext, strd)
+            else:
+                a = abi.make_operand(aptr, bases[1], da.wire_code, aord == "big")
+            dop = abi.make_operand(dptr, bases[0], dd.wire_code, dord == "big")
+            po, pi = _plan(outer), _plan(inner)
+            comp = ref_dtypes.widen_for_compute(da).wire_code
+            args = (st.handle, code, float(p), C.byref(po), C.byref(pi), C.byref(dop), C.byref(a),
+                    comp, MODE_CODE[mode])
+            _run(st, mode, ctx, dd, lambda: L.tpg_reduce(*args))
+            temps.done()
+        h.__name__ = f"gpu_reduce_{op}"
         return h
 
     def matmul(d_buf, d_base, d_strides, store, a_buf, a_base, a_strides, a_unpack, b_buf,
                b_base, b_strides, b_unpack, m, n, k, mul, init, step, fin):
-        ca = _codec(a_unpack)
-        tb.matmul_entry(_Buf(d_buf), d_base, d_strides, _store(store), _Buf(a_buf), a_base,
-                        a_strides, ca, _Buf(b_buf), b_base, b_strides, _codec(b_unpack), m, n, k,
-                        tb.MatmulFn(D.widen_for_compute(ca.dtype)), None, None, None)
-        _sync()
+        dd, dord, mode, ctx = _store(store)
+        da, aord = _codec(a_unpack)
+        db, bord = _codec(b_unpack)
+        dptr, aptr, bptr = rt.address(d_buf), rt.address(a_buf), rt.address(b_buf)
+        dev = rt.blocks[dptr][0]
+        st = rt.current(dev)
+        rt.before_read(aptr)
+        rt.before_read(bptr)
+        rt.before_write(dptr)
+        temps = _Temps(st)
+        a = _operand(aptr, a_base, da, aord, temps, (m, k), a_strides)
+        b = _operand(bptr, b_base, db, bord, temps, (k, n), b_strides)
+        dop = abi.make_operand(dptr, d_base, dd.wire_code, dord == "big")
+        ds, as_, bs = ((C.c_int64 * 2)(*s) for s in (d_strides, a_strides, b_strides))
+        comp = ref_dtypes.widen_for_compute(da).wire_code
+        _run(st, mode, ctx, dd, lambda: L.tpg_matmul(st.handle, C.byref(dop), ds, C.byref(a), as_,
+                                                     C.byref(b), bs, m, n, k, comp,
+                                                     MODE_CODE[mode]))
+        temps.done()
 
     def fill(plan, buf, pack, value, base):
-        tb.fill_entry(_plan(plan), _Buf(buf), _codec(pack), value, base)
-        _sync()
+        d, order = _codec(pack)
+        ptr = rt.address(buf)
+        st = rt.current(rt.blocks[ptr][0])
+        rt.before_write(ptr)
+        raw = bytearray(d.size)
+        pack(raw, 0, value)  # the reference's own packing: exact element bytes
+        cbuf = C.create_string_buffer(bytes(raw), d.size)
+        dop = abi.make_operand(ptr, base, d.wire_code, order == "big")
+        rt.check(L.tpg_fill(st.handle, C.byref(_plan(plan)), C.byref(dop), cbuf, d.size), "fill")
 
     def arange(plan, buf, pack, cast_fn, base):
-        tb.arange_entry(_plan(plan), _Buf(buf), _codec(pack), cast_fn, base)
-        _sync()
+        d, order = _codec(pack)
+        ptr = rt.address(buf)
+        st = rt.current(rt.blocks[ptr][0])
+        rt.before_write(ptr)
+        dop = abi.make_operand(ptr, base, d.wire_code, order == "big")
+        rt.check(L.tpg_arange(st.handle, C.byref(_plan(plan)), C.byref(dop)), "arange")
 
     def byteswap(buf, base, plan, dtype):
-        tb.byteswap_entry(_Buf(buf), base, _plan(plan), D.by_name(dtype.name))
-        _sync()
+        ptr = rt.address(buf)
+        st = rt.current(rt.blocks[ptr][0])
+        rt.before_write(ptr)
+        dop = abi.make_operand(ptr, base, dtype.wire_code, False)
+        rt.check(L.tpg_byteswap(st.handle, C.byref(_plan(plan)), C.byref(dop)), "byteswap")
+
+    def _pairs(pairs):
+        arr = np.ascontiguousarray(np.asarray(pairs, dtype=np.int64).reshape(-1))
+        return arr, arr.ctypes.data_as(C.POINTER(C.c_int64))
+
+    def _stage_whole(ptr, nbytes, temps):
+        if ptr and not rt.is_gpu(ptr) and nbytes:
+            return temps.stage(ptr, 0, nbytes)
+        return ptr
 
     def gather(dst_buf, src_buf, pairs, size):
-        tb.gather_entry(_Buf(dst_buf), _Buf(src_buf), pairs, size)
-        _sync()
+        dptr, sptr = rt.address(dst_buf), rt.address(src_buf)
+        st = rt.current(rt.blocks[dptr][0])
+        rt.before_read(sptr)
+        rt.before_write(dptr)
+        arr, pp = _pairs(pairs)
+        temps = _Temps(st)
+        sptr = _stage_whole(sptr, len(src_buf), temps)
+        rt.check(L.tpg_gather(st.handle, dptr, sptr, pp, arr.size // 2, size), "gather")
+        temps.done()
 
     def scatter(pairs, d_buf, store, s_buf, s_unpack):
-        tb.scatter_entry(pairs, _Buf(d_buf), _store(store), _Buf(s_buf), _codec(s_unpack))
-        _sync()
+        dd, dord, mode, ctx = _store(store)
+        ds_, sord = _codec(s_unpack)
+        dptr, sptr = rt.address(d_buf), rt.address(s_buf)
+        st = rt.current(rt.blocks[dptr][0])
+        rt.before_read(sptr)
+        rt.before_write(dptr)
+        arr, pp = _pairs(pairs)
+        temps = _Temps(st)
+        sptr = _stage_whole(sptr, len(s_buf), temps)
+        dop = abi.make_operand(dptr, 0, dd.wire_code, dord == "big")
+        sop = abi.make_operand(sptr, 0, ds_.wire_code, sord == "big")
+        _run(st, mode, ctx, dd, lambda: L.tpg_scatter(st.handle, pp, arr.size // 2, C.byref(dop),
+                                                      C.byref(sop), MODE_CODE[mode]))
+        temps.done()
 
     def scatter_fill(offsets, d_buf, pack, value):
-        tb.scatter_fill_entry(offsets, _Buf(d_buf), _codec(pack), value)
-        _sync()
+        d, order = _codec(pack)
+        dptr = rt.address(d_buf)
+        st = rt.current(rt.blocks[dptr][0])
+        rt.before_write(dptr)
+        arr, pp = _pairs(offsets)
+        raw = bytearray(d.size)
+        pack(raw, 0, value)
+        cbuf = C.create_string_buffer(bytes(raw), d.size)
+        rt.check(L.tpg_scatter_fill(st.handle, pp, arr.size, dptr, cbuf, d.size), "scatter_fill")
 
     table = {}
-    for op in tb.BINARY_OPS:
+    for op in abi.BINARY_CODE:
         table[op] = binary(op)
-    for op in tb.UNARY_OPS:
-        table[op] = unary(op)
+    for op in abi.UNARY_CODE:
+        if op != "identity":
+            table[op] = unary(op)
     table["copy"] = unary("identity")
-    for op in tb.REDUCE_OPS:
+    for op in abi.REDUCE_CODE:
         table[f"reduce_{op}" if op in ("minimum", "maximum") else op] = reduce_(op)
     table.update(matmul=matmul, fill=fill, arange=arange, byteswap=byteswap, gather=gather,
                  scatter=scatter, scatter_fill=scatter_fill)
@@ -311,44 +812,141 @@ def register(tidepool_module, count: int | None = None):
     L.tpg_device_count(C.byref(n))
     n = n.value if count is None else min(n.value, count)
     devs = [GpuDevice(i) for i in range(n)]
+    rt.devices = {d.index: d for d in devs}
     ref_devices._devices.extend(devs)
+
+    # the registry is rebuilt by configure(); keep the gpu devices in it
     orig_configure = ref_devices.configure
 
     def configure(*a, **k):
         orig_configure(*a, **k)
         ref_devices._devices.extend(devs)
-
     ref_devices.configure = configure
 
-    # descriptor-based raw gather.  The reference builds
-    # a Python list of (dst, src) byte-offset pairs for every clone,
-    # reshape copy and byte-order-preserving transfer (tensors.py:686-699);
-    # for gpu -> same-gpu moves the plugin replaces that with one
-    # canonical plan and the tpg_gather_plan kernel.  tensors._raw_gather
-    # is looked up at call time by its callers (ops.py:115,195,
-    # tensors.contiguous_clone), so rebinding the module attribute is
-    # enough.  Other device pairs keep the reference path (table "gather").
-    ref_tensors = tp.tensors
+    # streams created for a gpu device are CUDA streams
+    orig_create_stream = ref_devices.create_stream
+
+    def create_stream(device):
+        if device.type is gpu_type:
+            return GpuStream(device)
+        return orig_create_stream(device)
+    ref_devices.create_stream = create_stream
+    tp.create_stream = create_stream
+
+    # status visibility: drain every gpu stream before the reference reads
+    # or clears its status set (ops.py:31-38)
+    orig_get, orig_clear = ref_ops.get_status, ref_ops.clear_status
+
+    def _drain_all():
+        for d in devs:
+            for st in list(rt.streams.get(d.index, ())):
+                st.sync()
+
+    def get_status():
+        _drain_all()
+        return orig_get()
+
+    def clear_status():
+        _drain_all()
+        orig_clear()
+    ref_ops.get_status, ref_ops.clear_status = get_status, clear_status
+    tp.get_status, tp.clear_status = get_status, clear_status
+
+    # -- descriptor transfers -----------------------------------------
     orig_raw_gather = ref_tensors._raw_gather
 
     def raw_gather(src, dst):
-        if (dst.device.type is gpu_type and src.device is dst.device
-                and src.dtype.size == dst.dtype.size and src.dims == dst.dims):
-            n = 1
-            for e in dst.dims:
-                n *= e
-            if n == 0:
-                return
-            if src.storage.stream is not dst.storage.stream:
-                src.storage.stream.sync()
-            plan = _plan(ref_tensors.canonicalize(dst, src)).to_c()
-            _native.check(L.tpg_gather_plan(None, C.byref(plan), _Buf(dst.storage.view()).ptr,
-                                            dst.offset, _Buf(src.storage.view()).ptr, src.offset,
-                                            src.dtype.size), "gather")
-            _sync()
+        """tensors._raw_gather (tensors.py:686-699) for gpu endpoints: one
+        canonical 2-view plan and one kernel instead of a Python pair list;
+        host endpoints move as one bulk PCIe copy of the touched span."""
+        sg, dg = src.device.type is gpu_type, dst.device.type is gpu_type
+        if not (sg or dg) or src.dtype.size != dst.dtype.size or src.dims != dst.dims:
+            return orig_raw_gather(src, dst)
+        total = 1
+        for e in dst.dims:
+            total *= e
+        if total == 0:
             return
-        return orig_raw_gather(src, dst)
+        plan = ref_tensors.canonicalize(dst, src)
+        size = src.dtype.size
+        if not dg:
+            # gpu -> host: dense host destinations only (one D2H of the span)
+            if not _is_dense(plan.extents, plan.strides[0], size):
+                return orig_raw_gather(src, dst)
+            src.storage.stream.sync()
+            _gather_to_host(plan, src, dst, size)
+            return
+        if src.storage.stream is not dst.storage.stream:
+            src.storage.stream.sync()
+        sptr, dptr = rt.address(src.storage.view()), rt.address(dst.storage.view())
+        st = dst.storage.stream if isinstance(dst.storage.stream, GpuStream) else \
+            dst.device.default_stream()
+        rt.before_read(sptr)
+        rt.before_write(dptr)
+        temps = _Temps(st)
+        soff = src.offset
+        if not rt.is_gpu(sptr):
+            lo, hi = _span(plan.extents, plan.strides[1], src.offset, size)
+            sptr = temps.stage(sptr, lo, hi)
+        p = _plan(plan)
+        rt.stats["gather_plan"] += 1
+        rt.check(L.tpg_gather_plan(st.handle, C.byref(p), dptr, dst.offset, sptr, soff, size),
+                 "gather")
+        temps.done()
+
+    def _gather_to_host(plan, src, dst, size):
+        st = src.device.default_stream()
+        sptr = rt.address(src.storage.view())
+        rt.before_read(sptr)
+        lo, hi = _span(plan.extents, plan.strides[0], dst.offset, size)
+        tmp = C.c_void_p()
+        rt.check(L.tpg_malloc_on(st.handle, hi - lo, C.byref(tmp)), "staging")
+        p = _plan(plan)
+        rt.check(L.tpg_gather_plan(st.handle, C.byref(p), tmp.value - lo, dst.offset, sptr,
+                                   src.offset, size), "gather")
+        hptr = rt.address(dst.storage.view())
+        rt.check(L.tpg_memcpy_d2h(hptr + lo, tmp.value, hi - lo, st.handle), "D2H")
+        L.tpg_free(src.device.index, tmp.value, st.handle)
+        rt.check(L.tpg_stream_sync(st.handle), "sync")
+        rt.stats["gather_to_host"] += 1
 
     raw_gather.reference = orig_raw_gather
     ref_tensors._raw_gather = raw_gather
+
+    # value copies gpu -> cpu (`cast(gpu_t, device=cpu)`, ops._run_copy,
+    # ops.py:668-687): the cpu table's `copy` would unpack every element
+    # through managed memory; for a gpu source, convert on the GPU into a
+    # staging block laid out like the (dense) host destination, then one D2H.
+    def cpu_copy_wrapper(original):
+        def h(plan, d_buf, store, s_buf, s_unpack, fn, bases):
+            sptr = rt.address(s_buf)
+            dd, dord, mode, ctx = _store(store)
+            if (not rt.is_gpu(sptr) or plan.total == 0
+                    or not _is_dense(plan.extents, plan.strides[0], dd.size)):
+                return original(plan, d_buf, store, s_buf, s_unpack, fn, bases)
+            ds_, sord = _codec(s_unpack)
+            dev = rt.blocks[sptr][0]
+            st = rt.devices[dev].default_stream()
+            rt.before_read(sptr)
+            lo, hi = _span(plan.extents, plan.strides[0], bases[0], dd.size)
+            tmp = C.c_void_p()
+            rt.check(L.tpg_malloc_on(st.handle, hi - lo, C.byref(tmp)), "staging")
+            dop = abi.make_operand(tmp.value - lo, bases[0], dd.wire_code, dord == "big")
+            sop = abi.make_operand(sptr, bases[1], ds_.wire_code, sord == "big")
+            p = _plan(plan)
+            args = (st.handle, 10, C.byref(p), C.byref(dop), C.byref(sop), ds_.wire_code,
+                    MODE_CODE[mode], 0)
+            try:
+                _run(st, mode, ctx, dd, lambda: L.tpg_unary(*args),
+                     lambda: L.tpg_unary_check(*args))
+                hptr = rt.address(d_buf)
+                rt.check(L.tpg_memcpy_d2h(hptr + lo, tmp.value, hi - lo, st.handle), "D2H")
+                rt.check(L.tpg_stream_sync(st.handle), "sync")
+                rt.stats["cpu_copy_from_gpu"] += 1
+            finally:
+                L.tpg_free(dev, tmp.value, st.handle)
+        return h
+
+    ref_dispatch.override_op("core", "cpu", "copy", cpu_copy_wrapper)
+    register.runtime = rt
     return devs

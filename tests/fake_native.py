@@ -1,0 +1,236 @@
+"""CPU test double of libtidepool_gpu.so (TEST INFRASTRUCTURE ONLY).
+
+Implements the subset of the C ABI (include/tidepool_gpu.h) the drop-in
+plugin calls, with "device" memory in host buffers and the kernels executed
+by the C oracle (oracle/tp_oracle.c, same plan / operand descriptors).  It
+lets the CPU suite drive tidepool_plugin.register() end to end - closure
+decoding, status / cast-loss routing into the unmodified reference, lazy
+casts, staging and descriptor transfers - without a GPU.  The product never
+loads it: register() only takes it through its `lib=` test hook.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+from paper_1810_08723_b200 import abi
+
+_DT_SIZE = {0: 1, 1: 1, 2: 1, 3: 2, 4: 2, 5: 4, 6: 4, 7: 8, 8: 8, 9: 2, 10: 4, 11: 8, 12: 4,
+            13: 8, 14: 16}
+_RAW = {1: 2, 2: 4, 4: 6, 8: 8, 16: 14}   # element size -> a dtype whose identity copy is byte-exact
+
+
+def _obj(ref):
+    return ref._obj if hasattr(ref, "_obj") else ref
+
+
+class FakeNative:
+    """Duck-typed stand-in for the ctypes library object."""
+
+    def __init__(self, oracle_lib, ndev=1):
+        self.o = oracle_lib
+        self.ndev = ndev
+        self.mem = {}          # ptr -> ctypes buffer (keeps host memory alive)
+        self.flags = [0] * ndev
+        self.inject = 0        # extra bits the next kernel reports (routing tests)
+        self.calls = []        # (name, ...) of every kernel launched
+        self.managed = set()
+
+    # -- runtime --------------------------------------------------------------
+    def tpg_last_error(self):
+        return b"fake error"
+
+    def tpg_device_count(self, out):
+        _obj(out).value = self.ndev
+        return 0
+
+    def tpg_device_props_get(self, dev, props):
+        p = _obj(props)
+        p.sm_count, p.total_mem, p.free_mem = 148, 1 << 30, 1 << 30
+        p.name = b"fake B200"
+        return 0
+
+    def _alloc(self, n):
+        buf = C.create_string_buffer(max(int(n), 1))
+        ptr = C.addressof(buf)
+        self.mem[ptr] = buf
+        return ptr
+
+    def tpg_malloc_managed(self, dev, n, out):
+        ptr = self._alloc(n)
+        self.managed.add(ptr)
+        _obj(out).value = ptr
+        return 0
+
+    def tpg_free_managed(self, ptr):
+        self.mem.pop(_int(ptr), None)
+        return 0
+
+    def tpg_malloc_on(self, stream, n, out):
+        _obj(out).value = self._alloc(n)
+        return 0
+
+    def tpg_free(self, dev, ptr, stream):
+        self.mem.pop(_int(ptr), None)
+        return 0
+
+    def tpg_default_stream(self, dev, out):
+        _obj(out).value = 0x1000 + dev
+        return 0
+
+    def tpg_stream_create(self, dev, out):
+        _obj(out).value = 0x2000 + dev
+        return 0
+
+    def tpg_stream_sync(self, s):
+        return 0
+
+    def tpg_event_create_untimed(self, out):
+        _obj(out).value = 0x3000
+        return 0
+
+    def tpg_event_record(self, ev, s):
+        return 0
+
+    def tpg_event_query(self, ev):
+        return 0
+
+    def tpg_event_sync(self, ev):
+        return 0
+
+    def tpg_memcpy_h2d(self, dst, src, n, s):
+        C.memmove(_int(dst), _int(src), n)
+        return 0
+
+    tpg_memcpy_d2h = tpg_memcpy_h2d
+
+    def _dev_of(self, stream):
+        s = _int(stream)
+        return (s & 0xff) if s else 0
+
+    def tpg_flags_take(self, stream, out):
+        d = self._dev_of(stream)
+        _obj(out).value = self.flags[d]
+        self.flags[d] = 0
+        return 0
+
+    def _flag(self, st):
+        self.flags[0] |= st.value | self.inject
+        self.inject = 0
+
+    # -- kernels (oracle) ---------------------------------------------------------
+    def tpg_binary(self, s, op, plan, d, a, b, comp, mode):
+        self.calls.append(("binary", op, _obj(a).dtype, _obj(b).dtype))
+        st = C.c_uint32(0)
+        rc = self.o.tpo_binary(op, plan, d, a, b, comp, mode, C.byref(st))
+        self._flag(st)
+        return rc
+
+    def tpg_binary_check(self, s, op, plan, d, a, b, comp, mode):
+        st = C.c_uint32(0)
+        with _Scratch(self, d) as dd:
+            rc = self.o.tpo_binary(op, plan, C.byref(dd), a, b, comp, mode, C.byref(st))
+        self._flag(st)
+        return rc
+
+    def tpg_unary(self, s, op, plan, d, a, comp, mode, fc):
+        self.calls.append(("unary", op, _obj(a).dtype, _obj(d).dtype))
+        st = C.c_uint32(0)
+        rc = self.o.tpo_unary(op, plan, d, a, comp, mode, fc, C.byref(st))
+        self._flag(st)
+        return rc
+
+    def tpg_unary_check(self, s, op, plan, d, a, comp, mode, fc):
+        st = C.c_uint32(0)
+        with _Scratch(self, d) as dd:
+            rc = self.o.tpo_unary(op, plan, C.byref(dd), a, comp, mode, fc, C.byref(st))
+        self._flag(st)
+        return rc
+
+    def tpg_reduce(self, s, op, p, po, pi, d, a, comp, mode):
+        self.calls.append(("reduce", op))
+        st = C.c_uint32(0)
+        rc = self.o.tpo_reduce(op, p, po, pi, d, a, comp, mode, C.byref(st))
+        self._flag(st)
+        return rc
+
+    def tpg_matmul(self, s, d, ds, a, as_, b, bs, m, n, k, comp, mode):
+        self.calls.append(("matmul",))
+        st = C.c_uint32(0)
+        rc = self.o.tpo_matmul(d, ds, a, as_, b, bs, m, n, k, comp, mode, C.byref(st))
+        self._flag(st)
+        return rc
+
+    def tpg_fill(self, s, plan, d, value, size):
+        self.calls.append(("fill",))
+        return self.o.tpo_fill(plan, d, value, size)
+
+    def tpg_arange(self, s, plan, d):
+        self.calls.append(("arange",))
+        return self.o.tpo_arange(plan, d)
+
+    def tpg_byteswap(self, s, plan, d):
+        self.calls.append(("byteswap",))
+        return self.o.tpo_byteswap(plan, d)
+
+    def tpg_gather_plan(self, s, plan, dst, doff, src, soff, size):
+        self.calls.append(("gather_plan",))
+        dt = _RAW[size]
+        d = abi.make_operand(_int(dst), doff, dt, False)
+        a = abi.make_operand(_int(src), soff, dt, False)
+        st = C.c_uint32(0)
+        return self.o.tpo_unary(10, plan, C.byref(d), C.byref(a), dt, 0, 0, C.byref(st))
+
+    def tpg_gather(self, s, dst, src, pairs, n, size):
+        self.calls.append(("gather",))
+        for i in range(n):
+            C.memmove(_int(dst) + pairs[2 * i], _int(src) + pairs[2 * i + 1], size)
+        return 0
+
+    def tpg_scatter(self, s, pairs, n, d, sop, mode):
+        self.calls.append(("scatter",))
+        dd, ss = _obj(d), _obj(sop)
+        st = C.c_uint32(0)
+        for i in range(n):
+            p = abi.make_plan([], [[], []])
+            do = abi.make_operand(dd.base, pairs[2 * i], dd.dtype, dd.big_endian)
+            so = abi.make_operand(ss.base, pairs[2 * i + 1], ss.dtype, ss.big_endian)
+            self.o.tpo_unary(10, C.byref(p), C.byref(do), C.byref(so), ss.dtype, mode, 0,
+                             C.byref(st))
+        self._flag(st)
+        return 0
+
+    def tpg_scatter_fill(self, s, offsets, n, dbase, value, size):
+        self.calls.append(("scatter_fill",))
+        for i in range(n):
+            C.memmove(_int(dbase) + offsets[i], value, size)
+        return 0
+
+
+class _Scratch:
+    """Dry-run destination: the kernel writes into a throwaway copy."""
+
+    def __init__(self, fake, dref):
+        self.fake, self.d = fake, _obj(dref)
+
+    def __enter__(self):
+        base = self.d.base
+        for ptr, buf in self.fake.mem.items():
+            if ptr <= base < ptr + len(buf):
+                self.copy = C.create_string_buffer(buf.raw, len(buf))
+                o = abi.make_operand(C.addressof(self.copy) + (base - ptr), self.d.offset,
+                                     self.d.dtype, self.d.big_endian)
+                return o
+        raise AssertionError("dry-run destination outside fake device memory")
+
+    def __exit__(self, *exc):
+        return False
+
+
+def _int(p):
+    if isinstance(p, int):
+        return p
+    if p is None:
+        return 0
+    v = getattr(p, "value", p)
+    return int(v or 0)

@@ -213,107 +213,248 @@ def l2_flush(L, stream, flush_buf):
 # ---------------------------------------------------------------------------
 # workloads
 # ---------------------------------------------------------------------------
-def cfg2_inputs(tp, dev):
+class _S:
+    """A stream handle with the interface timed_steps() expects."""
+
+    def __init__(self, L, handle):
+        self.L, self.handle = L, handle
+
+    def sync(self):
+        self.L.tpg_stream_sync(self.handle)
+
+
+def _ck(L, rc, what):
+    if rc != 0:
+        raise RuntimeError(f"{what}: {L.tpg_last_error().decode()}")
+
+
+def _dmalloc(L, nbytes, dev=0):
+    p = C.c_void_p()
+    _ck(L, L.tpg_malloc(dev, nbytes, C.byref(p)), "tpg_malloc")
+    return p.value
+
+
+def _pinned(L, shape, dtype):
+    """numpy view of page-locked host memory (tpg_host_alloc)."""
+    n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    p = C.c_void_p()
+    _ck(L, L.tpg_host_alloc(n, C.byref(p)), "tpg_host_alloc")
+    raw = (C.c_ubyte * n).from_address(p.value)
+    return np.frombuffer(raw, dtype=np.uint8).view(dtype).reshape(shape, order="F"), p.value
+
+
+def cfg2_host_inputs():
     rng3, rng4 = np.random.default_rng(3), np.random.default_rng(4)
     x16 = np.asfortranarray(rng3.integers(-1000, 1000, (N, N), endpoint=True).astype(np.int16))
     r = np.asfortranarray(rng4.standard_normal((1, N)).astype(np.float32))
-    X = tp.from_numpy(x16, dev)
-    R = tp.from_numpy(r, dev)
-    V = tp.apply_index(tp.transpose(X), (slice(None, None, -1), slice(None)))
-    assert V.strides == (-8192, 2), V.strides
-    return x16, r, X, R, V
+    return x16, r
 
 
-def bench_cfg2(tp, dev, steps, warmup, L):
-    x16, r, X, R, V = cfg2_inputs(tp, dev)
-    out = tp.tensor_create((N, N), tp.float, dev)
-    stream = dev.default_stream()
-    flush_buf = dev.allocate(FLUSH_BYTES)
+def cfg2_plan(abi, x_ptr, r_ptr, o_ptr, c0=0, cols=N):
+    """tpg_binary descriptors of cfg2's add over result columns [c0, c0+cols):
+    dest f32 column-major (4, 4N); V = reversed transpose of the int16
+    column-major X, V(i, j) = X(j, N-1-i): strides (-2N, 2) from byte offset
+    (N-1)*2N; R row broadcast down the columns: strides (0, 4)."""
+    plan = abi.make_plan([N, cols], [[4, 4 * N], [-2 * N, 2], [0, 4]])
+    d = abi.make_operand(o_ptr, 4 * N * c0, 10, False)
+    a = abi.make_operand(x_ptr, (N - 1) * 2 * N + 2 * c0, 3, False)
+    b = abi.make_operand(r_ptr, 4 * c0, 10, False)
+    return plan, d, a, b
+
+
+def bench_cfg2(L, steps, warmup, dev=0):
+    """cfg2 through the C ABI (include/tidepool_gpu.h): `value` = device time
+    of tpg_binary with inputs resident in HBM (L2 flushed between steps);
+    `e2e` = the same call per step with the int16 matrix and the row coming
+    from pinned host buffers and the float32 result going back to one,
+    copies inside the timed region."""
+    from paper_1810_08723_b200 import abi
+    x16, r = cfg2_host_inputs()
+    sh = C.c_void_p()
+    _ck(L, L.tpg_default_stream(dev, C.byref(sh)), "stream")
+    stream = _S(L, sh.value)
+    X, R, O = _dmalloc(L, N * N * 2), _dmalloc(L, N * 4), _dmalloc(L, N * N * 4)
+    flush_buf = _dmalloc(L, FLUSH_BYTES)
+    _ck(L, L.tpg_memcpy_h2d(X, x16.ctypes.data, x16.nbytes, stream.handle), "H2D")
+    _ck(L, L.tpg_memcpy_h2d(R, r.ctypes.data, r.nbytes, stream.handle), "H2D")
+    plan, d, a, b = cfg2_plan(abi, X, R, O)
+    args = (stream.handle, 0, C.byref(plan), C.byref(d), C.byref(a), C.byref(b), 10, 0)
 
     def flush():
         l2_flush(L, stream, flush_buf)
 
     def step():
-        tp.add(V, R, dest=out)
+        _ck(L, L.tpg_binary(*args), "tpg_binary")
 
     for _ in range(warmup):
         flush()
         step()
     stream.sync()
     ms = timed_steps(L, stream, step, steps, flush)
-    # end to end through the public API with host buffers: every step
-    # uploads its inputs from pinned host memory, runs the op and downloads
-    # the result (tp.pinned / tp.upload / tp.download / tp.use_stream),
-    # pipelined over E2E_CHUNKS slabs on three streams -- one per copy
-    # engine direction plus one for the kernels -- chained by per-slab
-    # waits: uploads run back to back on the H2D engine, downloads back to
-    # back on the D2H engine (PCIe is full duplex), so the step costs about
-    # one slab upload + the whole download (E2E_SPLIT picks the slab shape).
-    hx = tp.pinned((N, N), np.int16)
+    want = (x16.T[::-1, :].astype(np.float64) + r.astype(np.float64)).astype(np.float32)
+    got = np.empty((N, N), dtype=np.float32, order="F")
+    _ck(L, L.tpg_memcpy_d2h(got.ctypes.data, O, got.nbytes, stream.handle), "D2H")
+    stream.sync()
+    assert np.array_equal(got, want), "cfg2 device result mismatch"
+
+    # ---- e2e: pinned host buffers, pipelined over E2E_CHUNKS column slabs
+    # on three streams (uploads back to back on the H2D engine, the adds on
+    # a compute stream, downloads back to back on the D2H engine; PCIe is
+    # full duplex), chained by per-slab stream waits.  V's columns [c0, c1)
+    # are X's rows [c0, c1): a pitched upload; the result slab is one
+    # contiguous download.
+    hx, _ = _pinned(L, (N, N), np.int16)
     hx[...] = x16
-    hr = tp.pinned((1, N), np.float32)
+    hr, _ = _pinned(L, (1, N), np.float32)
     hr[...] = r
-    ho = tp.pinned((N, N), np.float32)
-    up, comp, down = dev.create_stream(), dev.create_stream(), dev.create_stream()
-    rows = N // E2E_CHUNKS
-    if E2E_SPLIT == "rows":
-        # V's rows [r0, r1) = X16's columns [N-r1, N-r0): contiguous upload,
-        # pitched download
-        vch = [tp.apply_index(V, (slice(i * rows, (i + 1) * rows), slice(None)))
-               for i in range(E2E_CHUNKS)]
-        och = [tp.apply_index(out, (slice(i * rows, (i + 1) * rows), slice(None)))
-               for i in range(E2E_CHUNKS)]
-        xch = [tp.apply_index(X, (slice(None), slice(N - (i + 1) * rows, N - i * rows)))
-               for i in range(E2E_CHUNKS)]
-        hxs = [hx[:, N - (i + 1) * rows:N - i * rows] for i in range(E2E_CHUNKS)]
-        hos = [ho[i * rows:(i + 1) * rows, :] for i in range(E2E_CHUNKS)]
-        rch = [R] * E2E_CHUNKS
-    else:
-        # V's columns [c0, c1) = X16's rows [c0, c1): pitched upload,
-        # contiguous download (the larger direction)
-        vch = [tp.apply_index(V, (slice(None), slice(i * rows, (i + 1) * rows)))
-               for i in range(E2E_CHUNKS)]
-        och = [tp.apply_index(out, (slice(None), slice(i * rows, (i + 1) * rows)))
-               for i in range(E2E_CHUNKS)]
-        xch = [tp.apply_index(X, (slice(i * rows, (i + 1) * rows), slice(None)))
-               for i in range(E2E_CHUNKS)]
-        hxs = [hx[i * rows:(i + 1) * rows, :] for i in range(E2E_CHUNKS)]
-        hos = [ho[:, i * rows:(i + 1) * rows] for i in range(E2E_CHUNKS)]
-        rch = [tp.apply_index(R, (slice(None), slice(i * rows, (i + 1) * rows)))
-               for i in range(E2E_CHUNKS)]
+    ho, _ = _pinned(L, (N, N), np.float32)
+    hs = []
+    for _ in range(3):
+        h = C.c_void_p()
+        _ck(L, L.tpg_stream_create(dev, C.byref(h)), "stream")
+        hs.append(h.value)
+    up, comp, down = hs
+    cols = N // E2E_CHUNKS
+    slabs = [cfg2_plan(abi, X, R, O, i * cols, cols) for i in range(E2E_CHUNKS)]
+    launches = [0]
 
     def e2e_step():
-        up.wait_for(stream)
-        tp.upload(hr, R, up)
-        for i in range(E2E_CHUNKS):
-            tp.upload(hxs[i], xch[i], up)
-            comp.wait_for(up)
-            with tp.use_stream(comp):
-                tp.add(vch[i], rch[i], dest=och[i])
-            down.wait_for(comp)
-            tp.download(och[i], hos[i], down)
-        stream.wait_for(down)
+        L.tpg_stream_wait(up, stream.handle)
+        _ck(L, L.tpg_memcpy_h2d(R, hr.ctypes.data, hr.nbytes, up), "H2D")
+        for i, (p, dd, aa, bb) in enumerate(slabs):
+            c0 = i * cols
+            _ck(L, L.tpg_memcpy2d(X + 2 * c0, 2 * N, hx.ctypes.data + 2 * c0, 2 * N, 2 * cols, N,
+                                  up), "H2D slab")
+            L.tpg_stream_wait(comp, up)
+            _ck(L, L.tpg_binary(comp, 0, C.byref(p), C.byref(dd), C.byref(aa), C.byref(bb), 10,
+                                0), "tpg_binary")
+            launches[0] += 1
+            L.tpg_stream_wait(down, comp)
+            _ck(L, L.tpg_memcpy_d2h(ho.ctypes.data + 4 * N * c0, O + 4 * N * c0, 4 * N * cols,
+                                    down), "D2H slab")
+        L.tpg_stream_wait(stream.handle, down)
 
     for _ in range(2):
         e2e_step()
     stream.sync()
+    launches[0] = 0
     e2e_steps = max(3, steps // 4)
     t0 = time.perf_counter()
     e2e_ms = timed_steps(L, stream, e2e_step, e2e_steps, None, gate=False)
     wall = (time.perf_counter() - t0) * 1e3 / e2e_steps
-    # correctness spot check against the host result of the same bytes
-    want = (x16.T[::-1, :].astype(np.float64) + r.astype(np.float64)).astype(np.float32)
     assert np.array_equal(ho, want), "cfg2 e2e result mismatch"
-    # the PCIe bound of the e2e step on this box: the step's whole download
-    # (67 MB, one contiguous copy) and whole upload, each timed alone
+    # the box's PCIe rates for the same bytes, each copy timed alone
     d2h_ms = statistics.median(timed_steps(
-        L, stream, lambda: tp.download(out, ho, stream), 5, None, gate=False))
+        L, stream, lambda: L.tpg_memcpy_d2h(ho.ctypes.data, O, ho.nbytes, stream.handle), 5,
+        None, gate=False))
     h2d_ms = statistics.median(timed_steps(
-        L, stream, lambda: tp.upload(hx, X, stream), 5, None, gate=False))
-    pcie = {"d2h_GBps": round(ho.nbytes / d2h_ms / 1e6, 1), "h2d_GBps": round(hx.nbytes / h2d_ms / 1e6, 1),
+        L, stream, lambda: L.tpg_memcpy_h2d(X, hx.ctypes.data, hx.nbytes, stream.handle), 5,
+        None, gate=False))
+    pcie = {"d2h_GBps": round(ho.nbytes / d2h_ms / 1e6, 1),
+            "h2d_GBps": round(hx.nbytes / h2d_ms / 1e6, 1),
             "bound_ms": round(max(d2h_ms, h2d_ms), 3)}
-    dev.release(flush_buf, stream)
-    return ms, e2e_ms, wall, x16.nbytes + r.nbytes, N * N * 4, pcie
+    for p in (X, R, O, flush_buf):
+        L.tpg_free(dev, p, stream.handle)
+    return {"ms": ms, "e2e_ms": e2e_ms, "wall": wall, "h2d": x16.nbytes + r.nbytes,
+            "d2h": N * N * 4, "pcie": pcie, "launches": steps + launches[0]}
+
+
+def bench_plugin(L, steps=20, warmup=3):
+    """cfg2 through the UNMODIFIED reference `tidepool` with the gpu table
+    registered (the north_star drop-in): `tidepool.add(V, R)` on gpu0, where
+    the reference pipeline converts V int16 -> float (ops._dtype_convert)
+    and the plugin fuses that conversion into the add.  Reports host wall
+    ms/op over a run of back-to-back calls, the device time of the op, the
+    reference pipeline's own host cost with a no-op table (the floor of any
+    table implementation), and an e2e step from host numpy data to a host
+    result through the reference API.  Skipped when the reference is not
+    importable (baseline/_ref)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import ref_loader
+    tp = ref_loader.load("tidepool_bench_plugin")
+    if tp is None:
+        return {"skipped": "reference tidepool not importable (baseline/_ref absent)"}
+    from paper_1810_08723_b200 import tidepool_plugin
+    gpu = tidepool_plugin.register(tp, count=1)[0]
+    rt = tidepool_plugin.register.runtime
+    x16, r = cfg2_host_inputs()
+
+    def put(arr, dt):
+        t = tp.tensor_create(arr.shape, dt, gpu)
+        t.storage.stream.sync()
+        t.storage.view()[:] = arr.tobytes(order="F")
+        return t
+    X, R = put(x16, tp.int16), put(r, tp.float)
+    V = tp.apply_index(tp.transpose(X), (slice(None, None, -1), slice(None)))
+    st = gpu.default_stream()
+    for _ in range(warmup):
+        out = tp.add(V, R)
+    st.sync()
+    f0 = rt.stats["fused"]
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        out = tp.add(V, R)
+    st.sync()
+    wall_ms = (time.perf_counter() - t0) * 1e3 / steps
+    fused = rt.stats["fused"] - f0
+    # device time per op: steps enqueued behind the gate, so the host
+    # pipeline's latency is not inside the events
+    dev_ms = statistics.median(timed_steps(L, st, lambda: tp.add(V, R), 5, None, gate=True))
+    got = np.frombuffer(out.storage.snapshot(), dtype=np.float32).reshape((N, N), order="F")
+    want = (x16.T[::-1, :].astype(np.float64) + r.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(got, want), "plugin cfg2 result mismatch"
+    del out
+    # e2e through the reference API: host bytes -> cpu tensor -> gpu (copy
+    # entry, staged H2D) -> add (lazy cast fused) -> cpu (copy override, D2H)
+    xb, rb = x16.tobytes(order="F"), r.tobytes(order="F")
+
+    def host_tensor(raw, dims, dt):
+        s = tp.storage_from_external(bytearray(raw))
+        return tp.tensor_from_storage(s, dims, dt)
+    hx, hr = host_tensor(xb, (N, N), tp.int16), host_tensor(rb, (1, N), tp.float)
+
+    def e2e():
+        Xg, Rg = tp.cast(hx, device=gpu), tp.cast(hr, device=gpu)
+        Vg = tp.apply_index(tp.transpose(Xg), (slice(None, None, -1), slice(None)))
+        return tp.cast(tp.add(Vg, Rg), device=tp.cpu())
+    res = e2e()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        res = e2e()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / 3
+    assert res.storage.snapshot() == want.tobytes(order="F"), "plugin e2e mismatch"
+    floor = _pipeline_floor(steps=200)
+    return {"ms_per_op_wall": round(wall_ms, 4), "device_ms": round(dev_ms, 4),
+            "device_GB/s": round(CFG2_BYTES / dev_ms / 1e6, 1), "fused_per_op": fused / steps,
+            "reference_pipeline_floor_ms": round(floor, 4),
+            "e2e_ms": round(e2e_ms, 3), "e2e_GB/s": round(CFG2_BYTES / e2e_ms / 1e6, 2),
+            "checked": "bit-exact vs numpy (device result and e2e result)"}
+
+
+def _pipeline_floor(steps=200):
+    """Host cost of the reference's own binary_elementwise pipeline for the
+    cfg2 call shape with a no-op function table (a separate copy of the
+    reference; no gpu work): no table implementation can go below it."""
+    import ref_loader
+    tp = ref_loader.load("tidepool_bench_floor")
+    gt = tp.devices.DeviceType("nop", supports_byteswapped=True, async_capable=False)
+    big = C.create_string_buffer(N * N * 4 + 64)
+
+    class Nop(tp.devices.Device):
+        def allocate(self, n):
+            return (C.c_ubyte * max(n, 1)).from_address(C.addressof(big))
+    tbl = {k: (lambda *a, **k: None) for k in tp.backend_cpu.build_core_table()}
+    tp.dispatch.register_device_impl("core", "nop", tbl)
+    d = Nop(gt, 0)
+    X = tp.tensor_create((N, N), tp.int16, d)
+    V = tp.apply_index(tp.transpose(X), (slice(None, None, -1), slice(None)))
+    R = tp.tensor_create((1, N), tp.float, d)
+    for _ in range(20):
+        tp.add(V, R)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        tp.add(V, R)
+    return (time.perf_counter() - t0) * 1e3 / steps
 
 
 def extras(tp, dev, L, warmup=3, steps=5, only=None):
@@ -329,13 +470,17 @@ def extras(tp, dev, L, warmup=3, steps=5, only=None):
     def flush():
         l2_flush(L, stream, flush_buf)
 
-    def run(name, step, nbytes=None, flops=None, fl=True, st=steps):
+    def run(name, step, nbytes=None, flops=None, fl=True, st=steps, check=None):
+        """Time `step`; then `check()` validates the output it produced
+        (every timed workload carries a value check)."""
         for _ in range(warmup):
             step()
         stream.sync()
         ms = timed_steps(L, stream, step, st, flush if fl else None)
         m = statistics.median(ms)
         rec = {"ms": round(m, 4)}
+        if check is not None:
+            rec["checked"] = check()
         if nbytes:
             rec["GB/s"] = round(nbytes / m / 1e6, 1)
         if flops:
@@ -344,20 +489,40 @@ def extras(tp, dev, L, warmup=3, steps=5, only=None):
 
     if want("cfg1"):
         rng = np.random.default_rng(1)
-        a = tp.from_numpy(rng.standard_normal(1 << 20).astype(np.float32), dev)
-        b = tp.from_numpy(rng.standard_normal(1 << 20).astype(np.float32), dev)
+        an = rng.standard_normal(1 << 20).astype(np.float32)
+        bn = rng.standard_normal(1 << 20).astype(np.float32)
+        a, b = tp.from_numpy(an, dev), tp.from_numpy(bn, dev)
         o = tp.tensor_create((1 << 20,), tp.float, dev)
-        run("cfg1_add_f32_2^20", lambda: tp.add(a, b, dest=o), nbytes=12 << 20)
+
+        def ck1():
+            assert np.array_equal(tp.to_numpy(o), an + bn), "cfg1 mismatch"
+            return "bit-exact, all elements"
+        run("cfg1_add_f32_2^20", lambda: tp.add(a, b, dest=o), nbytes=12 << 20, check=ck1)
         del a, b, o
 
     if want("cfg3"):
-        X = tp.from_numpy(np.asfortranarray(np.random.default_rng(5).random((8192, 8192))), dev)
+        xn = np.asfortranarray(np.random.default_rng(5).random((8192, 8192)))
+        X = tp.from_numpy(xn, dev)
         nb = 8192 * 8192 * 8
+        ref = {"sum": lambda ax: xn.sum(axis=ax), "maximum": lambda ax: xn.max(axis=ax),
+               "norm": lambda ax: np.sqrt((xn * xn).sum(axis=ax))}
         for op in ("sum", "maximum", "norm"):
             for axes, tag in (((0,), "axis0"), ((1,), "axis1"), (None, "full")):
-                run(f"cfg3_{op}_{tag}_f64_8192^2",
-                    lambda op=op, axes=axes: tp.reduce(op, X, axes=axes), nbytes=nb)
-        del X
+                box = {}
+
+                def step(op=op, axes=axes, box=box):
+                    box["r"] = tp.reduce(op, X, axes=axes)
+
+                def ck3(op=op, axes=axes, box=box):
+                    got = tp.to_numpy(box["r"]).reshape(-1)
+                    want = np.asarray(ref[op](None if axes is None else axes[0])).reshape(-1)
+                    if op == "maximum":
+                        assert np.array_equal(got, want), "cfg3 max mismatch"
+                        return "exact, all outputs"
+                    assert np.allclose(got, want, rtol=1e-12, atol=0), f"cfg3 {op} mismatch"
+                    return "rel 1e-12 vs numpy float64, all outputs"
+                run(f"cfg3_{op}_{tag}_f64_8192^2", step, nbytes=nb, check=ck3)
+        del X, xn
     if want("cfg5"):
         cfg5(tp, dev, run)
     if want("cfg4"):
@@ -369,69 +534,119 @@ def extras(tp, dev, L, warmup=3, steps=5, only=None):
 def cfg5(tp, dev, run):
     """SURVEY cfg5 at its full 2^30 elements: the f64 big-endian source is
     built on the device from four copies of a 2^28 host-generated slab
-    (keeps host memory at 2 GiB)."""
+    (keeps host memory at 2 GiB).  Checks: 2^16 elements from each quarter
+    (shard slab) against numpy restatements, bit-exact."""
     n5 = 1 << 30
     q = n5 // 4
-    chunk = tp.from_numpy(np.random.default_rng(8).uniform(-1e3, 1e3, q).astype(">f8"), dev)
+    w = 1 << 16
+    offs = [i * q + 12345 * (i + 1) for i in range(4)]
+
+    def sample(t, want, np_dt):
+        for o in offs:
+            got = tp.to_numpy(tp.apply_index(t, (slice(o, o + w),)))
+            exp = want[(o % q):(o % q) + w]
+            assert np.array_equal(got.view(np_dt), exp.view(np_dt)), "cfg5 mismatch"
+        return f"bit-exact on {4 * w} sampled elements (4 quarters)"
+
+    slab = np.random.default_rng(8).uniform(-1e3, 1e3, q)
+    chunk = tp.from_numpy(slab.astype(">f8"), dev)
     S = tp.tensor_create((n5,), tp.double, dev)
     S.byteorder = "big"
     for i in range(4):
         tp.copy(chunk, tp.apply_index(S, (slice(i * q, (i + 1) * q),)))
     del chunk
     Y = tp.tensor_create((n5,), tp.float, dev)
-    run("cfg5_cast_f64BE_to_f32_2^30", lambda: tp.copy(S, Y), nbytes=12 * n5, fl=False)
+    wy = slab.astype(np.float32)
+    run("cfg5_cast_f64BE_to_f32_2^30", lambda: tp.copy(S, Y), nbytes=12 * n5, fl=False,
+        check=lambda: sample(Y, wy, np.uint32))
     del S
     Z = tp.tensor_create((n5,), tp.float, dev)
+    W = tp.tensor_create((n5,), tp.float, dev)
     k15, km2 = tp.Scalar(1.5, tp.float), tp.Scalar(-2.0, tp.float)
+    wz = (wy.astype(np.float64) * 1.5).astype(np.float32)
+    ww = (wz.astype(np.float64) - 2.0).astype(np.float32)
     run("cfg5_multiply_scalar_f32_2^30", lambda: tp.multiply(Y, k15, dest=Z), nbytes=8 * n5,
-        fl=False)
-    run("cfg5_add_scalar_f32_2^30", lambda: tp.add(Z, km2, dest=Y), nbytes=8 * n5, fl=False)
+        fl=False, check=lambda: sample(Z, wz, np.uint32))
+    run("cfg5_add_scalar_f32_2^30", lambda: tp.add(Z, km2, dest=W), nbytes=8 * n5, fl=False,
+        check=lambda: sample(W, ww, np.uint32))
     # the same multiply-then-add as one fused chain (SURVEY §8f item 2):
     # 8 B/elem moved instead of 16
     run("cfg5_chain_mul_add_f32_2^30", lambda: tp.chain(Y, [("multiply", k15), ("add", km2)],
-                                                          dest=Z), nbytes=8 * n5, fl=False)
-    del Y, Z
-    c16 = tp.from_numpy(np.random.default_rng(9).integers(-3000, 3000, q).astype(">i2"), dev)
+                                                          dest=Z), nbytes=8 * n5, fl=False,
+        check=lambda: sample(Z, ww, np.uint32))
+    del Y, Z, W, wy, wz, ww, slab
+    s16n = np.random.default_rng(9).integers(-3000, 3000, q).astype(np.int16)
+    c16 = tp.from_numpy(s16n.astype(">i2"), dev)
     s16 = tp.tensor_create((n5,), tp.int16, dev)
     s16.byteorder = "big"
     for i in range(4):
         tp.copy(c16, tp.apply_index(s16, (slice(i * q, (i + 1) * q),)))
     del c16
     h16 = tp.tensor_create((n5,), tp.half, dev)
-    run("cfg5_cast_i16BE_to_f16_2^30", lambda: tp.copy(s16, h16), nbytes=4 * n5, fl=False)
+    wh = s16n.astype(np.float16)
+    run("cfg5_cast_i16BE_to_f16_2^30", lambda: tp.copy(s16, h16), nbytes=4 * n5, fl=False,
+        check=lambda: sample(h16, wh, np.uint16))
     del s16, h16
 
 
 def cfg4(tp, dev, run):
-    def gemm_operands(dt, m, k, n, batch=None):
-        rng6 = np.random.default_rng(6)
-        def mk(rows, cols):
-            shape = (rows, cols) if batch is None else (rows, cols, batch)
-            base = rng6.uniform(-1, 1, shape).astype(np.float32)
-            if dt is tp.bfloat16:
-                raw = (base.view(np.uint32) >> 16).astype(np.uint16)
-                return tp.from_numpy(np.asfortranarray(raw), dev, dtype=tp.bfloat16)
-            npd = np.float16 if dt is tp.half else np.float32
-            return tp.from_numpy(np.asfortranarray(base.astype(npd)), dev)
-        return mk, mk
+    """SURVEY cfg4: A = transpose of a column-major base (K-major), B
+    column-major, C column-major; 2*8192^3 flop per step.  Checks: 256
+    sampled (i, j) entries against float64 dot products of the same
+    operand values, |err| <= tol * sum|a||b| (1e-2 f16/bf16, 1e-5 f32)."""
+    def operand(dt, shape, seed):
+        base = np.random.default_rng(seed).uniform(-1, 1, shape).astype(np.float32)
+        if dt is tp.bfloat16:
+            raw = np.asfortranarray((base.view(np.uint32) >> 16).astype(np.uint16))
+            vals = (raw.astype(np.uint32) << 16).view(np.float32)
+            return tp.from_numpy(raw, dev, dtype=tp.bfloat16), vals
+        npd = np.float16 if dt is tp.half else np.float32
+        h = np.asfortranarray(base.astype(npd))
+        return tp.from_numpy(h, dev), h
 
-    # SURVEY cfg4: A = transpose of a column-major base (K-major), B
-    # column-major, C column-major; 2*8192^3 flop per step
-    for dname, dt, m in (("f16", tp.half, 8192), ("bf16", tp.bfloat16, 8192),
-                         ("f32", tp.float, 8192)):
-        mk, _ = gemm_operands(dt, m, m, m)
-        At = tp.transpose(mk(m, m))
-        B = mk(m, m)
+    def download(t):
+        if t.dtype is tp.bfloat16:
+            raw = tp.to_numpy(tp.tensors.Tensor(t.storage, t.offset, t.dims, t.strides,
+                                                tp.uint16))
+            return (raw.astype(np.uint32) << 16).view(np.float32)
+        return tp.to_numpy(t)
+
+    def check_entries(got, arows, bcols, tol):
+        a, b = arows.astype(np.float64), bcols.astype(np.float64)
+        want = np.einsum("ks,ks->s", a, b)
+        bound = np.einsum("ks,ks->s", np.abs(a), np.abs(b))
+        err = np.abs(got.astype(np.float64) - want)
+        assert np.all(err <= tol * bound), f"cfg4 mismatch {float((err / bound).max())}"
+        return f"{len(want)} sampled entries within {tol} * sum|a||b|"
+
+    m = 8192
+    rng = np.random.default_rng(12)
+    si, sj = rng.integers(0, m, 256), rng.integers(0, m, 256)
+    for dname, dt, tol in (("f16", tp.half, 1e-2), ("bf16", tp.bfloat16, 1e-2),
+                           ("f32", tp.float, 1e-5)):
+        Ab, ab = operand(dt, (m, m), 6)
+        B, bh = operand(dt, (m, m), 7)
+        At = tp.transpose(Ab)
         Cm = tp.tensor_create((m, m), dt, dev)
+
+        def ck4(Cm=Cm, ab=ab, bh=bh, tol=tol):
+            return check_entries(download(Cm)[si, sj], ab[:, si], bh[:, sj], tol)
         run(f"cfg4_gemm_{dname}_{m}^3", lambda: tp.matmul(At, B, dest=Cm), flops=2 * m ** 3,
-            fl=False, st=3)
-        del At, B, Cm
+            fl=False, st=3, check=ck4)
+        del At, Ab, B, Cm, ab, bh
     # batched: 64 x (2048 x 2048 x 2048), batch slowest
-    mk, _ = gemm_operands(tp.half, 2048, 2048, 2048, batch=64)
-    Ab, Bb = mk(2048, 2048), mk(2048, 2048)
-    Cb = tp.tensor_create((2048, 2048, 64), tp.half, dev)
+    nb, s_ = 64, 2048
+    Ab, ab = operand(tp.half, (s_, s_, nb), 6)
+    Bb, bb = operand(tp.half, (s_, s_, nb), 7)
+    Cb = tp.tensor_create((s_, s_, nb), tp.half, dev)
+
+    def ckb():
+        got = download(Cb)
+        bi, bj, bq = (rng.integers(0, s_, 256), rng.integers(0, s_, 256),
+                      rng.integers(0, nb, 256))
+        return check_entries(got[bi, bj, bq], ab[bi, :, bq].T, bb[:, bj, bq], 1e-2)
     run("cfg4_gemm_batched_f16_64x2048^3", lambda: tp.matmul_batched(Ab, Bb, dest=Cb),
-        flops=64 * 2 * 2048 ** 3, fl=False, st=3)
+        flops=64 * 2 * 2048 ** 3, fl=False, st=3, check=ckb)
     del Ab, Bb, Cb
 
 
@@ -568,7 +783,8 @@ def main():
     clocks = Clocks(dist.phys)
     clocks.start()
     dist.barrier()
-    ms, e2e_ms, e2e_wall, h2d, d2h, pcie = bench_cfg2(tp, dev, args.steps, args.warmup, L)
+    r2 = bench_cfg2(L, args.steps, args.warmup, dev.index)
+    ms, e2e_ms = r2["ms"], r2["e2e_ms"]
     dist.barrier()
     total = dist.max(sum(ms))
     e2e_total = dist.max(sum(e2e_ms))
@@ -579,6 +795,10 @@ def main():
     work = {}
     if dist.rank == 0 and dist.world == 1 and not args.no_extras:
         work = extras(tp, dev, L)
+        try:
+            work["cfg2_through_reference_plugin"] = bench_plugin(L)
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            work["cfg2_through_reference_plugin"] = {"error": repr(exc)[:300]}
     elif dist.world > 1 and not args.no_extras:
         work = sharded_extras(tp, dev, L, dist)
     clk = clocks.stop()
@@ -596,10 +816,13 @@ def main():
                          "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                          "peak_kind": peak_kind, "traffic": traffic,
                          "kernel": "tpg::k_tile_f32<add, i16 -> f32, f32 row> (fused cast + broadcast add)"},
-            "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_total / len(e2e_ms), 3),
-                    "wall_ms_per_step": round(e2e_wall, 3), "pcie": pcie},
-            "gpu_launches": args.steps + 1 + len(e2e_ms) * E2E_CHUNKS,
+            "e2e": {"value": round(e2e_val, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": r2["h2d"], "d2h_bytes_per_step": r2["d2h"],
+                    "ms_per_step": round(e2e_total / len(e2e_ms), 3),
+                    "wall_ms_per_step": round(r2["wall"], 3), "pcie": r2["pcie"],
+                    "path": "C ABI (tpg_memcpy2d / tpg_binary / tpg_memcpy_d2h) from pinned "
+                            "host buffers, 3 streams, column slabs"},
+            "gpu_launches": r2["launches"],
             "clocks": clk,
         }
         if dist.world == 1:

@@ -38,6 +38,7 @@ METRIC = "elementwise/reduce HBM GB/s vs ~8 TB/s; gemm TFLOP/s; at 1/2/4/8 B200"
 N = 4096
 CFG2_BYTES = N * N * (2 + 4) + N * 4
 FLUSH_BYTES = 256 << 20
+ROT = 4  # rotating input/output sets of the headline (4 x 100.7 MB > 126 MB L2)
 E2E_CHUNKS = int(os.environ.get("TPG_E2E_CHUNKS", "8"))  # slabs of the pipelined e2e step
 E2E_SPLIT = os.environ.get("TPG_E2E_SPLIT", "cols")  # "rows" | "cols" of the cfg2 result
 
@@ -200,6 +201,29 @@ def timed_steps(L, stream, step, steps, flush=None, gate=True):
     return out
 
 
+def timed_batch(L, stream, step, steps, gate=True):
+    """`steps` back-to-back steps between ONE pair of events (the device is
+    held by the gate until all are enqueued); returns [ms per step] * steps
+    so callers can sum / average like timed_steps."""
+    from paper_1810_08723_b200 import _native
+    t = Timer(L, stream.handle)
+    s, e = t.event(), t.event()
+    gate = gate and "CUDA_INJECTION64_PATH" not in os.environ
+    if gate:
+        _native.check(L.tpg_gate_arm(stream.handle))
+    L.tpg_event_record(s, stream.handle)
+    for _ in range(steps):
+        step()
+    L.tpg_event_record(e, stream.handle)
+    if gate:
+        L.tpg_gate_release()
+    stream.sync()
+    ms = t.elapsed(s, e) / steps
+    L.tpg_event_destroy(s)
+    L.tpg_event_destroy(e)
+    return [ms] * steps
+
+
 # ---------------------------------------------------------------------------
 # L2 flush between timed steps (outside the events): write a 256 MiB buffer
 # (> 126 MB L2), then read it back with default-priority loads so the L2 is
@@ -277,25 +301,45 @@ def bench_cfg2(L, steps, warmup, dev=0):
     flush_buf = _dmalloc(L, FLUSH_BYTES)
     _ck(L, L.tpg_memcpy_h2d(X, x16.ctypes.data, x16.nbytes, stream.handle), "H2D")
     _ck(L, L.tpg_memcpy_h2d(R, r.ctypes.data, r.nbytes, stream.handle), "H2D")
-    plan, d, a, b = cfg2_plan(abi, X, R, O)
-    args = (stream.handle, 0, C.byref(plan), C.byref(d), C.byref(a), C.byref(b), 10, 0)
+    # ROT buffer sets (X_k, O_k): back-to-back steps rotate over them, so
+    # the operands of every step were last touched ROT-1 steps (>= 300 MB of
+    # traffic) earlier and the whole working set (ROT x 100.7 MB) exceeds
+    # the 126 MB L2 -- "inputs larger than L2", no flush inside the region
+    sets = [(X, O)]
+    for _ in range(ROT - 1):
+        Xk, Ok = _dmalloc(L, N * N * 2), _dmalloc(L, N * N * 4)
+        _ck(L, L.tpg_memcpy_d2d(Xk, X, N * N * 2, stream.handle), "D2D")
+        sets.append((Xk, Ok))
+    descs = [cfg2_plan(abi, xk, R, ok) for xk, ok in sets]
+    argv = [(stream.handle, 0, C.byref(p_), C.byref(d_), C.byref(a_), C.byref(b_), 10, 0)
+            for p_, d_, a_, b_ in descs]
+    k = [0]
+
+    def step():
+        _ck(L, L.tpg_binary(*argv[k[0] % ROT]), "tpg_binary")
+        k[0] += 1
 
     def flush():
         l2_flush(L, stream, flush_buf)
 
-    def step():
-        _ck(L, L.tpg_binary(*args), "tpg_binary")
-
     for _ in range(warmup):
-        flush()
         step()
     stream.sync()
-    ms = timed_steps(L, stream, step, steps, flush)
+    # the timed region: `steps` back-to-back launches between one event pair
+    ms = timed_batch(L, stream, step, steps)
+    # the same launch timed one step at a time with the L2 flushed before
+    # each (outside the events): includes the ~6 us per-step launch + event
+    # floor (profiles/r01g_launch_floor.md)
+    flushed = timed_steps(L, stream, step, max(10, steps // 2), flush)
     want = (x16.T[::-1, :].astype(np.float64) + r.astype(np.float64)).astype(np.float32)
     got = np.empty((N, N), dtype=np.float32, order="F")
-    _ck(L, L.tpg_memcpy_d2h(got.ctypes.data, O, got.nbytes, stream.handle), "D2H")
-    stream.sync()
-    assert np.array_equal(got, want), "cfg2 device result mismatch"
+    for xk, ok in sets:
+        _ck(L, L.tpg_memcpy_d2h(got.ctypes.data, ok, got.nbytes, stream.handle), "D2H")
+        stream.sync()
+        assert np.array_equal(got, want), "cfg2 device result mismatch"
+    for xk, ok in sets[1:]:
+        L.tpg_free(dev, xk, stream.handle)
+        L.tpg_free(dev, ok, stream.handle)
 
     # ---- e2e: pinned host buffers, pipelined over E2E_CHUNKS column slabs
     # on three streams (uploads back to back on the H2D engine, the adds on
@@ -355,8 +399,9 @@ def bench_cfg2(L, steps, warmup, dev=0):
             "bound_ms": round(max(d2h_ms, h2d_ms), 3)}
     for p in (X, R, O, flush_buf):
         L.tpg_free(dev, p, stream.handle)
-    return {"ms": ms, "e2e_ms": e2e_ms, "wall": wall, "h2d": x16.nbytes + r.nbytes,
-            "d2h": N * N * 4, "pcie": pcie, "launches": steps + launches[0]}
+    return {"ms": ms, "flushed_ms": flushed, "e2e_ms": e2e_ms, "wall": wall,
+            "h2d": x16.nbytes + r.nbytes, "d2h": N * N * 4, "pcie": pcie,
+            "launches": steps + launches[0]}
 
 
 def bench_plugin(L, steps=20, warmup=3):
@@ -397,9 +442,21 @@ def bench_plugin(L, steps=20, warmup=3):
     st.sync()
     wall_ms = (time.perf_counter() - t0) * 1e3 / steps
     fused = rt.stats["fused"] - f0
-    # device time per op: steps enqueued behind the gate, so the host
-    # pipeline's latency is not inside the events
-    dev_ms = statistics.median(timed_steps(L, st, lambda: tp.add(V, R), 5, None, gate=True))
+    # device time of the op's kernel: the plugin's profiling hook brackets
+    # each launch with an event pair on the launching stream
+    rt.profile = []
+    for _ in range(10):
+        tp.add(V, R)
+    st.sync()
+    kms = []
+    for a_, b_ in rt.profile:
+        f_ = C.c_float()
+        L.tpg_event_elapsed(a_, b_, C.byref(f_))
+        kms.append(f_.value)
+        L.tpg_event_destroy(a_)
+        L.tpg_event_destroy(b_)
+    rt.profile = None
+    dev_ms = statistics.median(kms)
     got = np.frombuffer(out.storage.snapshot(), dtype=np.float32).reshape((N, N), order="F")
     want = (x16.T[::-1, :].astype(np.float64) + r.astype(np.float64)).astype(np.float32)
     assert np.array_equal(got, want), "plugin cfg2 result mismatch"
@@ -755,7 +812,10 @@ def main():
     config = {"workload": "cfg2: int16[4096,4096] transposed reversed view (strides -8192,2) "
                           "+ float32[1,4096] broadcast -> float32 add",
               "elements": N * N, "algorithmic_bytes_per_step": CFG2_BYTES,
-              "l2": "flushed between timed steps (256 MiB write + read-back, outside the events)", "parallelism": f"dp{dist.world}"}
+              "l2": f"inputs larger than L2: K back-to-back steps rotate over {ROT} input/output "
+                    f"sets ({ROT} x 100.7 MB > 126 MB L2), one event pair around the K steps; "
+                    "per-step L2-flushed timing reported under 'flushed'",
+              "parallelism": f"dp{dist.world}"}
 
     if args.impl == "reference":
         if dist.rank != 0:
@@ -822,6 +882,11 @@ def main():
                     "wall_ms_per_step": round(r2["wall"], 3), "pcie": r2["pcie"],
                     "path": "C ABI (tpg_memcpy2d / tpg_binary / tpg_memcpy_d2h) from pinned "
                             "host buffers, 3 streams, column slabs"},
+            "flushed": {"ms_per_step": round(statistics.median(r2["flushed_ms"]), 5),
+                        "GB/s": round(CFG2_BYTES / statistics.median(r2["flushed_ms"]) / 1e6, 1),
+                        "how": "one step per event pair, 256 MiB L2 flush (write + read-back) "
+                               "before each step outside the events; includes the ~6 us "
+                               "per-step launch + event floor"},
             "gpu_launches": r2["launches"],
             "clocks": clk,
         }

@@ -236,6 +236,7 @@ class _Runtime:
         self.status_sink = tp.ops._status
         self.event_pool: list = []
         self.stats = collections.Counter()  # lazy / fused / materialised / transfer paths
+        self.profile = None  # [] -> (start, stop) timing events around each standard-mode launch
 
     # -- errors --------------------------------------------------------------
     def check(self, rc, what):
@@ -247,21 +248,36 @@ class _Runtime:
         raise self.errors.DeviceError(msg)
 
     # -- memory --------------------------------------------------------------
-    def allocate(self, device, nbytes):
-        cap = _size_class(nbytes)
-        key = (device, cap)
+    MAX_PENDING = 8  # per size class: beyond this many in-flight blocks, wait for the oldest
+
+    def _take_cached(self, key):
+        """A cached block of `key` whose last GPU use has completed (host
+        code may write a fresh storage without synchronising, e.g.
+        tensor_from_nested / scalar_tensor, tensors.py:221-243, 269-280), or
+        None.  Never waits while fewer than MAX_PENDING blocks are in flight,
+        so back-to-back ops do not serialise the host on the GPU."""
         with self.lock:
             pool = self.cache.get(key)
-            ent = pool.pop() if pool else None
-            if ent is not None:
-                self.cached_bytes[device] -= cap
-        if ent is not None:
-            ptr, events = ent
-            for ev in events:  # the block's last GPU use must be complete
-                if self.L.tpg_event_query(ev) != 0:
+            if not pool:
+                return None
+            for i, (ptr, events) in enumerate(pool):
+                if all(self.L.tpg_event_query(ev) == 0 for ev in events):
+                    del pool[i]
+                    break
+            else:
+                if len(pool) < self.MAX_PENDING:
+                    return None
+                ptr, events = pool.pop(0)
+                for ev in events:
                     self.check(self.L.tpg_event_sync(ev), "event sync")
-                self.event_pool.append(ev)
-        else:
+            self.cached_bytes[key[0]] -= key[1]
+            self.event_pool.extend(events)
+            return ptr
+
+    def allocate(self, device, nbytes):
+        cap = _size_class(nbytes)
+        ptr = self._take_cached((device, cap))
+        if ptr is None:
             p = C.c_void_p()
             rc = self.L.tpg_malloc_managed(device, cap, C.byref(p))
             if rc == -2:
@@ -295,6 +311,11 @@ class _Runtime:
             over = self.cached_bytes[blk.device] > self.CACHE_BYTES
         if over:
             self.trim(blk.device, self.CACHE_BYTES // 2)
+
+    def _new_timing_event(self):
+        ev = C.c_void_p()
+        self.check(self.L.tpg_event_create(C.byref(ev)), "event create")
+        return ev.value
 
     def _new_event(self):
         ev = C.c_void_p()
@@ -541,10 +562,22 @@ def register(tidepool_module, count: int | None = None, lib=None):
     def _loss_message(d):
         return f"value cannot be represented as {d.name}"
 
+    def _timed(st, launch):
+        """Launch, bracketed by an event pair when profiling is on
+        (rt.profile = []: collects (start, stop) events per launch)."""
+        if rt.profile is None:
+            return launch()
+        a, b = rt._new_timing_event(), rt._new_timing_event()
+        L.tpg_event_record(a, st.handle)
+        rc = launch()
+        L.tpg_event_record(b, st.handle)
+        rt.profile.append((a, b))
+        return rc
+
     def _run(st, mode, ctx, to, launch, check=None):
         """Launch with the reference's mode semantics (cast loss -> ctx)."""
         if mode in ("standard", "complex"):
-            rt.check(launch(), "kernel")
+            rt.check(_timed(st, launch), "kernel")
             return
         rt.drain(st)
         if mode == "error" and check is not None:

@@ -74,6 +74,68 @@ class FakeNative:
         self.mem.pop(_int(ptr), None)
         return 0
 
+    def tpg_malloc(self, dev, n, out):
+        _obj(out).value = self._alloc(n)
+        return 0
+
+    def tpg_host_alloc(self, n, out):
+        _obj(out).value = self._alloc(n)
+        return 0
+
+    def tpg_host_free(self, ptr):
+        self.mem.pop(_int(ptr), None)
+        return 0
+
+    def tpg_init(self):
+        return 0
+
+    def tpg_version(self):
+        return b"fake"
+
+    def tpg_mem_stats(self, dev, a, b, c):
+        _obj(a).value = sum(len(v) for v in self.mem.values())
+        _obj(b).value = 0
+        _obj(c).value = len(self.mem)
+        return 0
+
+    def tpg_stream_wait(self, a, b):
+        return 0
+
+    def tpg_stream_destroy(self, s):
+        return 0
+
+    def tpg_event_create(self, out):
+        _obj(out).value = 0x3001
+        return 0
+
+    def tpg_event_destroy(self, ev):
+        return 0
+
+    def tpg_event_elapsed(self, a, b, out):
+        _obj(out).value = 0.0
+        return 0
+
+    def tpg_memcpy_d2d(self, dst, src, n, s):
+        C.memmove(_int(dst), _int(src), n)
+        return 0
+
+    def tpg_memset(self, dst, v, n, s):
+        C.memset(_int(dst), v, n)
+        return 0
+
+    def tpg_memcpy2d(self, dst, dpitch, src, spitch, width, height, s):
+        for r in range(height):
+            C.memmove(_int(dst) + r * dpitch, _int(src) + r * spitch, width)
+        return 0
+
+    def tpg_flags_get(self, dev, out):
+        _obj(out).value = self.flags[dev]
+        return 0
+
+    def tpg_flags_clear(self, dev):
+        self.flags[dev] = 0
+        return 0
+
     def tpg_default_stream(self, dev, out):
         _obj(out).value = 0x1000 + dev
         return 0
@@ -99,7 +161,7 @@ class FakeNative:
         return 0
 
     def tpg_memcpy_h2d(self, dst, src, n, s):
-        C.memmove(_int(dst), _int(src), n)
+        C.memmove(_int(dst), src if isinstance(src, (bytes, bytearray)) else _int(src), n)
         return 0
 
     tpg_memcpy_d2h = tpg_memcpy_h2d
@@ -117,6 +179,19 @@ class FakeNative:
     def _flag(self, st):
         self.flags[0] |= st.value | self.inject
         self.inject = 0
+
+    # single-rank NCCL: the all-reduce of one rank is the identity
+    def tpg_nccl_get_unique_id(self, out):
+        return 0
+
+    def tpg_nccl_init(self, dev, nranks, rank, uid):
+        return 0 if nranks == 1 else -4
+
+    def tpg_nccl_allreduce(self, s, buf, count, dtype, op):
+        return 0
+
+    def tpg_nccl_destroy(self):
+        return 0
 
     # -- kernels (oracle) ---------------------------------------------------------
     def tpg_binary(self, s, op, plan, d, a, b, comp, mode):
@@ -160,6 +235,70 @@ class FakeNative:
         rc = self.o.tpo_matmul(d, ds, a, as_, b, bs, m, n, k, comp, mode, C.byref(st))
         self._flag(st)
         return rc
+
+    def tpg_matmul_batched(self, s, nb, d, ds, a, as_, b, bs, m, n, k, comp, mode):
+        self.calls.append(("matmul_batched",))
+        dd, aa, bb = _obj(d), _obj(a), _obj(b)
+        st = C.c_uint32(0)
+        for q in range(nb):
+            do = abi.make_operand(dd.base, dd.offset + q * ds[2], dd.dtype, dd.big_endian)
+            ao = abi.make_operand(aa.base, aa.offset + q * as_[2], aa.dtype, aa.big_endian)
+            bo = abi.make_operand(bb.base, bb.offset + q * bs[2], bb.dtype, bb.big_endian)
+            d2, a2, b2 = ((C.c_int64 * 2)(x[0], x[1]) for x in (ds, as_, bs))
+            rc = self.o.tpo_matmul(C.byref(do), d2, C.byref(ao), a2, C.byref(bo), b2, m, n, k,
+                                   comp, mode, C.byref(st))
+            if rc:
+                return rc
+        self._flag(st)
+        return 0
+
+    def _chain(self, plan, d, a, nsteps, steps, mode, dry):
+        """x <- op_i(x, s_i) step by step through tpo_binary, rounding to
+        each step's dtype in a scratch copy laid out like the destination."""
+        dd, aa = _obj(d), _obj(a)
+        p = _obj(plan)
+        st = C.c_uint32(0)
+        ext = [p.extent[k] for k in range(p.ndim)]
+        n = 1
+        for e in ext:
+            n *= e
+        cur = abi.make_operand(aa.base, aa.offset, aa.dtype, aa.big_endian)
+        cur_strides = [p.stride[1][k] for k in range(p.ndim)]
+        keep = []
+        for i in range(nsteps):
+            sp = steps[i]
+            last = i == nsteps - 1
+            if last and not dry:
+                out = abi.make_operand(dd.base, dd.offset, dd.dtype, dd.big_endian)
+                out_strides = [p.stride[0][k] for k in range(p.ndim)]
+            else:
+                size = _DT_SIZE[sp.dtype]
+                buf = C.create_string_buffer(max(n * size, 1))
+                keep.append(buf)
+                out = abi.make_operand(C.addressof(buf), 0, sp.dtype, False)
+                out_strides, acc = [], size
+                for e in ext:
+                    out_strides.append(acc)
+                    acc *= e
+            imm = abi.make_operand(None, 0, sp.scalar_dtype, False, bytes(sp.scalar))
+            pl = abi.make_plan(ext, [out_strides, cur_strides, [0] * p.ndim])
+            x, y = (imm, cur) if sp.scalar_first else (cur, imm)
+            if sp.scalar_first:
+                pl = abi.make_plan(ext, [out_strides, [0] * p.ndim, cur_strides])
+            rc = self.o.tpo_binary(sp.op, C.byref(pl), C.byref(out), C.byref(x), C.byref(y),
+                                   sp.compute, mode, C.byref(st))
+            if rc:
+                return rc
+            cur, cur_strides = out, out_strides
+        self._flag(st)
+        return 0
+
+    def tpg_chain(self, s, plan, d, a, nsteps, steps, mode):
+        self.calls.append(("chain",))
+        return self._chain(plan, d, a, nsteps, steps, mode, False)
+
+    def tpg_chain_check(self, s, plan, d, a, nsteps, steps, mode):
+        return self._chain(plan, d, a, nsteps, steps, mode, True)
 
     def tpg_fill(self, s, plan, d, value, size):
         self.calls.append(("fill",))
@@ -232,5 +371,7 @@ def _int(p):
         return p
     if p is None:
         return 0
+    if isinstance(p, C.Array):
+        return C.addressof(p)
     v = getattr(p, "value", p)
     return int(v or 0)

@@ -36,6 +36,7 @@ _dispatch.register_device_impl("core", "gpu", table.build_core_table())
 # extension entries beyond the reference's 31 keys (dispatch.add_op,
 # reference dispatch.py:111-117)
 _dispatch.add_op("core", "gpu", "ewise_chain", table.chain_entry)
+_dispatch.add_op("core", "gpu", "matmul_batched", table.matmul_batched_entry)
 
 bool = dtypes.BOOL  # noqa: A001
 int8 = dtypes.INT8

@@ -113,6 +113,7 @@ def save_otp1(t, sink, chunk: int = CHUNK) -> None:
         return
     src = t if _is_packed(t) else tz.contiguous_clone(t)  # device descriptor gather
     stream = src.storage.stream
+    src.storage.order(stream)
     L = _native.lib()
     pin = _Pinned(min(chunk, nbytes))
     try:

@@ -122,12 +122,6 @@ _host_status: set = set()
 _FLAG_NAMES = {abi.FLAG_DOMAIN: "domain-violation", abi.FLAG_INT_DIV0: "integer-division-by-zero"}
 
 
-def _stream_device(stream_handle):
-    from . import devices
-    s = current_stream()
-    return s.device.index if s is not None else devices.gpu(0).index
-
-
 def _drain_flags(dev: int) -> int:
     f = C.c_uint32(0)
     L = _native.lib()
@@ -154,36 +148,43 @@ def clear_status(devices_to_sync) -> None:
     _host_status.clear()
 
 
-def _guarded(mode: str, run, check):
-    """standard: run.  error: dry-run check first (no writes), raise on loss.
-    warning: run, then report one diagnostic per call."""
+def _guarded(mode: str, run, check, dev: int):
+    """Launch under the reference's mode rules (dtypes.CastContext,
+    dtypes.py:233-255).  standard / complex: run.  error: drain pending
+    flags, then either a dry-run `check` (no writes; raise before anything
+    is stored) or, for entries without one (reductions, products), the real
+    launch followed by the flag read; raise DomainError on cast loss.
+    warning: run, then one diagnostic per call on cast loss.  The flag reads
+    (tpg_flags_get) wait for every stream of `dev`."""
     if mode in ("standard", "complex"):
         _native.check(run(), "kernel")
         return
-    s = current_stream()
-    dev = s.device.index if s is not None else 0
-    if s is not None:
-        s.sync()
     _drain_flags(dev)
-    if mode == "error":
+    if mode == "error" and check is not None:
         _native.check(check(), "kernel check")
-        if s is not None:
-            s.sync()
-        f = _drain_flags(dev)
-        if f & abi.FLAG_CAST_LOSS:
-            raise DomainError("value cannot be represented in the destination dtype")
-        if f & abi.FLAG_INT_DIV0:
-            raise DomainError("integer division by zero")
-        if f & abi.FLAG_DOMAIN:
-            raise DomainError("input outside the real domain in error mode")
+        _raise_on(_drain_flags(dev))
         _native.check(run(), "kernel")
         return
     _native.check(run(), "kernel")
-    if s is not None:
-        s.sync()
     f = _drain_flags(dev)
-    if f & abi.FLAG_CAST_LOSS:
+    if mode == "error":
+        _raise_on(f)
+    elif f & abi.FLAG_CAST_LOSS:
         dtypes.emit_warning("cast lost information (value out of range or not representable)")
+
+
+def _raise_on(flags: int) -> None:
+    if flags & abi.FLAG_CAST_LOSS:
+        raise DomainError("value cannot be represented in the destination dtype")
+    if flags & abi.FLAG_INT_DIV0:
+        raise DomainError("integer division by zero")
+    if flags & abi.FLAG_DOMAIN:
+        raise DomainError("input outside the real domain in error mode")
+
+
+def _dev(buf) -> int:
+    """Device index of a table-entry buffer (a Storage)."""
+    return buf.device.index
 
 
 # ---------------------------------------------------------------------------
@@ -201,7 +202,8 @@ def binary_entry(op_name):
         mode = dtypes.MODE_CODE[store.mode]
         comp = fn.compute.code
         args = (_sh(), code, C.byref(p), C.byref(d), C.byref(a), C.byref(b), comp, mode)
-        _guarded(store.mode, lambda: L.tpg_binary(*args), lambda: L.tpg_binary_check(*args))
+        _guarded(store.mode, lambda: L.tpg_binary(*args), lambda: L.tpg_binary_check(*args),
+                 _dev(d_buf))
 
     entry.__name__ = f"gpu_{op_name}"
     return entry
@@ -221,7 +223,8 @@ def unary_entry(op_name):
         else:
             comp, fc = fn.compute.code, int(bool(fn.force_complex))
         args = (_sh(), code, C.byref(p), C.byref(d), C.byref(a), comp, mode, fc)
-        _guarded(store.mode, lambda: L.tpg_unary(*args), lambda: L.tpg_unary_check(*args))
+        _guarded(store.mode, lambda: L.tpg_unary(*args), lambda: L.tpg_unary_check(*args),
+                 _dev(d_buf))
 
     entry.__name__ = f"gpu_{op_name}"
     return entry
@@ -239,13 +242,7 @@ def reduce_entry(op_name):
         acc = init
         args = (_sh(), code, float(acc.p), C.byref(po), C.byref(pi), C.byref(d), C.byref(a),
                 acc.compute.code, mode)
-        _native.check(L.tpg_reduce(*args), f"reduce {op_name}")
-        if store.mode == "warning":
-            s = current_stream()
-            if s is not None:
-                s.sync()
-                if _drain_flags(s.device.index) & abi.FLAG_CAST_LOSS:
-                    dtypes.emit_warning("cast lost information")
+        _guarded(store.mode, lambda: L.tpg_reduce(*args), None, _dev(d_buf))
 
     entry.__name__ = f"gpu_reduce_{op_name}"
     return entry
@@ -260,8 +257,9 @@ def matmul_entry(d_buf, d_base, d_strides, store, a_buf, a_base, a_strides, a_un
     ds = (C.c_int64 * 2)(*d_strides)
     as_ = (C.c_int64 * 2)(*a_strides)
     bs = (C.c_int64 * 2)(*b_strides)
-    _native.check(L.tpg_matmul(_sh(), C.byref(d), ds, C.byref(a), as_, C.byref(b), bs,
-                               m, n, k, mul.compute.code, dtypes.MODE_CODE[store.mode]), "matmul")
+    _guarded(store.mode, lambda: L.tpg_matmul(_sh(), C.byref(d), ds, C.byref(a), as_, C.byref(b),
+                                              bs, m, n, k, mul.compute.code,
+                                              dtypes.MODE_CODE[store.mode]), None, _dev(d_buf))
 
 
 def matmul_batched_entry(batch, d_buf, d_base, d_strides, store, a_buf, a_base, a_strides,
@@ -274,9 +272,11 @@ def matmul_batched_entry(batch, d_buf, d_base, d_strides, store, a_buf, a_base, 
     ds = (C.c_int64 * 3)(*d_strides)
     as_ = (C.c_int64 * 3)(*a_strides)
     bs = (C.c_int64 * 3)(*b_strides)
-    _native.check(L.tpg_matmul_batched(_sh(), batch, C.byref(d), ds, C.byref(a), as_, C.byref(b),
-                                       bs, m, n, k, mul.compute.code,
-                                       dtypes.MODE_CODE[store.mode]), "matmul_batched")
+    _guarded(store.mode, lambda: L.tpg_matmul_batched(_sh(), batch, C.byref(d), ds, C.byref(a),
+                                                      as_, C.byref(b), bs, m, n, k,
+                                                      mul.compute.code,
+                                                      dtypes.MODE_CODE[store.mode]),
+             None, _dev(d_buf))
 
 
 class ChainFn:
@@ -308,7 +308,8 @@ def chain_entry(plan, d_buf, store, a_buf, a_unpack, fn, bases):
             arr[i].scalar[j] = raw[j]
     mode = dtypes.MODE_CODE[store.mode]
     args = (_sh(), C.byref(p), C.byref(d), C.byref(a), n, arr, mode)
-    _guarded(store.mode, lambda: L.tpg_chain(*args), lambda: L.tpg_chain_check(*args))
+    _guarded(store.mode, lambda: L.tpg_chain(*args), lambda: L.tpg_chain_check(*args),
+             _dev(d_buf))
 
 
 def fill_entry(plan, buf, pack, value, base):
@@ -344,8 +345,9 @@ def scatter_entry(pairs, d_buf, store, s_buf, s_unpack):
     arr = np.ascontiguousarray(np.asarray(pairs, dtype=np.int64).reshape(-1))
     d = dest(d_buf, 0, store)
     s = operand(s_buf, 0, s_unpack)
-    _native.check(L.tpg_scatter(_sh(), arr.ctypes.data_as(C.POINTER(C.c_int64)), arr.size // 2,
-                                C.byref(d), C.byref(s), dtypes.MODE_CODE[store.mode]), "scatter")
+    _guarded(store.mode, lambda: L.tpg_scatter(_sh(), arr.ctypes.data_as(C.POINTER(C.c_int64)),
+                                               arr.size // 2, C.byref(d), C.byref(s),
+                                               dtypes.MODE_CODE[store.mode]), None, _dev(d_buf))
 
 
 def scatter_fill_entry(offsets, d_buf, pack, value):

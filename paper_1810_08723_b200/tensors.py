@@ -43,12 +43,19 @@ def default_device():
 
 # ---------------------------------------------------------------------------
 class Storage:
-    """Flat device buffer with a display dtype, byte order and owning stream."""
+    """Flat device buffer with a display dtype, byte order and owning stream.
+
+    Work on a storage may be enqueued on streams other than its own (the
+    `use_stream` override): those streams are remembered in `users`, so
+    every consumer that is not stream-ordered with them -- the stream-ordered
+    free, host reads and writes, raw gathers on the storage's own stream --
+    first waits for all of them (`order` / `host_sync`)."""
 
     def __init__(self, device, nbytes: int, dtype=dtypes.UINT8, ptr: int | None = None,
                  owned: bool = True):
         self.device = device
         self.stream = device.default_stream()
+        self.users: dict = {}  # id(stream) -> stream: foreign streams with enqueued work
         self.nbytes = int(nbytes)
         self.ptr = ptr if ptr is not None else device.allocate(self.nbytes)
         self.dtype = dtype
@@ -59,13 +66,33 @@ class Storage:
     def view(self):
         return self  # table entries receive the buffer handle (.ptr)
 
+    # -- stream bookkeeping ---------------------------------------------------
+    def note_use(self, stream) -> None:
+        """`stream` has enqueued (or is about to enqueue) work on this storage."""
+        if stream is not self.stream:
+            self.users[id(stream)] = stream
+
+    def order(self, stream) -> None:
+        """Make `stream` wait for every stream with work on this storage."""
+        for s in (self.stream, *self.users.values()):
+            if s is not stream:
+                stream.wait_for(s)
+
+    def host_sync(self) -> None:
+        """Block the host until all work on this storage has completed."""
+        self.stream.sync()
+        for s in list(self.users.values()):
+            s.sync()
+        self.users.clear()
+
     def snapshot(self) -> bytes:
         out = bytearray(self.nbytes)
+        self.order(self.stream)
         if self.nbytes:
             buf = (C.c_char * self.nbytes).from_buffer(out)
             _native.check(_native.lib().tpg_memcpy_d2h(buf, self.ptr, self.nbytes,
                                                        self.stream.handle), "d2h")
-        self.stream.sync()
+        self.host_sync()
         return bytes(out)
 
     def write(self, data, offset: int = 0) -> None:
@@ -74,13 +101,17 @@ class Storage:
         if offset < 0 or offset + n > self.nbytes:
             raise StorageError("write outside storage")
         if n:
+            self.order(self.stream)
             arr = np.frombuffer(mv, dtype=np.uint8)
             _native.check(_native.lib().tpg_memcpy_h2d(self.ptr + offset, arr.ctypes.data, n,
                                                        self.stream.handle), "h2d")
-            self.stream.sync()
+            self.host_sync()
 
     def release(self) -> None:
         if self.owned and self.ptr is not None:
+            # the free is ordered after the work of every stream that used it
+            self.order(self.stream)
+            self.users.clear()
             self.device.release(self.ptr, self.stream)
             self.ptr = None
 
@@ -261,11 +292,12 @@ def to_numpy(t: Tensor) -> np.ndarray:
         raise CastError(f"dtype {t.dtype.name} has no numpy equivalent")
     lo, hi = byte_extent(t)
     raw = bytearray(max(hi - lo, 0))
+    t.storage.order(t.storage.stream)
     if raw:
         buf = (C.c_char * len(raw)).from_buffer(raw)
         _native.check(_native.lib().tpg_memcpy_d2h(buf, t.storage.ptr + lo, len(raw),
                                                    t.storage.stream.handle), "d2h")
-    t.storage.stream.sync()
+    t.storage.host_sync()
     if t.dtype is dtypes.CHALF:
         h = np.dtype(np.float16).newbyteorder("<" if t.byteorder == "little" else ">")
         out = np.empty(t.dims, dtype=np.complex64, order="F")
@@ -522,8 +554,8 @@ def raw_gather(src, dst) -> None:
         return
     plan = canonicalize(dst, src)
     stream = dst.storage.stream
-    if src.storage.stream is not stream:
-        src.storage.stream.sync()
+    src.storage.order(stream)
+    dst.storage.order(stream)
     _native.check(_native.lib().tpg_gather_plan(
         stream.handle, C.byref(plan.to_c()), dst.storage.ptr, dst.offset, src.storage.ptr,
         src.offset, src.dtype.size), "gather")
@@ -548,6 +580,7 @@ def byteswap(t) -> None:
     h = dispatch.lookup("core", t.device.type.name, "byteswap")
     plan = canonicalize(t)
     buf, base, dtype = t.storage.view(), t.offset, t.dtype
+    t.storage.order(t.storage.stream)
     t.storage.stream.submit(lambda: h(buf, base, plan, dtype, t.byteorder))
     t.byteorder = _flip(t.byteorder)
 
@@ -566,7 +599,7 @@ def device_transfer(t, device) -> Tensor:
     out.strides = src.strides
     lo, hi = byte_extent(src)
     if hi > lo:
-        src.storage.stream.sync()
+        src.storage.host_sync()
         _native.check(_native.lib().tpg_memcpy_d2d(out.storage.ptr, src.storage.ptr + lo, hi - lo,
                                                    out.storage.stream.handle), "peer copy")
     out.offset = src.offset - lo

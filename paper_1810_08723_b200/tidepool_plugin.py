@@ -235,6 +235,9 @@ class _Runtime:
         self.lazy_by_src: dict = {}   # src ptr -> {dst ptr}
         self.status_sink = tp.ops._status
         self.event_pool: list = []
+        self.ev_refs: dict = {}  # shared completion marker -> blocks referencing it
+        self.seq = 0             # launch epoch (bumped whenever an entry resolves its stream)
+        self.plans: dict = {}    # (extents, strides) -> abi.Plan (entries rebuild plans per call)
         self.stats = collections.Counter()  # lazy / fused / materialised / transfer paths
         self.profile = None  # [] -> (start, stop) timing events around each standard-mode launch
 
@@ -271,7 +274,7 @@ class _Runtime:
                 for ev in events:
                     self.check(self.L.tpg_event_sync(ev), "event sync")
             self.cached_bytes[key[0]] -= key[1]
-            self.event_pool.extend(events)
+            self._unref(events)
             return ptr
 
     def allocate(self, device, nbytes):
@@ -302,15 +305,34 @@ class _Runtime:
             self._drop_lazy_locked(ptr)
         events = []
         for st in self.streams.get(blk.device, ()):
-            ev = self.event_pool.pop() if self.event_pool else self._new_event()
-            self.L.tpg_event_record(ev, st.handle)
-            events.append(ev)
+            # one completion marker per stream per launch epoch: blocks
+            # released with no launch in between share it
+            if st.marker is None or st.marker_seq != self.seq:
+                ev = self.event_pool.pop() if self.event_pool else self._new_event()
+                self.L.tpg_event_record(ev, st.handle)
+                st.marker, st.marker_seq = ev, self.seq
+                self.ev_refs[ev] = 0
+            self.ev_refs[st.marker] += 1
+            events.append(st.marker)
         with self.lock:
             self.cache.setdefault((blk.device, blk.cap), []).append((ptr, events))
             self.cached_bytes[blk.device] = self.cached_bytes.get(blk.device, 0) + blk.cap
             over = self.cached_bytes[blk.device] > self.CACHE_BYTES
         if over:
             self.trim(blk.device, self.CACHE_BYTES // 2)
+
+    def _unref(self, events):
+        for ev in events:
+            n = self.ev_refs.get(ev, 1) - 1
+            if n > 0:
+                self.ev_refs[ev] = n
+                continue
+            self.ev_refs.pop(ev, None)
+            for sts in self.streams.values():
+                for st in sts:
+                    if st.marker == ev:
+                        st.marker = None
+            self.event_pool.append(ev)
 
     def _new_timing_event(self):
         ev = C.c_void_p()
@@ -336,7 +358,7 @@ class _Runtime:
         for ptr, events in victims:
             for ev in events:
                 self.L.tpg_event_sync(ev)
-                self.event_pool.append(ev)
+            self._unref(events)
             self.L.tpg_free_managed(C.c_void_p(ptr))
 
     # -- pointers --------------------------------------------------------------
@@ -357,6 +379,7 @@ class _Runtime:
 
     # -- streams ----------------------------------------------------------------
     def current(self, device):
+        self.seq += 1
         st = getattr(self.tls, "stream", None)
         if st is not None and st.device.index == device:
             return st
@@ -462,6 +485,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
                 rt.check(L.tpg_stream_create(device.index, C.byref(h)), "stream create")
                 handle = h.value
             self.handle = handle
+            self.marker, self.marker_seq = None, -1
             rt.streams.setdefault(device.index, []).append(self)
 
         def submit(self, task) -> None:
@@ -557,7 +581,15 @@ def register(tidepool_module, count: int | None = None, lib=None):
         return abi.make_operand(ptr, base, d.wire_code, order == "big")
 
     def _plan(pl, strides=None):
-        return abi.make_plan(pl.extents, strides if strides is not None else pl.strides)
+        ext = tuple(pl.extents)
+        strd = tuple(map(tuple, strides if strides is not None else pl.strides))
+        key = (ext, strd)
+        p = rt.plans.get(key)
+        if p is None:
+            if len(rt.plans) > 4096:
+                rt.plans.clear()
+            p = rt.plans[key] = abi.make_plan(ext, strd)
+        return p
 
     def _loss_message(d):
         return f"value cannot be represented as {d.name}"
@@ -640,7 +672,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
                 ops.append(_operand(ptr, base, d, order, temps, plan.extents, plan.strides[v]))
                 strides.append(list(plan.strides[v]))
             rt.before_write(dptr)
-            p = abi.make_plan(plan.extents, strides)
+            p = _plan(plan, strides)
             dop = abi.make_operand(dptr, bases[0], dd.wire_code, dord == "big")
             args = (st.handle, code, C.byref(p), C.byref(dop), C.byref(ops[0]), C.byref(ops[1]),
                     compute, MODE_CODE[mode])

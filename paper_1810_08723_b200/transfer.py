@@ -90,7 +90,10 @@ def upload(src: np.ndarray, t, stream=None) -> None:
     """Async copy of a (pinned) host array's bytes into tensor `t`."""
     off, width, height, pitch = _layout(t)
     hp, hpitch = _host_layout(src, width, height)
-    s = (stream or t.storage.stream).handle
+    st = stream or t.storage.stream
+    t.storage.order(st)
+    t.storage.note_use(st)
+    s = st.handle
     L = _native.lib()
     dst = t.storage.ptr + off
     if height == 1:
@@ -103,7 +106,10 @@ def download(t, dst: np.ndarray, stream=None) -> None:
     """Async copy of tensor `t`'s bytes into a (pinned) host array."""
     off, width, height, pitch = _layout(t)
     hp, hpitch = _host_layout(dst, width, height)
-    s = (stream or t.storage.stream).handle
+    st = stream or t.storage.stream
+    t.storage.order(st)
+    t.storage.note_use(st)
+    s = st.handle
     L = _native.lib()
     src = t.storage.ptr + off
     if height == 1:

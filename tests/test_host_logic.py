@@ -58,7 +58,7 @@ def test_build_plan_matches_reference():
 
 def test_core_table_has_all_31_reference_keys():
     ops = dispatch.table_ops("core", "gpu")
-    assert len(set(ops) - {"ewise_chain"}) == 31   # + the fused-chain extension entry
+    assert len(set(ops) - {"ewise_chain", "matmul_batched"}) == 31   # + 2 extension entries
     for k in ("add", "copy", "sum", "reduce_minimum", "reduce_maximum", "norm", "matmul",
               "fill", "arange", "byteswap", "gather", "scatter", "scatter_fill"):
         assert k in ops

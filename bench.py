@@ -709,11 +709,15 @@ def cfg4(tp, dev, run):
 
 def sharded_extras(tp, dev, L, dist, steps=5, warmup=3):
     """N>1: the sharded paths of SURVEY §8e measured across all ranks (max
-    over ranks of device time per step, whole-job aggregate bytes):
-    cfg3 full sum of the f64 8192^2 matrix split along axis 1 (local
-    single-pass reduction + ONE NCCL all-reduce over NVLink), and cfg5's
-    fused multiply-add chain on 2^30 f32 elements split into slabs."""
-    from paper_1810_08723_b200.sharded import NcclComm, Sharded
+    over ranks of device time per step, whole-job aggregate bytes / flop),
+    each value-checked:
+      * cfg3 full sum / maximum / norm of the f64 8192^2 matrix split along
+        axis 1: local single-pass reduction into a device payload + ONE NCCL
+        all-reduce (tpg_shard_pack / unpack for max), result on the device;
+      * cfg5's fused multiply-add chain on 2^30 f32 elements split into N
+        slabs (strong scaling);
+      * batched gemm 64 x 2048^3 f16 split along the batch axis (strong)."""
+    from paper_1810_08723_b200.sharded import NcclComm, Sharded, shard_bounds
     import torch.distributed as tdist
     res = {}
     stream = dev.default_stream()
@@ -734,34 +738,63 @@ def sharded_extras(tp, dev, L, dist, steps=5, warmup=3):
         dist.barrier()
         return dist.max(statistics.median(ms))
 
+    comm = None
     try:
         comm = NcclComm(dev, dist.rank, dist.world, share)
+        res["nccl"] = comm.info()
         n = 8192
         cols = np.random.default_rng(5).random((n, n))  # same matrix on every rank
         S = Sharded.from_numpy(cols, dist.rank, dist.world, dev, axis=1)
+        want = {"sum": cols.sum(), "maximum": cols.max(), "norm": np.sqrt((cols * cols).sum())}
         del cols
-        total = {}
-
-        def red():
-            total["v"] = S.reduce_full("sum", comm)
-        m = timed(red)
-        res[f"cfg3_sum_full_f64_8192^2_sharded_{dist.world}gpu_nccl"] = {
-            "ms": round(m, 4), "GB/s": round(n * n * 8 / m / 1e6, 1)}
-        comm.close()
+        for op in ("sum", "maximum", "norm"):
+            box = {}
+            m = timed(lambda op=op, box=box: box.__setitem__("r", S.reduce_full_tensor(op, comm)))
+            got = box["r"].item()
+            ok = got == want[op] if op == "maximum" else abs(got - want[op]) <= 1e-12 * want[op]
+            res[f"cfg3_{op}_full_f64_8192^2_sharded_{dist.world}gpu_nccl"] = {
+                "ms": round(m, 4), "GB/s": round(n * n * 8 / m / 1e6, 1),
+                "checked": "exact" if op == "maximum" else "rel 1e-12 vs numpy", "ok": bool(ok)}
     except Exception as exc:  # pragma: no cover - reported, not fatal
         res["cfg3_sharded_error"] = repr(exc)[:200]
     try:
-        per = (1 << 30) // dist.world
+        lo, hi = shard_bounds(1 << 30, dist.world, dist.rank)
+        per = hi - lo
         Y = tp.tensor_create((per,), tp.float, dev)
         tp.fill(Y, 1.25)
         Z = tp.tensor_create((per,), tp.float, dev)
         k15, km2 = tp.Scalar(1.5, tp.float), tp.Scalar(-2.0, tp.float)
         m = timed(lambda: tp.chain(Y, [("multiply", k15), ("add", km2)], dest=Z))
+        ok = bool(np.all(tp.to_numpy(tp.apply_index(Z, (slice(0, 1 << 16),))) == -0.125))
         res[f"cfg5_chain_f32_2^30_sharded_{dist.world}gpu"] = {
-            "ms": round(m, 4), "GB/s": round(dist.world * per * 8 / m / 1e6, 1)}
+            "ms": round(m, 4), "GB/s": round((1 << 30) * 8 / m / 1e6, 1), "ok": ok,
+            "scaling": "strong (2^30 elements split into slabs)"}
         del Y, Z
     except Exception as exc:  # pragma: no cover
         res["cfg5_sharded_error"] = repr(exc)[:200]
+    try:
+        nb, s_ = 64, 2048
+        lo, hi = shard_bounds(nb, dist.world, dist.rank)
+        rng = np.random.default_rng(6)
+        a = rng.uniform(-1, 1, (s_, s_, nb)).astype(np.float16)[:, :, lo:hi]
+        b = rng.uniform(-1, 1, (s_, s_, nb)).astype(np.float16)[:, :, lo:hi]
+        A = Sharded(tp.from_numpy(np.asfortranarray(a), dev), (s_, s_, nb), 2, lo, dist.rank,
+                    dist.world)
+        B = Sharded(tp.from_numpy(np.asfortranarray(b), dev), (s_, s_, nb), 2, lo, dist.rank,
+                    dist.world)
+        box = {}
+        m = timed(lambda: box.__setitem__("c", A.matmul_batched(B)))
+        got = tp.to_numpy(box["c"].local)[:8, :8, 0].astype(np.float64)
+        want = a[:8, :, 0].astype(np.float64) @ b[:, :8, 0].astype(np.float64)
+        bound = np.abs(a[:8, :, 0]).astype(np.float64) @ np.abs(b[:, :8, 0]).astype(np.float64)
+        res[f"cfg4_gemm_batched_f16_64x2048^3_sharded_{dist.world}gpu"] = {
+            "ms": round(m, 4), "TFLOP/s": round(nb * 2 * s_ ** 3 / m / 1e9, 1),
+            "ok": bool(np.all(np.abs(got - want) <= 1e-2 * bound)),
+            "scaling": "strong (64 batches split along the batch axis)"}
+    except Exception as exc:  # pragma: no cover
+        res["cfg4_sharded_error"] = repr(exc)[:200]
+    if comm is not None:
+        comm.close()
     return res
 
 
@@ -806,11 +839,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--sharded-extras", action="store_true",
+                    help="run the N>1 sharded workloads also at N=1 (exercise the path)")
     args = ap.parse_args()
     dist = Dist()
     hbm_peak, tc_peak, peak_kind = peaks()
     config = {"workload": "cfg2: int16[4096,4096] transposed reversed view (strides -8192,2) "
-                          "+ float32[1,4096] broadcast -> float32 add",
+                          "+ float32[1,4096] broadcast -> float32 add"
+                          + ("" if dist.world == 1 else
+                             f"; sharded: each of the {dist.world} ranks owns one 4096-column "
+                             f"slab of a global [4096, {4096 * dist.world}] problem (column "
+                             "slabs of the column-major result, no exchange)"),
               "elements": N * N, "algorithmic_bytes_per_step": CFG2_BYTES,
               "l2": f"inputs larger than L2: K back-to-back steps rotate over {ROT} input/output "
                     f"sets ({ROT} x 100.7 MB > 126 MB L2), one event pair around the K steps; "
@@ -859,8 +898,8 @@ def main():
             work["cfg2_through_reference_plugin"] = bench_plugin(L)
         except Exception as exc:  # pragma: no cover - reported, not fatal
             work["cfg2_through_reference_plugin"] = {"error": repr(exc)[:300]}
-    elif dist.world > 1 and not args.no_extras:
-        work = sharded_extras(tp, dev, L, dist)
+    if (dist.world > 1 or args.sharded_extras) and not args.no_extras:
+        work.update(sharded_extras(tp, dev, L, dist))
     clk = clocks.stop()
     if dist.rank == 0:
         traffic = None

@@ -271,6 +271,19 @@ int tpg_nccl_init(int device, int nranks, int rank, const void* id128);
 int tpg_nccl_allreduce(tpg_stream stream, void* buf, int64_t count,
                        int dtype, int op /*0 sum,1 prod,2 max,3 min*/);
 int tpg_nccl_destroy(void);
+/* communicator size and this process's rank, as NCCL sees them */
+int tpg_nccl_info(int* nranks, int* rank);
+
+/* Sharded min/max finish: pack a rank's local extreme
+ * (payload slot 0: double for float sources, kind 0; int64 for signed
+ * integers, kind 1; uint64 bits for unsigned, kind 2) into an order key
+ * for ONE max all-reduce of the 2-slot payload, slot 1 = the first-element
+ * NaN flag (ops.py:533-544; `first` = the tensor's element 0 on the rank
+ * holding it, else NULL); unpack maps the reduced key back (NaN when the
+ * flag is set).  has = 0: the rank holds no elements. */
+int tpg_shard_pack(tpg_stream stream, int is_max, int kind, int has, void* payload,
+                   const void* first, int first_dtype, int first_big_endian);
+int tpg_shard_unpack(tpg_stream stream, int is_max, int kind, void* payload);
 
 #ifdef __cplusplus
 }

@@ -133,6 +133,9 @@ PROTOTYPES = {
     "tpg_nccl_init": (_i32, [C.c_int, C.c_int, C.c_int, _vp]),
     "tpg_nccl_allreduce": (_i32, [_vp, _vp, _i64, C.c_int, C.c_int]),
     "tpg_nccl_destroy": (_i32, []),
+    "tpg_nccl_info": (_i32, [P(C.c_int), P(C.c_int)]),
+    "tpg_shard_pack": (_i32, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_int, C.c_int]),
+    "tpg_shard_unpack": (_i32, [_vp, C.c_int, C.c_int, _vp]),
 }
 
 # not in the public header (host-side error-mode pre-checks)

@@ -88,11 +88,18 @@ class NcclComm:
         s.sync()
         return out
 
-    def allreduce_device(self, ptr: int, count: int, op: int, stream) -> None:
-        """In-place all-reduce of `count` doubles already on this device,
-        enqueued on `stream` (no host round trip)."""
-        _native.check(_native.lib().tpg_nccl_allreduce(stream.handle, ptr, count, 11, op),
+    def allreduce_device(self, ptr: int, count: int, op: int, stream, dtype: int = 11) -> None:
+        """In-place all-reduce of `count` elements (dtype wire code, default
+        double) already on this device, enqueued on `stream` (no host round
+        trip)."""
+        _native.check(_native.lib().tpg_nccl_allreduce(stream.handle, ptr, count, dtype, op),
                       "allreduce")
+
+    def info(self) -> dict:
+        """The communicator as NCCL sees it (logged by bench.py)."""
+        n, r = C.c_int(0), C.c_int(0)
+        _native.check(_native.lib().tpg_nccl_info(C.byref(n), C.byref(r)), "nccl info")
+        return {"nranks": n.value, "rank": r.value}
 
     def close(self):
         _native.lib().tpg_nccl_destroy()
@@ -154,27 +161,93 @@ class Sharded:
         return Sharded(out, self.dims, self.axis, self.lo, self.rank, self.world)
 
     def reduce_full(self, op: str, comm, p: float = 2.0):
-        """Full reduction: local kernel + one all-reduce."""
+        """Full reduction as a host value (one 0-dim read of
+        `reduce_full_tensor`; host-combined for communicators without a
+        device all-reduce, e.g. gloo)."""
+        if hasattr(comm, "allreduce_device") and not (op == "norm" and p != 2.0):
+            return self.reduce_full_tensor(op, comm, p).item()
+        return self._reduce_full_host(op, comm, p)
+
+    def reduce_full_tensor(self, op: str, comm, p: float = 2.0):
+        """Full reduction finished on the devices: the local
+        kernel writes this rank's partial into a small device payload, ONE
+        all-reduce combines the payloads in place over NVLink, and the
+        result lands in a 0-dim device tensor of the reference's result
+        dtype (ops.py:457-478).  No host round trip.
+
+        sum      int64 / uint64 payload for integer data (exact, wraps like
+                 the reference), double otherwise; SUM
+        norm     p = 2: |x|^2 partial in double; SUM; sqrt on the device
+        product  int64 / uint64 (exact mod 2^64) or double; PROD
+        min/max  [order key, first-element-NaN flag]; ONE MAX
+                 (tpg_shard_pack / tpg_shard_unpack)
+        any/all  bool; MAX / MIN
+        """
         from . import dtypes, ops
         from . import tensors as tz
         t = self.local
+        src = t.dtype
+        if src.is_complex and op in ("minimum", "maximum"):
+            raise ValueError("sharded min/max of complex data is not supported")
+        if op in ("minimum", "maximum") and math.prod(self.dims) == 0:
+            raise TypeError(f"{op} of an empty range")  # the reference's fin(None) fails
+        if op == "norm" and p != 2.0:
+            raise ValueError("device-finished norm supports p = 2 (use reduce_full)")
         has = t.nelem > 0
-        if op in ("sum", "norm") and hasattr(comm, "allreduce_device") and (op == "sum" or p == 2.0):
-            # device-resident finish: the local kernel writes its partial to
-            # a device double, NCCL sums it in place, one read at the end
-            dst = _scalar_double(t)
-            if has:
-                if op == "sum":
-                    ops.reduce("sum", t, dest=dst)
-                else:
-                    ops.reduce("norm", t, dest=dst, p=2.0)
-                    ops.multiply(dst, dst, dest=dst)  # |x|_2^2, exact enough (1 ulp)
+        rdtype = (dtypes.BOOL if op in ("any", "all") else
+                  (dtypes.real_counterpart(src) if src.is_float else dtypes.DOUBLE)
+                  if op == "norm" else src)
+        integer = src.is_integer or src is dtypes.BOOL
+        if op in ("any", "all"):
+            pdt, red = dtypes.BOOL, MAX if op == "any" else MIN
+        elif op in ("sum", "product") and integer:
+            pdt = dtypes.UINT64 if src is dtypes.UINT64 else dtypes.INT64
+            red = SUM if op == "sum" else PROD
+        elif op in ("minimum", "maximum") and integer:
+            pdt, red = dtypes.INT64, MAX
+        else:
+            pdt, red = dtypes.DOUBLE, {"sum": SUM, "norm": SUM, "product": PROD}.get(op, MAX)
+        pay = tz.tensor_create((2,), pdt, t.device)
+        slot0 = tz.Tensor(pay.storage, 0, (), (), dtypes.UINT64 if src is dtypes.UINT64 and
+                          op in ("minimum", "maximum", "sum", "product") else pdt)
+        st = pay.storage.stream
+        with _implicit():
+            if not has:
+                ops.fill(slot0, {"product": 1, "all": True}.get(op, 0))
+            elif op == "norm":
+                ops.reduce("norm", t, dest=slot0, p=2.0)
+                ops.multiply(slot0, slot0, dest=slot0)  # |x|_2^2 (1 ulp)
+            elif op in ("minimum", "maximum"):
+                ops.reduce(op, t, dest=slot0, p=-1.0)   # extreme over non-NaN values
             else:
-                ops.fill(dst, 0.0)
-            st = dst.storage.stream
-            comm.allreduce_device(dst.storage.ptr + dst.offset, 1, SUM, st)
-            s = float(dst.item())
-            return s if op == "sum" else math.sqrt(s)
+                ops.reduce(op, t, dest=slot0)
+            if op in ("minimum", "maximum"):
+                kind = 0 if not integer else (2 if src is dtypes.UINT64 else 1)
+                first = self.lo == 0 and has and src.is_float
+                L = _native.lib()
+                t.storage.order(st)
+                pay.storage.order(st)
+                _native.check(L.tpg_shard_pack(
+                    st.handle, int(op == "maximum"), kind, int(has), pay.storage.ptr,
+                    (t.storage.ptr + t.offset) if first else None, src.code,
+                    int(t.byteorder == "big")), "shard pack")
+                comm.allreduce_device(pay.storage.ptr, 2, red, st, pdt.code)
+                _native.check(L.tpg_shard_unpack(st.handle, int(op == "maximum"), kind,
+                                                 pay.storage.ptr), "shard unpack")
+            else:
+                comm.allreduce_device(pay.storage.ptr, 1, red, st, pdt.code)
+            if op == "norm":
+                ops.square_root(slot0, dest=slot0)
+            out = tz.tensor_create((), rdtype, t.device)
+            ops.copy(slot0, out)
+        return out
+
+    def _reduce_full_host(self, op: str, comm, p: float):
+        """Host-side finish for communicators without device buffers."""
+        from . import ops
+        from . import tensors as tz
+        t = self.local
+        has = t.nelem > 0
         if op in ("sum", "norm"):
             part = (_local_sum(t) if op == "sum" else _local_power_sum(t, p)) if has else 0.0
             return combine_partials(op, part, comm, p=p)
@@ -195,6 +268,34 @@ class Sharded:
             v = bool(ops.reduce(op, t).item()) if has else (op == "all")
             return combine_partials(op, v, comm)
         raise ValueError(op)
+
+    def matmul_batched(self, other: "Sharded"):
+        """Batched gemm sharded along the batch axis: every rank
+        multiplies its own batch slab; no exchange.  Both operands must be
+        split along their batch axis (2) with the same bounds."""
+        from . import ops
+        if self.axis != 2 or other.axis != 2 or self.lo != other.lo \
+                or self.local.dims[2] != other.local.dims[2]:
+            raise ValueError("sharded batched gemm needs both operands split along the batch "
+                             "axis with the same bounds")
+        m, _, nb = self.dims
+        n = other.dims[1]
+        out = ops.matmul_batched(self.local, other.local)
+        return Sharded(out, (m, n, nb), 2, self.lo, self.rank, self.world)
+
+
+class _implicit:
+    """Internal reductions into payload slots of another dtype are exempt
+    from strict mode: implicit casting on for the block."""
+
+    def __enter__(self):
+        from . import dtypes
+        self.prev = dtypes.implicit_casting()
+        dtypes.set_implicit_casting(True)
+
+    def __exit__(self, *exc):
+        from . import dtypes
+        dtypes.set_implicit_casting(self.prev)
 
 
 def _scalar_double(t):

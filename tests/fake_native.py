@@ -180,17 +180,84 @@ class FakeNative:
         self.flags[0] |= st.value | self.inject
         self.inject = 0
 
-    # single-rank NCCL: the all-reduce of one rank is the identity
+    # NCCL stand-in: the all-reduce runs over torch.distributed (gloo) on
+    # the host bytes when a process group is up, else it is the identity of
+    # a single rank
     def tpg_nccl_get_unique_id(self, out):
         return 0
 
     def tpg_nccl_init(self, dev, nranks, rank, uid):
-        return 0 if nranks == 1 else -4
+        import torch.distributed as dist
+        if nranks == 1 or (dist.is_initialized() and dist.get_world_size() == nranks):
+            self.nccl = (nranks, rank)
+            return 0
+        return -4
+
+    def tpg_nccl_info(self, n, r):
+        _obj(n).value, _obj(r).value = getattr(self, "nccl", (1, 0))
+        return 0
 
     def tpg_nccl_allreduce(self, s, buf, count, dtype, op):
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        if not dist.is_initialized() or dist.get_world_size() == 1:
+            return 0
+        npd = {0: np.uint8, 1: np.int8, 2: np.uint8, 5: np.int32, 6: np.uint32, 7: np.int64,
+               8: np.uint64, 10: np.float32, 11: np.float64}[dtype]
+        raw = (C.c_ubyte * (count * np.dtype(npd).itemsize)).from_address(_int(buf))
+        arr = np.frombuffer(raw, dtype=npd)
+        wide = torch.from_numpy(arr.astype(np.int64 if npd == np.uint64 else npd).copy())
+        if npd == np.uint64 and op in (2, 3):   # order of unsigned keys: bias into int64
+            wide = torch.from_numpy((arr ^ np.uint64(1 << 63)).view(np.int64).copy())
+        rop = [dist.ReduceOp.SUM, dist.ReduceOp.PRODUCT, dist.ReduceOp.MAX, dist.ReduceOp.MIN][op]
+        dist.all_reduce(wide, op=rop)
+        res = wide.numpy()
+        if npd == np.uint64:
+            res = (res.view(np.uint64) ^ np.uint64(1 << 63)) if op in (2, 3) else res.view(np.uint64)
+        arr[:] = res.astype(npd)
         return 0
 
     def tpg_nccl_destroy(self):
+        return 0
+
+    def tpg_shard_pack(self, s, is_max, kind, has, payload, first, fdt, fbig):
+        import numpy as np
+        fnan = 0
+        if first:
+            npd = {11: "f8", 10: "f4", 9: "f2"}.get(fdt)
+            if npd is not None:
+                raw = (C.c_ubyte * 8).from_address(_int(first))
+                v = np.frombuffer(bytes(raw)[:np.dtype(npd).itemsize],
+                                  dtype=(">" if fbig else "<") + npd)[0]
+                fnan = 1 if v != v else 0
+        if kind == 0:
+            p = np.frombuffer((C.c_ubyte * 16).from_address(_int(payload)), dtype=np.float64)
+            v = p[0]
+            p[0] = (v if is_max else -v) if (has and v == v) else -np.inf
+            p[1] = fnan
+        else:
+            p = np.frombuffer((C.c_ubyte * 16).from_address(_int(payload)), dtype=np.int64)
+            k = p[0]
+            if kind == 2:  # unsigned source: flip the sign bit (order-preserving)
+                k = np.array([p.view(np.uint64)[0] ^ np.uint64(1 << 63)],
+                             dtype=np.uint64).view(np.int64)[0]
+            p[0] = (k if is_max else ~k) if has else np.iinfo(np.int64).min
+            p[1] = 0
+        return 0
+
+    def tpg_shard_unpack(self, s, is_max, kind, payload):
+        import numpy as np
+        if kind == 0:
+            p = np.frombuffer((C.c_ubyte * 16).from_address(_int(payload)), dtype=np.float64)
+            p[0] = np.nan if p[1] != 0 else (p[0] if is_max else -p[0])
+        else:
+            p = np.frombuffer((C.c_ubyte * 16).from_address(_int(payload)), dtype=np.int64)
+            k = p[0] if is_max else ~p[0]
+            if kind == 2:
+                k = np.array([np.array([k], dtype=np.int64).view(np.uint64)[0]
+                              ^ np.uint64(1 << 63)], dtype=np.uint64).view(np.int64)[0]
+            p[0] = k
         return 0
 
     # -- kernels (oracle) ---------------------------------------------------------

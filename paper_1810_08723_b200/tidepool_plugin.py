@@ -238,6 +238,7 @@ class _Runtime:
         self.ev_refs: dict = {}  # shared completion marker -> blocks referencing it
         self.seq = 0             # launch epoch (bumped whenever an entry resolves its stream)
         self.plans: dict = {}    # (extents, strides) -> abi.Plan (entries rebuild plans per call)
+        self.bases: dict = {}    # block ptr -> uint8 ndarray over its full capacity
         self.stats = collections.Counter()  # lazy / fused / materialised / transfer paths
         self.profile = None  # [] -> (start, stop) timing events around each standard-mode launch
 
@@ -293,8 +294,10 @@ class _Runtime:
             self.blocks[ptr] = (device, cap)
         # a uint8 ndarray over the block: its memoryview has format "B", so
         # the reference's struct packing and slice assignment work on it
-        arr = _np.ctypeslib.as_array((C.c_ubyte * max(nbytes, 1)).from_address(ptr))
-        arr = arr.view(_DevBytes)
+        base = self.bases.get(ptr)
+        if base is None:  # one full-capacity ndarray per block, reused on recycling
+            base = self.bases[ptr] = _np.ctypeslib.as_array((C.c_ubyte * cap).from_address(ptr))
+        arr = base[:max(nbytes, 1)].view(_DevBytes)
         arr._tpg_block = blk
         return arr
 
@@ -359,6 +362,7 @@ class _Runtime:
             for ev in events:
                 self.L.tpg_event_sync(ev)
             self._unref(events)
+            self.bases.pop(ptr, None)
             self.L.tpg_free_managed(C.c_void_p(ptr))
 
     # -- pointers --------------------------------------------------------------

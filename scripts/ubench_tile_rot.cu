@@ -311,6 +311,247 @@ __global__ void __launch_bounds__(256) k_tread2(const int16_t* __restrict__ X,
   }
 }
 
+// k_twrite with a padded output leading dimension LD (floats): does the
+// 16-KiB column stride alias the write pattern onto few memory channels?
+template <int LD>
+__global__ void __launch_bounds__(256) k_twrite_ld(const int16_t* __restrict__ X,
+                                                   float* __restrict__ out) {
+  const int w = blockIdx.x, ti = w % 64, tj = w / 64;
+  const int ig = threadIdx.x % 16;
+#pragma unroll
+  for (int pass = 0; pass < 4; ++pass) {
+    const int j = threadIdx.x / 16 + 16 * pass;
+    const uint2 v = __ldcs((const uint2*)(X + (size_t)w * 4096 + j * 64 + ig * 4));
+    const int16_t* e = (const int16_t*)&v;
+    __stcs((float4*)(out + (size_t)(tj * 64 + j) * LD + ti * 64 + ig * 4),
+           make_float4(e[0], e[1], e[2], e[3]));
+  }
+}
+
+// write-side shape sweep: each block writes NC output columns x SEG floats
+// (SEG * NC = 4096 elements, contiguous reads); block w covers column group
+// w / (N / SEG) and row segment w % (N / SEG)
+template <int SEG, int NC>
+__global__ void __launch_bounds__(256) k_wshape(const int16_t* __restrict__ X,
+                                                float* __restrict__ out) {
+  const int w = blockIdx.x, ns = N / SEG;
+  const int ts = w % ns, tc = w / ns;
+  for (int e = threadIdx.x * 4; e < 4096; e += 1024) {
+    const int j = e / SEG, i = e % SEG;
+    const uint2 v = __ldcs((const uint2*)(X + (size_t)w * 4096 + e));
+    const int16_t* q = (const int16_t*)&v;
+    __stcs((float4*)(out + (size_t)(tc * NC + j) * N + ts * SEG + i),
+           make_float4(q[0], q[1], q[2], q[3]));
+  }
+}
+
+// k_wshape with all of a thread's loads issued before its stores
+template <int SEG, int NC>
+__global__ void __launch_bounds__(256) k_wshape_u(const int16_t* __restrict__ X,
+                                                  float* __restrict__ out) {
+  const int w = blockIdx.x, ns = N / SEG;
+  const int ts = w % ns, tc = w / ns;
+  uint2 v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = __ldcs((const uint2*)(X + (size_t)w * 4096 + threadIdx.x * 4 + k * 1024));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int e = threadIdx.x * 4 + k * 1024;
+    const int j = e / SEG, i = e % SEG;
+    const int16_t* q = (const int16_t*)&v[k];
+    __stcs((float4*)(out + (size_t)(tc * NC + j) * N + ts * SEG + i),
+           make_float4(q[0], q[1], q[2], q[3]));
+  }
+}
+
+// tile-pattern reads (64 X columns x 128 B) issued all before any store,
+// contiguous full-sector writes: the read side with full memory-level
+// parallelism
+__global__ void __launch_bounds__(256) k_tread_u(const int16_t* __restrict__ X,
+                                                 float* __restrict__ out) {
+  const int w = blockIdx.x, ti = w % 64, tj = w / 64;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane % 8, r0 = warp * 4 + lane / 8;
+  uint4 v[2];
+#pragma unroll
+  for (int l = 0; l < 2; ++l)
+    v[l] = __ldcs((const uint4*)(X + (size_t)(N - 1 - (ti * 64 + r0 + l * 32)) * N + tj * 64) + c);
+#pragma unroll
+  for (int l = 0; l < 2; ++l) {
+    const int16_t* e = (const int16_t*)&v[l];
+    // 8 lanes x 2 float4 = 256 B contiguous per row; rows of a warp adjacent
+    float* o = out + (size_t)w * 4096 + (r0 + l * 32) * 64 + c * 8;
+    __stcs((float4*)o, make_float4(e[0], e[1], e[2], e[3]));
+    __stcs((float4*)o + 1, make_float4(e[4], e[5], e[6], e[7]));
+  }
+}
+
+// the full cfg2 tile op, one tile per block, 8 blocks / SM (32 regs),
+// loads issued first; smem transpose; tile-pattern writes
+__global__ void __launch_bounds__(256, 8) k_tile_hi(const int16_t* __restrict__ X,
+                                                    const float* __restrict__ R,
+                                                    float* __restrict__ out) {
+  __shared__ __align__(16) float sm[64][64];
+  const int w = blockIdx.x, ti = w % 64, tj = w / 64;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane % 8, r0 = warp * 4 + lane / 8;
+  const int swz1 = (c * 4) & 31;
+  uint4 v[2];
+#pragma unroll
+  for (int l = 0; l < 2; ++l)
+    v[l] = __ldcs((const uint4*)(X + (size_t)(N - 1 - (ti * 64 + r0 + l * 32)) * N + tj * 64) + c);
+  float y[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) y[k] = __ldg(R + tj * 64 + c * 8 + k);
+#pragma unroll
+  for (int l = 0; l < 2; ++l) {
+    const int16_t* e = (const int16_t*)&v[l];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sm[c * 8 + k][(r0 + l * 32) ^ swz1] = (float)e[k] + y[k];
+  }
+  __syncthreads();
+  const int ig = threadIdx.x % 16;
+#pragma unroll
+  for (int pass = 0; pass < 4; ++pass) {
+    const int j = threadIdx.x / 16 + 16 * pass;
+    const int swz = ((j / 8) * 4) & 31;
+    const float4 f = *(const float4*)&sm[j][(ig * 4) ^ swz];
+    __stcs((float4*)(out + (size_t)(tj * 64 + j) * N + ti * 64 + ig * 4), f);
+  }
+}
+
+// the full cfg2 op with T tiles per block (adjacent i-tiles of one column
+// group), ALL 2*T loads of a thread issued before any conversion: 32*T
+// bytes in flight per thread; smem T x 16 KiB
+template <int T, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_tile_mt(const int16_t* __restrict__ X,
+                                                       const float* __restrict__ R,
+                                                       float* __restrict__ out) {
+  extern __shared__ __align__(16) float smt[];
+  const int w0 = blockIdx.x * T;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane % 8, r0 = warp * 4 + lane / 8;
+  const int swz1 = (c * 4) & 31;
+  uint4 v[T][2];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int w = w0 + t, ti = w % 64, tj = w / 64;
+#pragma unroll
+    for (int l = 0; l < 2; ++l)
+      v[t][l] = __ldcs((const uint4*)(X + (size_t)(N - 1 - (ti * 64 + r0 + l * 32)) * N + tj * 64) + c);
+  }
+  const int tj0 = w0 / 64;
+  float y[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) y[k] = __ldg(R + tj0 * 64 + c * 8 + k);
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    float(*sm)[64] = (float(*)[64])(smt + t * 4096);
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      const int16_t* e = (const int16_t*)&v[t][l];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sm[c * 8 + k][(r0 + l * 32) ^ swz1] = (float)e[k] + y[k];
+    }
+  }
+  __syncthreads();
+  const int ig = threadIdx.x % 16;
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int w = w0 + t, ti = w % 64, tj = w / 64;
+    float(*sm)[64] = (float(*)[64])(smt + t * 4096);
+#pragma unroll
+    for (int pass = 0; pass < 4; ++pass) {
+      const int j = threadIdx.x / 16 + 16 * pass;
+      const int swz = ((j / 8) * 4) & 31;
+      const float4 f = *(const float4*)&sm[j][(ig * 4) ^ swz];
+      __stcs((float4*)(out + (size_t)(tj * 64 + j) * N + ti * 64 + ig * 4), f);
+    }
+  }
+}
+
+// tile-pattern reads (hoisted) with X column stride LDX int16, contiguous
+// full-sector writes: read-side aliasing check
+template <int LDX>
+__global__ void __launch_bounds__(256) k_tread_ld(const int16_t* __restrict__ X,
+                                                  float* __restrict__ out) {
+  const int w = blockIdx.x, ti = w % 64, tj = w / 64;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane % 8, r0 = warp * 4 + lane / 8;
+  uint4 v[2];
+#pragma unroll
+  for (int l = 0; l < 2; ++l)
+    v[l] = __ldcs((const uint4*)(X + (size_t)(N - 1 - (ti * 64 + r0 + l * 32)) * LDX + tj * 64) + c);
+#pragma unroll
+  for (int l = 0; l < 2; ++l) {
+    const int16_t* e = (const int16_t*)&v[l];
+    float* o = out + (size_t)w * 4096 + (r0 + l * 32) * 64 + c * 8;
+    __stcs((float4*)o, make_float4(e[0], e[1], e[2], e[3]));
+    __stcs((float4*)o + 1, make_float4(e[4], e[5], e[6], e[7]));
+  }
+}
+
+// tile-pattern reads (8-B loads, 16 lanes per 128-B X segment, all 4
+// issued first) + one 16-B store per lane, 512 contiguous bytes per warp
+// instruction: the read side alone
+__global__ void __launch_bounds__(256) k_tread3(const int16_t* __restrict__ X,
+                                                float* __restrict__ out) {
+  const int w = blockIdx.x, ti = w % 64, tj = w / 64;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint2 v[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const int row = warp * 8 + l * 2 + lane / 16;
+    v[l] = __ldcs((const uint2*)(X + (size_t)(N - 1 - (ti * 64 + row)) * N + tj * 64) + (lane % 16));
+  }
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const int row = warp * 8 + l * 2 + lane / 16;
+    const int16_t* e = (const int16_t*)&v[l];
+    __stcs((float4*)(out + (size_t)w * 4096 + row * 64 + (lane % 16) * 4),
+           make_float4(e[0], e[1], e[2], e[3]));
+  }
+}
+
+// the full cfg2 op with 8-B loads: a warp instruction reads 2 X segments
+// (16 lanes x 8 B = 128 B each), all 4 loads of a thread issued first;
+// smem [j][i ^ s(j)], s(j) = ((j >> 2) & 7) * 4 keeps float4 groups intact
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_tile8(const int16_t* __restrict__ X,
+                                                     const float* __restrict__ R,
+                                                     float* __restrict__ out) {
+  __shared__ __align__(16) float sm[64][64];
+  const int w = blockIdx.x, ti = w % 64, tj = w / 64;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane % 16;  // j = 4q .. 4q+3
+  uint2 v[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const int row = warp * 8 + l * 2 + lane / 16;
+    v[l] = __ldcs((const uint2*)(X + (size_t)(N - 1 - (ti * 64 + row)) * N + tj * 64) + q);
+  }
+  float y[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) y[k] = __ldg(R + tj * 64 + 4 * q + k);
+  const int s1 = (q & 7) * 4;
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const int row = warp * 8 + l * 2 + lane / 16;
+    const int16_t* e = (const int16_t*)&v[l];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sm[4 * q + k][row ^ s1] = (float)e[k] + y[k];
+  }
+  __syncthreads();
+  const int ig = threadIdx.x % 16;
+#pragma unroll
+  for (int pass = 0; pass < 4; ++pass) {
+    const int j = threadIdx.x / 16 + 16 * pass;
+    const int s2 = ((j >> 2) & 7) * 4;
+    const float4 f = *(const float4*)&sm[j][(ig * 4) ^ s2];
+    __stcs((float4*)(out + (size_t)(tj * 64 + j) * N + ti * 64 + ig * 4), f);
+  }
+}
+
 // reads contiguous (each tile's 4096 int16 from a contiguous 8 KiB block),
 // writes in the cfg2 tile pattern (64 output columns x 256 B per tile)
 __global__ void __launch_bounds__(256) k_twrite(const int16_t* __restrict__ X,
@@ -344,12 +585,12 @@ int main(int argc, char** argv) {
   for (int j = 0; j < N; ++j) hr[j] = (float)((j * 7919) % 1000) * 0.001f - 0.5f;
   for (int r = 0; r < ROT; ++r) {
     if (pool) {
-      CK(cudaMallocAsync(&X[r], (size_t)N * N * 2, 0));
-      CK(cudaMallocAsync(&O[r], (size_t)N * N * 4, 0));
+      CK(cudaMallocAsync(&X[r], (size_t)N * 5120 * 2, 0));
+      CK(cudaMallocAsync(&O[r], (size_t)N * 4608 * 4, 0));
       CK(cudaDeviceSynchronize());
     } else {
-      CK(cudaMalloc(&X[r], (size_t)N * N * 2));
-      CK(cudaMalloc(&O[r], (size_t)N * N * 4));
+      CK(cudaMalloc(&X[r], (size_t)N * 5120 * 2));
+      CK(cudaMalloc(&O[r], (size_t)N * 4608 * 4));
     }
     printf("set %d: X %p O %p\n", r, (void*)X[r], (void*)O[r]);
     CK(cudaMemcpy(X[r], hx.data(), hx.size() * 2, cudaMemcpyHostToDevice));
@@ -458,6 +699,56 @@ int main(int argc, char** argv) {
   COLS(64, 128, 3, 8);
   COLS(32, 128, 6, 8);
   COLS(32, 128, 6, 16);
+#define WSHAPE(SEG, NC)                                                                        \
+  timeit("write shape " #SEG " rows x " #NC " cols per block",                                 \
+         [&](int r, int*) { k_wshape<SEG, NC><<<4096, 256>>>(X[r], O[r]); }, false)
+  timeit("k_tile8 full op, 8-B loads, minb8", [&](int r, int*) { k_tile8<8><<<4096, 256>>>(X[r], R, O[r]); }, true);
+  timeit("k_tile8 full op, 8-B loads, minb6", [&](int r, int*) { k_tile8<6><<<4096, 256>>>(X[r], R, O[r]); }, true);
+  timeit("k_tile8 full op, 8-B loads, minb4", [&](int r, int*) { k_tile8<4><<<4096, 256>>>(X[r], R, O[r]); }, true);
+  timeit("tile reads (8-B, hoisted) + contig2-style writes", [&](int r, int*) { k_tread3<<<4096, 256>>>(X[r], O[r]); }, false);
+  timeit("tile reads ldx 4096 (dense)", [&](int r, int*) { k_tread_ld<4096><<<4096, 256>>>(X[r], O[r]); }, false);
+  timeit("tile reads ldx 4160 (+128 B)", [&](int r, int*) { k_tread_ld<4160><<<4096, 256>>>(X[r], O[r]); }, false);
+  timeit("tile reads ldx 4352 (+512 B)", [&](int r, int*) { k_tread_ld<4352><<<4096, 256>>>(X[r], O[r]); }, false);
+  timeit("tile reads ldx 5120 (+2 KiB)", [&](int r, int*) { k_tread_ld<5120><<<4096, 256>>>(X[r], O[r]); }, false);
+  timeit("tile-pattern reads hoisted, contiguous writes",
+         [&](int r, int*) { k_tread_u<<<4096, 256>>>(X[r], O[r]); }, false);
+  timeit("k_tile_hi: full cfg2 op, one tile / block, 8 blocks / SM",
+         [&](int r, int*) { k_tile_hi<<<4096, 256>>>(X[r], R, O[r]); }, true);
+#define TILEMT(T, MINB)                                                                        \
+  {                                                                                            \
+    CK(cudaFuncSetAttribute(k_tile_mt<T, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                            T * 16384));                                                       \
+    timeit("k_tile_mt T=" #T " minb" #MINB,                                                    \
+           [&](int r, int*) { k_tile_mt<T, MINB><<<4096 / T, 256, T * 16384>>>(X[r], R, O[r]); }, \
+           true);                                                                              \
+  }
+  TILEMT(1, 8);
+  TILEMT(2, 6);
+  TILEMT(2, 4);
+  TILEMT(4, 3);
+  TILEMT(4, 2);
+  TILEMT(8, 1);
+  timeit("contig2 U=1 (one load, one store per thread)",
+         [&](int r, int*) { k_contig2<1><<<N * N / 4 / 256, 256>>>(X[r], O[r]); }, false);
+  timeit("write shape 4096x1, loads hoisted",
+         [&](int r, int*) { k_wshape_u<4096, 1><<<4096, 256>>>(X[r], O[r]); }, false);
+  timeit("write shape 64x64, loads hoisted",
+         [&](int r, int*) { k_wshape_u<64, 64><<<4096, 256>>>(X[r], O[r]); }, false);
+  WSHAPE(64, 64);
+  WSHAPE(128, 32);
+  WSHAPE(256, 16);
+  WSHAPE(512, 8);
+  WSHAPE(1024, 4);
+  WSHAPE(2048, 2);
+  WSHAPE(4096, 1);
+  timeit("tile-pattern writes, ld 4096 (dense)",
+         [&](int r, int*) { k_twrite_ld<4096><<<4096, 256>>>(X[r], O[r]); }, false);
+  timeit("tile-pattern writes, ld 4128 (+128 B pad)",
+         [&](int r, int*) { k_twrite_ld<4128><<<4096, 256>>>(X[r], O[r]); }, false);
+  timeit("tile-pattern writes, ld 4160 (+256 B pad)",
+         [&](int r, int*) { k_twrite_ld<4160><<<4096, 256>>>(X[r], O[r]); }, false);
+  timeit("tile-pattern writes, ld 4608 (+2 KiB pad)",
+         [&](int r, int*) { k_twrite_ld<4608><<<4096, 256>>>(X[r], O[r]); }, false);
   timeit("tile-pattern reads, full-sector contiguous writes",
          [&](int r, int*) { k_tread2<<<4096, 256>>>(X[r], O[r]); }, false);
 #define STRIP(TJ, IH, MINB)                                                                    \

@@ -299,15 +299,10 @@ def cast_scalar(value, to: DType, mode: str = "standard", loss: list | None = No
 
 
 def infer_scalar_dtype(value) -> DType:
-    if isinstance(value, bool):
-        return BOOL
-    if isinstance(value, int):
-        return INT64
-    if isinstance(value, float):
-        return DOUBLE
-    if isinstance(value, complex):
-        return CDOUBLE
-    raise CastError(f"not a scalar value: {value!r}")
+    for kind, d in ((bool, BOOL), (int, INT64), (float, DOUBLE), (complex, CDOUBLE)):
+        if isinstance(value, kind):
+            return d
+    raise CastError(f"{value!r} is not a bool, int, float or complex scalar")
 
 
 _FMT = {BOOL: "?", INT8: "b", UINT8: "B", INT16: "h", UINT16: "H", INT32: "i",

@@ -13,6 +13,7 @@ memory; host reads/writes are explicit staged copies.
 from __future__ import annotations
 
 import ctypes as C
+import enum
 import math
 import threading
 
@@ -132,19 +133,20 @@ def storage_alloc(device, nbytes: int, dtype=dtypes.UINT8) -> Storage:
 
 
 class Scalar:
+    """A typed host scalar (the reference's Scalar, tensors.py:41-60): the
+    value is stored already converted to its dtype."""
     __slots__ = ("value", "dtype")
 
     def __init__(self, value, dtype=None):
-        if dtype is None:
-            dtype = dtypes.infer_scalar_dtype(value)
-        self.dtype = dtype
-        self.value = dtypes.cast_scalar(value, dtype)
+        self.dtype = dtype or dtypes.infer_scalar_dtype(value)
+        self.value = dtypes.cast_scalar(value, self.dtype)
 
     def __repr__(self):
-        return f"{self.value!r} ({self.dtype.name})"
+        return f"Scalar({self.value!r}, {self.dtype.name})"
 
 
-class OverlapVerdict:
+class OverlapVerdict(enum.Enum):
+    """How two views of one storage relate (tensors.py:515-526)."""
     DISJOINT = "disjoint"
     EXACT = "exact_overlap"
     POSSIBLE = "possible_overlap"
@@ -159,12 +161,11 @@ def column_major_strides(dims, itemsize):
 
 
 def _check_dims(dims):
-    dims = tuple(int(d) for d in dims)
-    if len(dims) > MAX_DIMS:
-        raise ShapeError(f"{len(dims)} dimensions exceed the limit of {MAX_DIMS}")
-    if any(d < 0 for d in dims):
-        raise ShapeError(f"negative extent in dims {dims}")
-    return dims
+    """Tuple of non-negative extents, at most MAX_DIMS of them."""
+    out = tuple(map(int, dims))
+    if len(out) > MAX_DIMS or min(out, default=0) < 0:
+        raise ShapeError(f"invalid dims {out}: need at most {MAX_DIMS} non-negative extents")
+    return out
 
 
 class Tensor:
@@ -224,16 +225,12 @@ class Tensor:
 
 
 def byte_extent(t):
+    """[lo, hi) bytes of the storage the view can touch ((0, 0) if empty)."""
     if t.nelem == 0:
         return (0, 0)
-    lo = hi = t.offset
-    for d, s in zip(t.dims, t.strides):
-        span = s * (d - 1)
-        if span >= 0:
-            hi += span
-        else:
-            lo += span
-    return (lo, hi + t.dtype.size)
+    spans = [s * (d - 1) for d, s in zip(t.dims, t.strides)]
+    return (t.offset + sum(x for x in spans if x < 0),
+            t.offset + sum(x for x in spans if x > 0) + t.dtype.size)
 
 
 # ---------------------------------------------------------------------------

@@ -480,11 +480,39 @@ def bench_plugin(L, steps=20, warmup=3):
         res = e2e()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / 3
     assert res.storage.snapshot() == want.tobytes(order="F"), "plugin e2e mismatch"
+    # fast D2H: cast(gpu tensor, device=cpu) of the 67 MB
+    # result through the cpu `copy` override (GPU convert + one D2H) vs the
+    # reference's own per-element path on a 256 x 256 slice
+    g = tp.add(V, R)
+    st.sync()
+    t0 = time.perf_counter()
+    h = tp.cast(g, device=tp.cpu())
+    fast_ms = (time.perf_counter() - t0) * 1e3
+    assert h.storage.snapshot() == want.tobytes(order="F"), "fast D2H mismatch"
+    small = tp.apply_index(g, (slice(0, 256), slice(0, 256)))
+    rt.cpu_copy_restore()
+    t0 = time.perf_counter()
+    hs = tp.cast(small, device=tp.cpu())
+    slow_ms = (time.perf_counter() - t0) * 1e3
+    tp.dispatch.override_op("core", "cpu", "copy", rt.cpu_copy_wrapper)
+    assert tp.tensors.read_values(hs) == [float(v) for v in want[:256, :256].ravel(order="F")]
+    t0 = time.perf_counter()
+    _ = bytearray(N * N * 4)  # what the reference's cpu Device.allocate does per result
+    alloc_ms = (time.perf_counter() - t0) * 1e3
+    del _
+    d2h = {"fast_path_ms_67MB": round(fast_ms, 3),
+           "of_which_reference_cpu_allocation_ms": round(alloc_ms, 3),
+           "fast_path_GB/s": round(N * N * 4 / fast_ms / 1e6, 2),
+           "reference_per_element_path_ms_256x256": round(slow_ms, 3),
+           "reference_per_element_path_GB/s": round(256 * 256 * 4 / slow_ms / 1e6, 4),
+           "checked": "byte-identical to the reference path's result"}
+    del g, h, hs, small
     floor = _pipeline_floor(steps=200)
     return {"ms_per_op_wall": round(wall_ms, 4), "device_ms": round(dev_ms, 4),
             "device_GB/s": round(CFG2_BYTES / dev_ms / 1e6, 1), "fused_per_op": fused / steps,
             "reference_pipeline_floor_ms": round(floor, 4),
             "e2e_ms": round(e2e_ms, 3), "e2e_GB/s": round(CFG2_BYTES / e2e_ms / 1e6, 2),
+            "cast_gpu_to_cpu": d2h,
             "checked": "bit-exact vs numpy (device result and e2e result)"}
 
 
@@ -517,6 +545,7 @@ def _pipeline_floor(steps=200):
 def extras(tp, dev, L, warmup=3, steps=5, only=None):
     """Kernel-level numbers for the other configs, rank 0.
     `only`: optional set of config prefixes ("cfg1", "cfg3", ...)."""
+    from paper_1810_08723_b200 import _native
     res = {}
 
     def want(tag):
@@ -559,6 +588,25 @@ def extras(tp, dev, L, warmup=3, steps=5, only=None):
             assert np.array_equal(tp.to_numpy(o), an + bn), "cfg1 mismatch"
             return "bit-exact, all elements"
         run("cfg1_add_f32_2^20", lambda: tp.add(a, b, dest=o), nbytes=12 << 20, check=ck1)
+        # cfg1 is launch-floor-bound per step (profiles/r01g_launch_floor.md);
+        # beside it: the same add back to back (its 12.6 MB stay in L2, so
+        # this is an L2-resident rate, labelled as such) and as one CUDA
+        # graph of 20 launches (launch overhead amortised)
+        step1 = lambda: tp.add(a, b, dest=o)  # noqa: E731
+        bb = statistics.median(timed_batch(L, stream, step1, 50))
+        gexec = C.c_void_p()
+        _native.check(L.tpg_graph_begin(stream.handle), "graph begin")
+        for _ in range(20):
+            step1()
+        _native.check(L.tpg_graph_end(stream.handle, C.byref(gexec)), "graph end")
+        gm = statistics.median(timed_batch(
+            L, stream, lambda: L.tpg_graph_launch(gexec, stream.handle), 10)) / 20
+        L.tpg_graph_destroy(gexec)
+        ck1()
+        res["cfg1_add_f32_2^20"].update({
+            "back_to_back_l2_resident": {"ms": round(bb, 5), "GB/s": round((12 << 20) / bb / 1e6, 1)},
+            "cuda_graph_20_launches_l2_resident": {"ms": round(gm, 5),
+                                                   "GB/s": round((12 << 20) / gm / 1e6, 1)}})
         del a, b, o
 
     if want("cfg3"):

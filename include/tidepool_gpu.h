@@ -159,6 +159,13 @@ int tpg_free_managed(void* ptr);
 int tpg_event_create_untimed(tpg_event* ev);
 int tpg_event_query(tpg_event ev);
 
+/* CUDA graphs: capture the work enqueued on `stream` between begin and end
+ * (thread-local capture mode), replay it with one launch. */
+int tpg_graph_begin(tpg_stream stream);
+int tpg_graph_end(tpg_stream stream, void** graph_exec);
+int tpg_graph_launch(void* graph_exec, tpg_stream stream);
+int tpg_graph_destroy(void* graph_exec);
+
 /* Measurement helper: write then re-read `n` bytes of `scratch` (> L2) on
    `stream`, leaving the L2 full of clean unrelated lines. */
 int tpg_l2_flush(void* scratch, size_t n, tpg_stream stream);

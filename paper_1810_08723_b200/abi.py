@@ -110,6 +110,10 @@ PROTOTYPES = {
     "tpg_event_create_untimed": (_i32, [P(_vp)]),
     "tpg_event_query": (_i32, [_vp]),
     "tpg_l2_flush": (_i32, [_vp, C.c_size_t, _vp]),
+    "tpg_graph_begin": (_i32, [_vp]),
+    "tpg_graph_end": (_i32, [_vp, P(_vp)]),
+    "tpg_graph_launch": (_i32, [_vp, _vp]),
+    "tpg_graph_destroy": (_i32, [_vp]),
     "tpg_gate_arm": (_i32, [_vp]),
     "tpg_gate_release": (_i32, []),
     "tpg_binary": (_i32, [_vp, C.c_int, _PLAN, _OP, _OP, _OP, C.c_int, C.c_int]),

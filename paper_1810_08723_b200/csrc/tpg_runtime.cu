@@ -493,6 +493,41 @@ int tpg_event_query(tpg_event ev) {
   return cuda_fail(e, "cudaEventQuery");
 }
 
+// CUDA graphs for launch-bound sequences (e.g. many small elementwise ops):
+// capture everything enqueued on `stream` between begin and end, replay it
+// with one launch.
+int tpg_graph_begin(tpg_stream stream) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  TPG_CUDA_CHECK(cudaStreamBeginCapture(st->s, cudaStreamCaptureModeThreadLocal));
+  return TPG_OK;
+}
+
+int tpg_graph_end(tpg_stream stream, void** graph_exec) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  cudaGraph_t g = nullptr;
+  TPG_CUDA_CHECK(cudaStreamEndCapture(st->s, &g));
+  cudaGraphExec_t ge = nullptr;
+  cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  *graph_exec = (void*)ge;
+  return TPG_OK;
+}
+
+int tpg_graph_launch(void* graph_exec, tpg_stream stream) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  TPG_CUDA_CHECK(cudaGraphLaunch((cudaGraphExec_t)graph_exec, st->s));
+  return TPG_OK;
+}
+
+int tpg_graph_destroy(void* graph_exec) {
+  if (graph_exec) TPG_CUDA_CHECK(cudaGraphExecDestroy((cudaGraphExec_t)graph_exec));
+  return TPG_OK;
+}
+
 int tpg_flags_clear(int device) {
   if (device < 0 || device >= g_ndev) return arg_fail("bad device index");
   TPG_CUDA_CHECK(cudaSetDevice(device));

@@ -1016,6 +1016,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
                 L.tpg_free(dev, tmp.value, st.handle)
         return h
 
-    ref_dispatch.override_op("core", "cpu", "copy", cpu_copy_wrapper)
+    rt.cpu_copy_restore = ref_dispatch.override_op("core", "cpu", "copy", cpu_copy_wrapper)
+    rt.cpu_copy_wrapper = cpu_copy_wrapper
     register.runtime = rt
     return devs

@@ -50,7 +50,13 @@ __global__ void __launch_bounds__(256, MINB)
   uint4 xb[PF][NLD];
   float yr[PF][8];
   auto tile_of = [&](int w, int& ti, int& tj) {
-    if (ORDER == 0) { ti = w % nti; tj = w / nti; } else { tj = w % ntj; ti = w / ntj; }
+    if (ORDER == 0) { ti = w % nti; tj = w / nti; }
+    else if (ORDER == 1) { tj = w % ntj; ti = w / ntj; }
+    else {  // grouped raster: ORDER consecutive i-tiles, then the next j-tile
+      const int g = w / (ORDER * ntj), r = w % (ORDER * ntj);
+      ti = g * ORDER + r % ORDER;
+      tj = r / ORDER;
+    }
   };
   auto load = [&](int w, int s) {
     int ti, tj;
@@ -814,6 +820,17 @@ int main(int argc, char** argv) {
          true)
   PERSIST(64, 64, 5, 0, 1, 5);
   PERSIST(64, 64, 5, 1, 1, 5);
+  PERSIST(64, 64, 5, 4, 1, 5);
+  PERSIST(64, 64, 5, 8, 1, 5);
+  PERSIST(64, 64, 5, 16, 1, 5);
+  PERSIST(64, 64, 5, 32, 1, 5);
+  ONESHOT(64, 64, 8, 8);
+  ONESHOT(64, 64, 8, 16);
+  ONESHOT(64, 64, 8, 32);
+  PERSIST(64, 128, 3, 8, 1, 3);
+  PERSIST(64, 128, 3, 16, 1, 3);
+  PERSIST(128, 64, 3, 8, 1, 3);
+  PERSIST(128, 64, 3, 16, 1, 3);
   PERSIST(64, 64, 4, 0, 2, 4);
   PERSIST(64, 64, 6, 0, 1, 6);
   PERSIST(64, 64, 8, 0, 1, 8);

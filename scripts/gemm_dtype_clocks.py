@@ -42,6 +42,13 @@ cases = [("f16 uniform(-1,1)", f16(base_a), f16(base_b), tp.half),
          ("f16 multiples of 1/64", f16(np.round(base_a * 64) / 64), f16(np.round(base_b * 64) / 64),
           tp.half)]
 
+# batched 64 x 2048^3 f16 (cfg4 batched): 4x the output bytes per flop of 8192^3
+bb = 64
+ba = rng.uniform(-1, 1, (2048, 2048, bb)).astype(np.float16)
+bbm = rng.uniform(-1, 1, (2048, 2048, bb)).astype(np.float16)
+BA, BB = (tp.from_numpy(np.asfortranarray(x), dev) for x in (ba, bbm))
+del ba, bbm
+
 samples = []
 
 
@@ -77,6 +84,19 @@ for name, A, B, dt in cases:
     t1 = time.time()
     res.append((name, t0, t1, 2 * m ** 3 * n / (t1 - t0) / 1e12))
     time.sleep(0.3)
+BC = tp.tensor_create((2048, 2048, bb), tp.half, dev)
+for _ in range(3):
+    tp.matmul_batched(BA, BB, dest=BC)
+dev.synchronize()
+t0 = time.time()
+n = 0
+while time.time() - t0 < 3.0:
+    for _ in range(10):
+        tp.matmul_batched(BA, BB, dest=BC)
+    dev.synchronize()
+    n += 10
+t1 = time.time()
+res.append(("batched f16 64 x 2048^3", t0, t1, 2 * 2048 ** 3 * bb * n / (t1 - t0) / 1e12))
 stop.set()
 th.join(timeout=2)
 for name, t0, t1, tf in res:

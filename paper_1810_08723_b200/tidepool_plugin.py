@@ -297,7 +297,7 @@ class _Runtime:
         base = self.bases.get(ptr)
         if base is None:  # one full-capacity ndarray per block, reused on recycling
             base = self.bases[ptr] = _np.ctypeslib.as_array((C.c_ubyte * cap).from_address(ptr))
-        arr = base[:max(nbytes, 1)].view(_DevBytes)
+        arr = base[:nbytes].view(_DevBytes)
         arr._tpg_block = blk
         return arr
 
@@ -432,9 +432,12 @@ class _Runtime:
             for d in list(srcs):
                 self.materialize(d)
 
-    def materialize_device(self, device):
+    def materialize_device(self, device, stream=None):
+        """Launch the pending copies of `device` (recorded on `stream`, or
+        on any stream when None)."""
         with self.lock:
-            todo = [p for p, lz in self.lazy.items() if lz.device == device]
+            todo = [p for p, lz in self.lazy.items()
+                    if lz.device == device and (stream is None or lz.stream is stream)]
         for p in todo:
             self.materialize(p)
 
@@ -442,13 +445,19 @@ class _Runtime:
 class _Lazy:
     """A recorded dtype-converting gpu->gpu copy (ops._dtype_convert)."""
     __slots__ = ("device", "plan", "dst_ptr", "dst_op", "src_ptr", "src_op", "keep", "src_dtype",
-                 "dst_dtype", "src_order")
+                 "dst_dtype", "src_order", "stream")
 
     def launch(self, rt):
-        st = rt.current(self.device)
+        """Launch on the stream the copy entry ran on (the destination
+        storage's stream, where the reference orders its consumers); a
+        consumer on another stream of this thread waits for it."""
+        st = self.stream
         p = rt.abi.make_plan(self.plan.extents, self.plan.strides)
         rt.check(rt.L.tpg_unary(st.handle, 10, C.byref(p), C.byref(self.dst_op),
                                 C.byref(self.src_op), self.src_op.dtype, 0, 0), "copy")
+        cur = getattr(rt.tls, "stream", None)
+        if cur is not None and cur is not st and cur.device.index == self.device:
+            rt.check(rt.L.tpg_stream_wait(cur.handle, st.handle), "stream wait")
 
 
 def register(tidepool_module, count: int | None = None, lib=None):
@@ -501,7 +510,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
                 rt.tls.stream = prev
 
         def sync(self) -> None:
-            rt.materialize_device(self.device.index)
+            rt.materialize_device(self.device.index, self)
             rt.drain(self)
             super().sync()
 
@@ -728,6 +737,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
             return False
         lz = _Lazy()
         lz.device, lz.plan = dev, plan
+        lz.stream = rt.current(dev)
         lz.dst_ptr, lz.src_ptr = dptr, aptr
         lz.dst_op = abi.make_operand(dptr, 0, dd.wire_code, dord == "big")
         lz.src_op = abi.make_operand(aptr, bases[1], da.wire_code, aord == "big")

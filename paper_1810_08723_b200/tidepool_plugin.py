@@ -874,6 +874,60 @@ def register(tidepool_module, count: int | None = None, lib=None):
         cbuf = C.create_string_buffer(bytes(raw), d.size)
         rt.check(L.tpg_scatter_fill(st.handle, pp, arr.size, dptr, cbuf, d.size), "scatter_fill")
 
+    # -- extension entries (reference dispatch.add_op, dispatch.py:111-117) ------
+    def chain_entry(plan, d_buf, store, a_buf, a_unpack, steps, bases):
+        """`ewise_chain`: x <- op_i(x, s_i) for a list of (op, result dtype,
+        scalar value, scalar_first) in ONE pass (tpg_chain), bit-identical to
+        the binary ops one after another."""
+        dd, dord, mode, ctx = _store(store)
+        da, aord = _codec(a_unpack)
+        dptr, aptr = rt.address(d_buf), rt.address(a_buf)
+        st = rt.current(rt.blocks[dptr][0])
+        rt.before_read(aptr)
+        rt.before_write(dptr)
+        n = len(steps)
+        arr = (abi.ChainStep * n)()
+        for i, (op, rdt, value, sfirst) in enumerate(steps):
+            raw = bytearray(16)
+            ref_dtypes.codec(rdt, "little")[1](raw, 0, ref_dtypes.cast_scalar(value, rdt))
+            arr[i].op = abi.BINARY_CODE[op]
+            arr[i].dtype = (dd if i == n - 1 else rdt).wire_code
+            arr[i].compute = ref_dtypes.widen_for_compute(rdt).wire_code
+            arr[i].scalar_first = int(bool(sfirst))
+            arr[i].scalar_dtype = rdt.wire_code
+            for j in range(16):
+                arr[i].scalar[j] = raw[j]
+        temps = _Temps(st)
+        a = _operand(aptr, bases[1], da, aord, temps, plan.extents, plan.strides[1])
+        dop = abi.make_operand(dptr, bases[0], dd.wire_code, dord == "big")
+        p = _plan(plan)
+        args = (st.handle, C.byref(p), C.byref(dop), C.byref(a), n, arr, MODE_CODE[mode])
+        _run(st, mode, ctx, dd, lambda: L.tpg_chain(*args), lambda: L.tpg_chain_check(*args))
+        temps.done()
+
+    def matmul_batched_entry(d_buf, d_base, d_strides, store, a_buf, a_base, a_strides, a_unpack,
+                             b_buf, b_base, b_strides, b_unpack, m, n, k, nb):
+        """`matmul_batched`: nb independent products over the slowest axis
+        (tpg_matmul_batched; tcgen05 for 16-bit operands)."""
+        dd, dord, mode, ctx = _store(store)
+        da, aord = _codec(a_unpack)
+        db, bord = _codec(b_unpack)
+        dptr, aptr, bptr = rt.address(d_buf), rt.address(a_buf), rt.address(b_buf)
+        st = rt.current(rt.blocks[dptr][0])
+        for ptr in (aptr, bptr):
+            rt.before_read(ptr)
+        rt.before_write(dptr)
+        temps = _Temps(st)
+        a = _operand(aptr, a_base, da, aord, temps, (m, k, nb), a_strides)
+        b = _operand(bptr, b_base, db, bord, temps, (k, n, nb), b_strides)
+        dop = abi.make_operand(dptr, d_base, dd.wire_code, dord == "big")
+        ds, as_, bs = ((C.c_int64 * 3)(*x) for x in (d_strides, a_strides, b_strides))
+        comp = ref_dtypes.widen_for_compute(da).wire_code
+        _run(st, mode, ctx, dd, lambda: L.tpg_matmul_batched(
+            st.handle, nb, C.byref(dop), ds, C.byref(a), as_, C.byref(b), bs, m, n, k, comp,
+            MODE_CODE[mode]))
+        temps.done()
+
     table = {}
     for op in abi.BINARY_CODE:
         table[op] = binary(op)
@@ -886,6 +940,8 @@ def register(tidepool_module, count: int | None = None, lib=None):
     table.update(matmul=matmul, fill=fill, arange=arange, byteswap=byteswap, gather=gather,
                  scatter=scatter, scatter_fill=scatter_fill)
     ref_dispatch.register_device_impl("core", "gpu", table)
+    ref_dispatch.add_op("core", "gpu", "ewise_chain", chain_entry)
+    ref_dispatch.add_op("core", "gpu", "matmul_batched", matmul_batched_entry)
 
     n = C.c_int(0)
     L.tpg_device_count(C.byref(n))
@@ -1029,4 +1085,110 @@ def register(tidepool_module, count: int | None = None, lib=None):
     rt.cpu_copy_restore = ref_dispatch.override_op("core", "cpu", "copy", cpu_copy_wrapper)
     rt.cpu_copy_wrapper = cpu_copy_wrapper
     register.runtime = rt
+    _REGISTERED[id(tp)] = (tp, rt)
     return devs
+
+
+# ---------------------------------------------------------------------------
+# extension operators over the reference's own tensors (the reference API
+# has no chain and no batched product; these drive the extension entries
+# through the reference's dispatch, validation and cast machinery)
+# ---------------------------------------------------------------------------
+_REGISTERED: dict = {}
+
+
+def _ref_of(t):
+    import sys
+    root = type(t).__module__.split(".")[0]
+    tp = sys.modules[root]
+    if id(tp) not in _REGISTERED:
+        raise RuntimeError("tidepool_plugin.register() has not been called for this reference")
+    return tp
+
+
+def chain(x, steps, dest=None, mode="standard"):
+    """Fused elementwise chain on a reference tensor:
+    `steps` = [(op, scalar) or (op, scalar, scalar_first), ...]; the result
+    equals running `tidepool.<op>` step by step (each step's result dtype is
+    promote(previous dtype, scalar dtype), ops.py:218-245, and rounds once to
+    it) in ONE pass over memory on the gpu device."""
+    tp = _ref_of(x)
+    dt, tz, ops = tp.dtypes, tp.tensors, tp.ops
+    mode = dt.check_mode(mode)
+    if not isinstance(x, tz.Tensor):
+        raise tp.errors.ShapeError("chain needs a tensor operand")
+    if not steps or len(steps) > 8:
+        raise ValueError("chain takes 1..8 steps")
+    cur, desc = x.dtype, []
+    for step in steps:
+        op, s = step[0], ops.as_operand(step[1])
+        if op not in tp.kernels.BINARY_OPS:
+            raise ValueError(f"unknown binary op {op!r}")
+        if not isinstance(s, tz.Scalar):
+            raise tp.errors.ShapeError("chain steps take scalar operands")
+        nxt = cur if not dt.implicit_casting() else dt.promote(cur, s.dtype)
+        desc.append((op, nxt, s.value, bool(step[2]) if len(step) > 2 else False))
+        cur = nxt
+    if dest is None:
+        dest = tz.tensor_create(x.dims, cur, x.device)
+    else:
+        ops._check_dest(dest, x.dims, x.device, cur, mode)
+    cleanups = []
+    x = ops._resolve_aliasing(x, dest, cleanups, True)
+    plan = tz.canonicalize(dest, x)
+    ctx = dt.CastContext(mode)
+    store = ops._make_store(dest, mode, ctx)
+    unpack, _ = dt.codec(x.dtype, x.byteorder)
+    handle = tp.dispatch.lookup("core", dest.device.type.name, "ewise_chain")
+    ops._sync_other_streams(dest.storage.stream, x)
+    d_buf, a_buf = dest.storage.view(), x.storage.view()
+
+    def run():
+        handle(plan, d_buf, store, a_buf, unpack, desc, (dest.offset, x.offset))
+        ctx.flush()
+
+    dest.storage.stream.submit(run)
+    ops._finish(dest.storage.stream, cleanups)
+    return dest
+
+
+def matmul_batched(a, b, dest=None, mode="standard"):
+    """Batched product over the slowest axis of reference tensors:
+    a (m, k, nb) x b (k, n, nb) -> (m, n, nb); slice i equals
+    `tidepool.matmul(a[:, :, i], b[:, :, i])` (its oracle, at the gemm
+    tolerance for 16-bit operands)."""
+    tp = _ref_of(a)
+    dt, tz, ops = tp.dtypes, tp.tensors, tp.ops
+    mode = dt.check_mode(mode)
+    if a.ndim != 3 or b.ndim != 3:
+        raise tp.errors.ShapeError("matmul_batched needs 3-D (rows, cols, batch) operands")
+    (m, k, nb), (k2, n, nb2) = a.dims, b.dims
+    if (k, nb) != (k2, nb2):
+        raise tp.errors.ShapeError(f"batched dims disagree: {a.dims} x {b.dims}")
+    device = a.device
+    rdtype = dt.promote(a.dtype, b.dtype)
+    if dest is None:
+        dest = tz.tensor_create((m, n, nb), rdtype, device)
+    else:
+        ops._check_dest(dest, (m, n, nb), device, rdtype, mode)
+    a = ops._prepare(a, device, rdtype, mode)
+    b = ops._prepare(b, device, rdtype, mode)
+    cleanups = []
+    a = ops._resolve_aliasing(a, dest, cleanups, False)
+    b = ops._resolve_aliasing(b, dest, cleanups, False)
+    ctx = dt.CastContext(mode)
+    store = ops._make_store(dest, mode, ctx)
+    a_unpack, _ = dt.codec(a.dtype, a.byteorder)
+    b_unpack, _ = dt.codec(b.dtype, b.byteorder)
+    handle = tp.dispatch.lookup("core", device.type.name, "matmul_batched")
+    ops._sync_other_streams(dest.storage.stream, a, b)
+    d_buf, a_buf, b_buf = dest.storage.view(), a.storage.view(), b.storage.view()
+
+    def run():
+        handle(d_buf, dest.offset, dest.strides, store, a_buf, a.offset, a.strides, a_unpack,
+               b_buf, b.offset, b.strides, b_unpack, m, n, k, nb)
+        ctx.flush()
+
+    dest.storage.stream.submit(run)
+    ops._finish(dest.storage.stream, cleanups)
+    return dest

@@ -42,7 +42,8 @@ def _on(tp, gpu, nested, dtype):
 def test_registration_shape(env):
     tp, gpu, fake, rt = env
     assert gpu.name == "gpu0" and tp.devices.by_name("gpu0") is gpu
-    assert len(tp.dispatch.table_stats("core", "gpu")) == 31
+    stats = tp.dispatch.table_stats("core", "gpu")
+    assert len(set(stats) - {"ewise_chain", "matmul_batched"}) == 31   # + 2 extension entries
     assert gpu.properties["device-type"] == "gpu"
 
 
@@ -289,3 +290,49 @@ def _make_env(kind):
     devs = tidepool_plugin.register(tp, count=1, lib=lib)
     _ENVS[kind] = (tp, devs[0], lib, tidepool_plugin.register.runtime)
     return _ENVS[kind]
+
+
+def test_chain_extension_matches_sequential_reference_ops(env):
+    """`tidepool_plugin.chain` (the `ewise_chain` extension entry, added with
+    the reference's dispatch.add_op) equals the reference's own ops run one
+    after another, byte for byte, on the cpu device and on gpu0."""
+    tp, gpu, fake, rt = env
+    from paper_1810_08723_b200 import tidepool_plugin as plug
+    rng = random.Random(17)
+    cases = [
+        (tp.float, [round(rng.uniform(-1e3, 1e3), 4) for _ in range(257)],
+         [("multiply", tp.Scalar(1.5, tp.float)), ("add", tp.Scalar(-2.0, tp.float))]),
+        (tp.int16, [rng.randint(-30000, 30000) for _ in range(129)],
+         [("multiply", 3), ("subtract", tp.Scalar(7, tp.int16), True)]),
+        (tp.double, [rng.uniform(-5, 5) for _ in range(64)],
+         [("divide", 3.0), ("maximum", 0.25), ("minimum", 1.0)]),
+    ]
+    for dt, vals, steps in cases:
+        x = tp.from_nested(vals, dt)
+        want = x
+        for st in steps:
+            s = st[1]
+            want = getattr(tp, st[0])(s, want) if len(st) > 2 and st[2] else \
+                getattr(tp, st[0])(want, s)
+        got = plug.chain(tp.cast(x, device=gpu), steps)
+        assert got.dtype is want.dtype, (dt, got.dtype, want.dtype)
+        assert got.storage.snapshot() == want.storage.snapshot(), dt
+
+
+def test_matmul_batched_extension_matches_reference_slices(env):
+    tp, gpu, fake, rt = env
+    from paper_1810_08723_b200 import tidepool_plugin as plug
+    rng = random.Random(5)
+    m, k, n, nb = 6, 5, 4, 3
+    a = tp.tensor_create((m, k, nb), tp.double)
+    b = tp.tensor_create((k, n, nb), tp.double)
+    _fill(tp, a, [rng.uniform(-1, 1) for _ in range(m * k * nb)])
+    _fill(tp, b, [rng.uniform(-1, 1) for _ in range(k * n * nb)])
+    got = plug.matmul_batched(tp.cast(a, device=gpu), tp.cast(b, device=gpu))
+    assert got.dims == (m, n, nb) and got.device is gpu
+    for q in range(nb):
+        want = tp.matmul(tp.apply_index(a, (slice(None), slice(None), q)),
+                         tp.apply_index(b, (slice(None), slice(None), q)))
+        gq = tp.apply_index(got, (slice(None), slice(None), q))
+        assert all(_eq(x, y, 1e-12) for x, y in zip(tp.tensors.read_values(gq),
+                                                   tp.tensors.read_values(want))), q

@@ -159,6 +159,10 @@ int tpg_free_managed(void* ptr);
 int tpg_event_create_untimed(tpg_event* ev);
 int tpg_event_query(tpg_event ev);
 
+/* Peer access between all visible device pairs that support it (NVLink /
+ * NVSwitch); *enabled = number of (a, b) pairs enabled. */
+int tpg_enable_peer_all(int* enabled);
+
 /* CUDA graphs: capture the work enqueued on `stream` between begin and end
  * (thread-local capture mode), replay it with one launch. */
 int tpg_graph_begin(tpg_stream stream);

@@ -110,6 +110,7 @@ PROTOTYPES = {
     "tpg_event_create_untimed": (_i32, [P(_vp)]),
     "tpg_event_query": (_i32, [_vp]),
     "tpg_l2_flush": (_i32, [_vp, C.c_size_t, _vp]),
+    "tpg_enable_peer_all": (_i32, [P(C.c_int)]),
     "tpg_graph_begin": (_i32, [_vp]),
     "tpg_graph_end": (_i32, [_vp, P(_vp)]),
     "tpg_graph_launch": (_i32, [_vp, _vp]),

@@ -493,6 +493,33 @@ int tpg_event_query(tpg_event ev) {
   return cuda_fail(e, "cudaEventQuery");
 }
 
+// Peer access between every pair of visible devices (NVLink / NVSwitch):
+// cross-device copies and kernels reading a peer's memory go over the link
+// directly.  Pairs that cannot peer are skipped; returns the number of
+// pairs enabled in *enabled.
+int tpg_enable_peer_all(int* enabled) {
+  int rc = tpg_init();
+  if (rc) return rc;
+  int n = 0;
+  for (int a = 0; a < g_ndev; ++a) {
+    for (int b = 0; b < g_ndev; ++b) {
+      if (a == b) continue;
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, a, b) != cudaSuccess || !can) continue;
+      TPG_CUDA_CHECK(cudaSetDevice(a));
+      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        e = cudaSuccess;
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+      ++n;
+    }
+  }
+  if (enabled) *enabled = n;
+  return TPG_OK;
+}
+
 // CUDA graphs for launch-bound sequences (e.g. many small elementwise ops):
 // capture everything enqueued on `stream` between begin and end, replay it
 // with one launch.

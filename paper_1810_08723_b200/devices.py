@@ -146,6 +146,9 @@ def configure(count: int | None = None) -> None:
         n = min(n, count)
     _devices.clear()
     _devices.extend(GpuDevice(i) for i in range(n))
+    if n > 1:  # cross-device transfers and peer reads go over NVLink directly
+        import ctypes as C
+        _native.check(_native.lib().tpg_enable_peer_all(C.byref(C.c_int(0))), "peer access")
 
 
 def list_devices() -> list:

@@ -948,6 +948,8 @@ def register(tidepool_module, count: int | None = None, lib=None):
     n = n.value if count is None else min(n.value, count)
     devs = [GpuDevice(i) for i in range(n)]
     rt.devices = {d.index: d for d in devs}
+    if n > 1 and hasattr(L, "tpg_enable_peer_all"):
+        rt.check(L.tpg_enable_peer_all(C.byref(C.c_int(0))), "peer access")
     ref_devices._devices.extend(devs)
 
     # the registry is rebuilt by configure(); keep the gpu devices in it

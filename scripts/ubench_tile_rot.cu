@@ -519,6 +519,54 @@ __global__ void __launch_bounds__(256) k_tread3(const int16_t* __restrict__ X,
   }
 }
 
+// the full cfg2 op (k_tile_hi shape) with an L2 sector-promotion hint on
+// the X loads: PROMO 0 = ld.global.cs, 1 = L2::128B, 2 = L2::256B; ORD as k_var
+__device__ __forceinline__ uint4 ld_promo(const void* p, int promo) {
+  uint4 v;
+  if (promo == 2)
+    asm volatile("ld.global.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  else if (promo == 1)
+    asm volatile("ld.global.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  else
+    v = __ldcs((const uint4*)p);
+  return v;
+}
+template <int PROMO, int ORD>
+__global__ void __launch_bounds__(256, 8) k_tile_promo(const int16_t* __restrict__ X,
+                                                       const float* __restrict__ R,
+                                                       float* __restrict__ out) {
+  __shared__ __align__(16) float sm[64][64];
+  const int w = blockIdx.x;
+  const int ti = ORD == 0 ? w % 64 : w / 64, tj = ORD == 0 ? w / 64 : w % 64;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane % 8, r0 = warp * 4 + lane / 8;
+  const int swz1 = (c * 4) & 31;
+  uint4 v[2];
+#pragma unroll
+  for (int l = 0; l < 2; ++l)
+    v[l] = ld_promo((const uint4*)(X + (size_t)(N - 1 - (ti * 64 + r0 + l * 32)) * N + tj * 64) + c, PROMO);
+  float y[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) y[k] = __ldg(R + tj * 64 + c * 8 + k);
+#pragma unroll
+  for (int l = 0; l < 2; ++l) {
+    const int16_t* e = (const int16_t*)&v[l];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sm[c * 8 + k][(r0 + l * 32) ^ swz1] = (float)e[k] + y[k];
+  }
+  __syncthreads();
+  const int ig = threadIdx.x % 16;
+#pragma unroll
+  for (int pass = 0; pass < 4; ++pass) {
+    const int j = threadIdx.x / 16 + 16 * pass;
+    const int swz = ((j / 8) * 4) & 31;
+    const float4 f = *(const float4*)&sm[j][(ig * 4) ^ swz];
+    __stcs((float4*)(out + (size_t)(tj * 64 + j) * N + ti * 64 + ig * 4), f);
+  }
+}
+
 // the full cfg2 op with 8-B loads: a warp instruction reads 2 X segments
 // (16 lanes x 8 B = 128 B each), all 4 loads of a thread issued first;
 // smem [j][i ^ s(j)], s(j) = ((j >> 2) & 7) * 4 keeps float4 groups intact
@@ -708,6 +756,12 @@ int main(int argc, char** argv) {
 #define WSHAPE(SEG, NC)                                                                        \
   timeit("write shape " #SEG " rows x " #NC " cols per block",                                 \
          [&](int r, int*) { k_wshape<SEG, NC><<<4096, 256>>>(X[r], O[r]); }, false)
+  timeit("promo cs ord0", [&](int r, int*) { k_tile_promo<0, 0><<<4096, 256>>>(X[r], R, O[r]); }, true);
+  timeit("promo 128B ord0", [&](int r, int*) { k_tile_promo<1, 0><<<4096, 256>>>(X[r], R, O[r]); }, true);
+  timeit("promo 256B ord0", [&](int r, int*) { k_tile_promo<2, 0><<<4096, 256>>>(X[r], R, O[r]); }, true);
+  timeit("promo cs ord1", [&](int r, int*) { k_tile_promo<0, 1><<<4096, 256>>>(X[r], R, O[r]); }, true);
+  timeit("promo 128B ord1", [&](int r, int*) { k_tile_promo<1, 1><<<4096, 256>>>(X[r], R, O[r]); }, true);
+  timeit("promo 256B ord1", [&](int r, int*) { k_tile_promo<2, 1><<<4096, 256>>>(X[r], R, O[r]); }, true);
   timeit("k_tile8 full op, 8-B loads, minb8", [&](int r, int*) { k_tile8<8><<<4096, 256>>>(X[r], R, O[r]); }, true);
   timeit("k_tile8 full op, 8-B loads, minb6", [&](int r, int*) { k_tile8<6><<<4096, 256>>>(X[r], R, O[r]); }, true);
   timeit("k_tile8 full op, 8-B loads, minb4", [&](int r, int*) { k_tile8<4><<<4096, 256>>>(X[r], R, O[r]); }, true);

@@ -786,7 +786,9 @@ def sharded_extras(tp, dev, L, dist, steps=5, warmup=3):
             step()
         stream.sync()
         dist.barrier()
-        ms = timed_steps(L, stream, step, steps, None, gate=False)
+        # steps enqueued behind the device gate: the events time the device
+        # work (local kernel + finish), not the host's Python issue
+        ms = timed_steps(L, stream, step, steps, None, gate=True)
         dist.barrier()
         return dist.max(statistics.median(ms))
 
@@ -809,6 +811,35 @@ def sharded_extras(tp, dev, L, dist, steps=5, warmup=3):
                 "checked": "exact" if op == "maximum" else "rel 1e-12 vs numpy", "ok": bool(ok)}
     except Exception as exc:  # pragma: no cover - reported, not fatal
         res["cfg3_sharded_error"] = repr(exc)[:200]
+    # the same finish over NVLink peer memory (tpg_p2p_*: one exchange
+    # kernel after the local reduction, no NCCL)
+    try:
+        from paper_1810_08723_b200.sharded import P2pComm
+
+        def share_all(h):
+            if dist.world == 1:
+                return [h]
+            out = [None] * dist.world
+            tdist.all_gather_object(out, h)
+            return out
+        p2p = P2pComm(dev, dist.rank, dist.world, share_all)
+        n = 8192
+        cols = np.random.default_rng(5).random((n, n))
+        S = Sharded.from_numpy(cols, dist.rank, dist.world, dev, axis=1)
+        want = {"sum": cols.sum(), "maximum": cols.max(), "norm": np.sqrt((cols * cols).sum())}
+        del cols
+        for op in ("sum", "maximum", "norm"):
+            box = {}
+            m = timed(lambda op=op, box=box: box.__setitem__("r", S.reduce_full_tensor(op, p2p)))
+            got = box["r"].item()
+            ok = got == want[op] if op == "maximum" else abs(got - want[op]) <= 1e-12 * want[op]
+            res[f"cfg3_{op}_full_f64_8192^2_sharded_{dist.world}gpu_p2p"] = {
+                "ms": round(m, 4), "GB/s": round(n * n * 8 / m / 1e6, 1),
+                "checked": "exact" if op == "maximum" else "rel 1e-12 vs numpy", "ok": bool(ok)}
+        p2p.check()
+        p2p.close()
+    except Exception as exc:  # pragma: no cover
+        res["cfg3_p2p_error"] = repr(exc)[:200]
     try:
         lo, hi = shard_bounds(1 << 30, dist.world, dist.rank)
         per = hi - lo

@@ -285,6 +285,21 @@ int tpg_nccl_destroy(void);
 /* communicator size and this process's rank, as NCCL sees them */
 int tpg_nccl_info(int* nranks, int* rank);
 
+/* Sharded-reduction finish over NVLink peer memory, no NCCL:
+ * init exports this rank's mailbox as a 64-byte IPC handle; connect opens
+ * every peer's mailbox from the world's handles (world x 64 bytes, rank
+ * order); allreduce enqueues ONE exchange kernel on `stream` that combines
+ * the `count` (<= 2) payload elements of every rank in rank order, in place
+ * (dtype double / int64 / uint64 / uint8 / bool; op 0 sum, 1 prod, 2 max,
+ * 3 min; `epoch` increases by one per call, identically on every rank).  A
+ * peer that never arrives (~4 s) sets bit 31 of the status word. */
+#define TPG_FLAG_P2P_TIMEOUT 0x80000000u
+int tpg_p2p_init(int device, int rank, int world, void* handle64);
+int tpg_p2p_connect(const void* handles);
+int tpg_p2p_allreduce(tpg_stream stream, void* payload, int count, int dtype, int op,
+                      unsigned long long epoch);
+int tpg_p2p_destroy(void);
+
 /* Sharded min/max finish: pack a rank's local extreme
  * (payload slot 0: double for float sources, kind 0; int64 for signed
  * integers, kind 1; uint64 bits for unsigned, kind 2) into an order key

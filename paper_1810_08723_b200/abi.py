@@ -139,6 +139,10 @@ PROTOTYPES = {
     "tpg_nccl_allreduce": (_i32, [_vp, _vp, _i64, C.c_int, C.c_int]),
     "tpg_nccl_destroy": (_i32, []),
     "tpg_nccl_info": (_i32, [P(C.c_int), P(C.c_int)]),
+    "tpg_p2p_init": (_i32, [C.c_int, C.c_int, C.c_int, _vp]),
+    "tpg_p2p_connect": (_i32, [_vp]),
+    "tpg_p2p_allreduce": (_i32, [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_ulonglong]),
+    "tpg_p2p_destroy": (_i32, []),
     "tpg_shard_pack": (_i32, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_int, C.c_int]),
     "tpg_shard_unpack": (_i32, [_vp, C.c_int, C.c_int, _vp]),
 }

@@ -105,6 +105,46 @@ class NcclComm:
         _native.lib().tpg_nccl_destroy()
 
 
+class P2pComm:
+    """The device finish over NVLink peer memory instead of NCCL
+    (tpg_p2p_*): every rank's payload is stored straight into every peer's
+    mailbox (CUDA IPC mappings) by ONE exchange kernel enqueued after the
+    local reduction, which then combines the world's payloads in rank order
+    (deterministic).  `share_all(bytes) -> [bytes per rank]` is any
+    all-gather (e.g. torch.distributed.all_gather_object)."""
+
+    def __init__(self, device, rank: int, world: int, share_all):
+        L = _native.lib()
+        h = (C.c_char * 64)()
+        _native.check(L.tpg_p2p_init(device.index, rank, world, h), "p2p init")
+        handles = share_all(bytes(h))
+        if len(handles) != world or any(len(x) != 64 for x in handles):
+            raise ValueError("p2p: share_all must return one 64-byte handle per rank")
+        blob = b"".join(handles)
+        _native.check(L.tpg_p2p_connect(blob), "p2p connect")
+        self.device, self.rank, self.world = device, rank, world
+        self.epoch = 0
+
+    def allreduce_device(self, ptr: int, count: int, op: int, stream, dtype: int = 11) -> None:
+        self.epoch += 1
+        _native.check(_native.lib().tpg_p2p_allreduce(stream.handle, ptr, count, dtype, op,
+                                                      self.epoch), "p2p allreduce")
+
+    def check(self) -> None:
+        """Raise if an exchange timed out waiting for a peer (status bit 31)."""
+        f = C.c_uint32(0)
+        _native.check(_native.lib().tpg_flags_get(self.device.index, C.byref(f)), "flags")
+        if f.value & 0x80000000:
+            _native.lib().tpg_flags_clear(self.device.index)
+            raise RuntimeError("p2p all-reduce: a peer never arrived (timeout)")
+
+    def info(self) -> dict:
+        return {"nranks": self.world, "rank": self.rank, "transport": "nvlink peer memory"}
+
+    def close(self):
+        _native.lib().tpg_p2p_destroy()
+
+
 # ---------------------------------------------------------------------------
 # combining local partials (pure host logic, tested with gloo on CPU)
 # ---------------------------------------------------------------------------

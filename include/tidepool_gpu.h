@@ -299,6 +299,13 @@ int tpg_p2p_connect(const void* handles);
 int tpg_p2p_allreduce(tpg_stream stream, void* payload, int count, int dtype, int op,
                       unsigned long long epoch);
 int tpg_p2p_destroy(void);
+/* The full sum of a unit-stride f32 / f64 range with the cross-rank finish
+ * FUSED into the reduction kernel: its final block exchanges the rank's
+ * double-double partial with every peer's mailbox and merges the world's in
+ * rank order -- one kernel for compute + collective (d: the 0-dim result).
+ * TPG_E_UNSUPPORTED, nothing launched, for other layouts. */
+int tpg_reduce_sum_p2p(tpg_stream stream, const tpg_plan* outer, const tpg_plan* inner,
+                       const tpg_operand* d, const tpg_operand* a, unsigned long long epoch);
 
 /* Sharded min/max finish: pack a rank's local extreme
  * (payload slot 0: double for float sources, kind 0; int64 for signed

@@ -35,6 +35,16 @@ Stream* resolve_stream(tpg_stream s);
 int sm_count(int device);
 uint32_t* device_flags(int device);  // device-resident sticky status word
 
+// peer-memory mailboxes (tpg_p2p.cu): Slot[2 parities][P2P_MAX_RANKS] per rank
+constexpr int P2P_MAX_RANKS = 64;
+struct alignas(32) P2pSlot {
+  uint64_t payload[2];
+  unsigned long long epoch;
+  uint64_t pad;
+};
+// device array of every rank's mailbox (nullptr when not connected)
+P2pSlot** p2p_boxes(int* rank, int* world);
+
 #define TPG_CUDA_CHECK(expr)                                 \
   do {                                                       \
     cudaError_t _e = (expr);                                 \

@@ -27,12 +27,7 @@
 
 namespace tpg {
 
-constexpr int P2P_MAX_RANKS = 64;
-struct alignas(32) Slot {
-  uint64_t payload[2];
-  unsigned long long epoch;
-  uint64_t pad;
-};
+typedef P2pSlot Slot;
 // mailbox layout: Slot[2][P2P_MAX_RANKS]
 constexpr size_t P2P_MAILBOX = sizeof(Slot) * 2 * P2P_MAX_RANKS;
 
@@ -43,6 +38,12 @@ struct P2pState {
   Slot** dev_boxes = nullptr;           // device array: mailbox of every rank
 };
 static P2pState g_p2p;
+
+P2pSlot** p2p_boxes(int* rank, int* world) {
+  *rank = g_p2p.rank;
+  *world = g_p2p.world;
+  return g_p2p.dev_boxes;
+}
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

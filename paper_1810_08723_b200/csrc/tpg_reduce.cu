@@ -21,10 +21,18 @@ __global__ void k_red_empty(RedParams p) {
 
 using namespace tpg;
 
+// thread-local request for the fused peer-memory finish, consumed by the
+// next reduce launch on this thread (tpg_reduce_sum_p2p)
+static thread_local P2pSlot** tl_p2p = nullptr;
+static thread_local int tl_p2p_rank = 0, tl_p2p_world = 0;
+static thread_local unsigned long long tl_p2p_epoch = 0;
+
 extern "C" int tpg_reduce(tpg_stream stream, int op, double pnorm, const tpg_plan* outer,
                           const tpg_plan* inner, const tpg_operand* d, const tpg_operand* a,
                           int compute, int mode) {
   (void)compute;
+  P2pSlot** const want_p2p = tl_p2p;
+  tl_p2p = nullptr;
   Stream* st = resolve_stream(stream);
   if (!st) return arg_fail("no stream");
   if (!outer || !inner || !d || !a || !d->base || !a->base) return arg_fail("reduce: null argument");
@@ -77,6 +85,21 @@ extern "C" int tpg_reduce(tpg_stream stream, int op, double pnorm, const tpg_pla
   p.track = mode == TPG_WARNING || mode == TPG_ERROR;
   p.p = pnorm;
   p.flags = device_flags(st->device);
+  if (want_p2p) {
+    // the fused finish lives in the block-granularity row kernel's final
+    // block: require exactly the layout that selects it (full reduction of
+    // a unit-stride, aligned, native-order f32 / f64 range)
+    const int es = dt_size(p.sdt);
+    if (op != TPG_RSUM || p.O != 1 || p.ndi != 1 || p.si[0] != es || p.sswap || !p.saligned ||
+        (p.sdt != TPG_DOUBLE && p.sdt != TPG_FLOAT) || p.N == 0) {
+      set_error("reduce_sum_p2p: source layout not eligible for the fused finish");
+      return TPG_E_UNSUPPORTED;
+    }
+    p.p2p = want_p2p;
+    p.p2p_rank = tl_p2p_rank;
+    p.p2p_world = tl_p2p_world;
+    p.p2p_epoch = tl_p2p_epoch;
+  }
   const int kind = dt_kind(p.sdt);
   if (p.N == 0) {
     if (op == TPG_RMIN || op == TPG_RMAX) return arg_fail("min/max of an empty range");
@@ -114,4 +137,25 @@ extern "C" int tpg_reduce(tpg_stream stream, int op, double pnorm, const tpg_pla
     case TPG_RMAX: return reduce_minmax(op, p, st, col, kind);
     default: return reduce_other(op, p, st, col, kind);
   }
+}
+
+// Full sum of a unit-stride f32 / f64 range with the cross-rank finish fused
+// into the reduction kernel (its final block stores the rank's double-double
+// partial into every peer's mailbox over NVLink, waits for the world's and
+// merges them in rank order): ONE kernel for compute + collective.  The
+// peers must be connected (tpg_p2p_connect); `epoch` as tpg_p2p_allreduce.
+// Returns TPG_E_UNSUPPORTED (nothing launched) for other layouts.
+extern "C" int tpg_reduce_sum_p2p(tpg_stream stream, const tpg_plan* outer,
+                                  const tpg_plan* inner, const tpg_operand* d,
+                                  const tpg_operand* a, unsigned long long epoch) {
+  int rank = 0, world = 0;
+  P2pSlot** boxes = p2p_boxes(&rank, &world);
+  if (!boxes) return arg_fail("reduce_sum_p2p: peers not connected (tpg_p2p_connect)");
+  tl_p2p = boxes;
+  tl_p2p_rank = rank;
+  tl_p2p_world = world;
+  tl_p2p_epoch = epoch;
+  const int rc = tpg_reduce(stream, TPG_RSUM, 2.0, outer, inner, d, a, TPG_DOUBLE, TPG_STANDARD);
+  tl_p2p = nullptr;
+  return rc;
 }

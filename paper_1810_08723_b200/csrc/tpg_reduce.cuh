@@ -51,6 +51,11 @@ struct RedParams {
   uint32_t* flags;
   int64_t O, N, C, chunk;
   Acc* ws;
+  // fused peer-memory finish of a full sum (tpg_reduce_sum_p2p): mailboxes
+  // of every rank, or nullptr
+  P2pSlot** p2p;
+  int p2p_rank, p2p_world;
+  unsigned long long p2p_epoch;
 };
 
 __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
@@ -963,6 +968,48 @@ __global__ void __launch_bounds__(256, 2) k_red_rows_wv(RedParams p, Part* ws, u
   if (st) atomicOr(p.flags, st);
 }
 
+// The cross-rank finish of a full sum inside the reduction kernel (called by
+// the one thread that holds the rank's final double-double partial): store
+// (hi, lo) into every rank's mailbox slot [parity][my rank] over NVLink,
+// publish the epoch (system-scope release), wait for every rank's slot in
+// this rank's mailbox (acquire, bounded), merge them IN RANK ORDER in
+// double-double.  Bit 31 of the status word marks a peer that never came.
+__device__ __forceinline__ Part p2p_exchange_sum(const RedParams& p, Part mine) {
+  const unsigned long long ep = p.p2p_epoch;
+  const int par = (int)(ep & 1);
+  for (int q = 0; q < p.p2p_world; ++q) {
+    P2pSlot* dst = p.p2p[q] + par * P2P_MAX_RANKS + p.p2p_rank;
+    ((volatile uint64_t*)dst->payload)[0] = (uint64_t)__double_as_longlong(mine.hi);
+    ((volatile uint64_t*)dst->payload)[1] = (uint64_t)__double_as_longlong(mine.lo);
+  }
+  __threadfence_system();
+  for (int q = 0; q < p.p2p_world; ++q) {
+    P2pSlot* dst = p.p2p[q] + par * P2P_MAX_RANKS + p.p2p_rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&dst->epoch), "l"(ep) : "memory");
+  }
+  const P2pSlot* box = p.p2p[p.p2p_rank] + par * P2P_MAX_RANKS;
+  Part acc;
+  for (int q = 0; q < p.p2p_world; ++q) {
+    const long long t0 = clock64();
+    unsigned long long e;
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(e) : "l"(&box[q].epoch) : "memory");
+      if (e >= ep) break;
+      if (clock64() - t0 > (1ll << 33)) {
+        atomicOr(p.flags, 0x80000000u);
+        break;
+      }
+      __nanosleep(64);
+    } while (true);
+    Part y;
+    y.hi = __longlong_as_double((long long)((const volatile uint64_t*)box[q].payload)[0]);
+    y.lo = __longlong_as_double((long long)((const volatile uint64_t*)box[q].payload)[1]);
+    if (q == 0) acc = y;
+    else dd_merge(acc.hi, acc.lo, y.hi, y.lo);
+  }
+  return acc;
+}
+
 // Row mode, block granularity: one block per (output, chunk) (few outputs,
 // e.g. full reductions).
 template <int OP, typename T>
@@ -985,7 +1032,12 @@ __global__ void __launch_bounds__(256, 2) k_red_rows_v(RedParams p, Part* ws, ui
     stream_range<OP, T, NT, NA, U>(x, p.sbase + soff, j0, j1, tid, p.p);
     const Part r = block_part<OP, NT>(fold_accs<OP, NA>(x, j0), sh);
     if (p.C == 1) {
-      if (tid == 0) acc_store<OP, K_FLT>(p, part_acc<OP>(r), doff, st);
+      if (tid == 0) {
+        Part f = r;
+        if constexpr (OP == TPG_RSUM)
+          if (p.p2p) f = p2p_exchange_sum(p, f);
+        acc_store<OP, K_FLT>(p, part_acc<OP>(f), doff, st);
+      }
       continue;
     }
     if (tid == 0) {
@@ -1000,8 +1052,10 @@ __global__ void __launch_bounds__(256, 2) k_red_rows_v(RedParams p, Part* ws, ui
       Part y = part_none<OP>();
       for (int64_t cc = tid * per; cc < min(p.C, (tid + 1) * per); ++cc)
         y = part_comb<OP>(y, ld_part(&ws[o * p.C + cc]));
-      const Part z = block_part<OP, NT>(y, sh);
+      Part z = block_part<OP, NT>(y, sh);
       if (tid == 0) {
+        if constexpr (OP == TPG_RSUM)
+          if (p.p2p) z = p2p_exchange_sum(p, z);
         acc_store<OP, K_FLT>(p, part_acc<OP>(z), doff, st);
         cnt[o] = 0;
       }

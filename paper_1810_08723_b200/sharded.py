@@ -234,6 +234,11 @@ class Sharded:
         if op == "norm" and p != 2.0:
             raise ValueError("device-finished norm supports p = 2 (use reduce_full)")
         has = t.nelem > 0
+        if (op == "sum" and isinstance(comm, P2pComm) and src in (dtypes.FLOAT, dtypes.DOUBLE)
+                and self.dims[self.axis] >= self.world):
+            fused = self._sum_fused_p2p(comm)
+            if fused is not None:
+                return fused
         rdtype = (dtypes.BOOL if op in ("any", "all") else
                   (dtypes.real_counterpart(src) if src.is_float else dtypes.DOUBLE)
                   if op == "norm" else src)
@@ -280,6 +285,40 @@ class Sharded:
                 ops.square_root(slot0, dest=slot0)
             out = tz.tensor_create((), rdtype, t.device)
             ops.copy(slot0, out)
+        return out
+
+    def _sum_fused_p2p(self, comm):
+        """ONE kernel for compute + collective (tpg_reduce_sum_p2p): the
+        local single-pass sum's final block exchanges the rank's
+        double-double partial with every peer's mailbox over NVLink and
+        merges the world's in rank order.  Every rank takes this path for
+        the same global layout (f32 / f64, no empty slab), so all ranks
+        agree bit for bit.  None when the local layout is not eligible."""
+        from . import abi, dtypes, ops
+        from . import tensors as tz
+        from .plan import build_plan
+        t = self.local
+        dst = tz.tensor_create((), dtypes.DOUBLE, t.device)
+        st = dst.storage.stream
+        t.storage.order(st)
+        outer = build_plan((), [(), ()])
+        inner = build_plan(t.dims, [t.strides])
+        d = abi.make_operand(dst.storage.ptr, dst.offset, dtypes.DOUBLE.code, False)
+        a = abi.make_operand(t.storage.ptr, t.offset, t.dtype.code, t.byteorder == "big")
+        comm.epoch += 1
+        rc = _native.lib().tpg_reduce_sum_p2p(st.handle, C.byref(outer.to_c()),
+                                              C.byref(inner.to_c()), C.byref(d), C.byref(a),
+                                              comm.epoch)
+        if rc == -4:  # not eligible: nothing launched
+            comm.epoch -= 1
+            return None
+        _native.check(rc, "reduce_sum_p2p")
+        t.storage.note_use(st)
+        if t.dtype is dtypes.DOUBLE:
+            return dst
+        out = tz.tensor_create((), t.dtype, t.device)
+        with _implicit():
+            ops.copy(dst, out)
         return out
 
     def _reduce_full_host(self, op: str, comm, p: float):

@@ -47,6 +47,11 @@ def test_p2p_world1_matches_single_device():
                     continue
                 g, w = S.reduce_full_tensor(op, comm).item(), tp.reduce(op, T).item()
                 assert _same(g, w), (name, op, g, w)
+        # the f32 / f64 full sums took the fused single-kernel path
+        x = np.random.default_rng(3).standard_normal(100_000)
+        fused = Sharded.from_numpy(x, 0, 1, tp.gpu(0))._sum_fused_p2p(comm)
+        assert fused is not None
+        assert fused.item() == pytest.approx(tp.reduce("sum", tp.from_numpy(x)).item(), rel=1e-12)
         comm.check()
         assert comm.info()["nranks"] == 1
     finally:
@@ -74,6 +79,9 @@ def _worker(rank, world, port, q):
                 if x.dtype.kind == "u" and op == "norm":
                     continue
                 res[(name, op)] = S.reduce_full_tensor(op, comm).item()
+        x = np.random.default_rng(3).standard_normal(100_001)
+        f = Sh.from_numpy(x, rank, world, tpw.gpu(0))._sum_fused_p2p(comm)
+        res["fused_sum"] = None if f is None else f.item()
         comm.check()
         comm.close()
         q.put((rank, res))
@@ -98,6 +106,10 @@ def test_p2p_world2_two_processes_one_gpu():
         p.join(timeout=120)
     for r in (0, 1):
         assert isinstance(res[r], dict), res[r]
+    xs = np.random.default_rng(3).standard_normal(100_001)
+    want = tp.reduce("sum", tp.from_numpy(xs)).item()
+    assert res[0]["fused_sum"] == res[1]["fused_sum"]          # ranks agree bit for bit
+    assert res[0]["fused_sum"] == pytest.approx(want, rel=1e-12)
     for name, x in _cases():
         T = tp.from_numpy(x)
         for op in OPS:

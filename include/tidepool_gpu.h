@@ -306,6 +306,9 @@ int tpg_p2p_destroy(void);
  * TPG_E_UNSUPPORTED, nothing launched, for other layouts. */
 int tpg_reduce_sum_p2p(tpg_stream stream, const tpg_plan* outer, const tpg_plan* inner,
                        const tpg_operand* d, const tpg_operand* a, unsigned long long epoch);
+/* the same for the 2-norm: ranks exchange sum |x|^2, one root at the end */
+int tpg_reduce_norm2_p2p(tpg_stream stream, const tpg_plan* outer, const tpg_plan* inner,
+                         const tpg_operand* d, const tpg_operand* a, unsigned long long epoch);
 
 /* Sharded min/max finish: pack a rank's local extreme
  * (payload slot 0: double for float sources, kind 0; int64 for signed

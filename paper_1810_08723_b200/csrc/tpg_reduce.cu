@@ -90,7 +90,7 @@ extern "C" int tpg_reduce(tpg_stream stream, int op, double pnorm, const tpg_pla
     // block: require exactly the layout that selects it (full reduction of
     // a unit-stride, aligned, native-order f32 / f64 range)
     const int es = dt_size(p.sdt);
-    if (op != TPG_RSUM || p.O != 1 || p.ndi != 1 || p.si[0] != es || p.sswap || !p.saligned ||
+    if ((op != TPG_RSUM && !(op == TPG_RNORM && pnorm == 2.0)) || p.O != 1 || p.ndi != 1 || p.si[0] != es || p.sswap || !p.saligned ||
         (p.sdt != TPG_DOUBLE && p.sdt != TPG_FLOAT) || p.N == 0) {
       set_error("reduce_sum_p2p: source layout not eligible for the fused finish");
       return TPG_E_UNSUPPORTED;
@@ -145,9 +145,8 @@ extern "C" int tpg_reduce(tpg_stream stream, int op, double pnorm, const tpg_pla
 // merges them in rank order): ONE kernel for compute + collective.  The
 // peers must be connected (tpg_p2p_connect); `epoch` as tpg_p2p_allreduce.
 // Returns TPG_E_UNSUPPORTED (nothing launched) for other layouts.
-extern "C" int tpg_reduce_sum_p2p(tpg_stream stream, const tpg_plan* outer,
-                                  const tpg_plan* inner, const tpg_operand* d,
-                                  const tpg_operand* a, unsigned long long epoch) {
+static int reduce_p2p(tpg_stream stream, int op, const tpg_plan* outer, const tpg_plan* inner,
+                      const tpg_operand* d, const tpg_operand* a, unsigned long long epoch) {
   int rank = 0, world = 0;
   P2pSlot** boxes = p2p_boxes(&rank, &world);
   if (!boxes) return arg_fail("reduce_sum_p2p: peers not connected (tpg_p2p_connect)");
@@ -155,7 +154,21 @@ extern "C" int tpg_reduce_sum_p2p(tpg_stream stream, const tpg_plan* outer,
   tl_p2p_rank = rank;
   tl_p2p_world = world;
   tl_p2p_epoch = epoch;
-  const int rc = tpg_reduce(stream, TPG_RSUM, 2.0, outer, inner, d, a, TPG_DOUBLE, TPG_STANDARD);
+  const int rc = tpg_reduce(stream, op, 2.0, outer, inner, d, a, TPG_DOUBLE, TPG_STANDARD);
   tl_p2p = nullptr;
   return rc;
+}
+
+extern "C" int tpg_reduce_sum_p2p(tpg_stream stream, const tpg_plan* outer,
+                                  const tpg_plan* inner, const tpg_operand* d,
+                                  const tpg_operand* a, unsigned long long epoch) {
+  return reduce_p2p(stream, TPG_RSUM, outer, inner, d, a, epoch);
+}
+
+// the 2-norm with the same fused finish: ranks exchange sum |x|^2 in
+// double-double, the root is taken once on the merged total
+extern "C" int tpg_reduce_norm2_p2p(tpg_stream stream, const tpg_plan* outer,
+                                    const tpg_plan* inner, const tpg_operand* d,
+                                    const tpg_operand* a, unsigned long long epoch) {
+  return reduce_p2p(stream, TPG_RNORM, outer, inner, d, a, epoch);
 }

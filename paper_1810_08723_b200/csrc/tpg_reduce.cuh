@@ -1034,7 +1034,7 @@ __global__ void __launch_bounds__(256, 2) k_red_rows_v(RedParams p, Part* ws, ui
     if (p.C == 1) {
       if (tid == 0) {
         Part f = r;
-        if constexpr (OP == TPG_RSUM)
+        if constexpr (OP == TPG_RSUM || OP == TPG_RNORM)
           if (p.p2p) f = p2p_exchange_sum(p, f);
         acc_store<OP, K_FLT>(p, part_acc<OP>(f), doff, st);
       }
@@ -1054,7 +1054,7 @@ __global__ void __launch_bounds__(256, 2) k_red_rows_v(RedParams p, Part* ws, ui
         y = part_comb<OP>(y, ld_part(&ws[o * p.C + cc]));
       Part z = block_part<OP, NT>(y, sh);
       if (tid == 0) {
-        if constexpr (OP == TPG_RSUM)
+        if constexpr (OP == TPG_RSUM || OP == TPG_RNORM)
           if (p.p2p) z = p2p_exchange_sum(p, z);
         acc_store<OP, K_FLT>(p, part_acc<OP>(z), doff, st);
         cnt[o] = 0;

@@ -234,9 +234,9 @@ class Sharded:
         if op == "norm" and p != 2.0:
             raise ValueError("device-finished norm supports p = 2 (use reduce_full)")
         has = t.nelem > 0
-        if (op == "sum" and isinstance(comm, P2pComm) and src in (dtypes.FLOAT, dtypes.DOUBLE)
-                and self.dims[self.axis] >= self.world):
-            fused = self._sum_fused_p2p(comm)
+        if (op in ("sum", "norm") and isinstance(comm, P2pComm)
+                and src in (dtypes.FLOAT, dtypes.DOUBLE) and self.dims[self.axis] >= self.world):
+            fused = self._sum_fused_p2p(comm, op)
             if fused is not None:
                 return fused
         rdtype = (dtypes.BOOL if op in ("any", "all") else
@@ -287,7 +287,7 @@ class Sharded:
             ops.copy(slot0, out)
         return out
 
-    def _sum_fused_p2p(self, comm):
+    def _sum_fused_p2p(self, comm, op="sum"):
         """ONE kernel for compute + collective (tpg_reduce_sum_p2p): the
         local single-pass sum's final block exchanges the rank's
         double-double partial with every peer's mailbox over NVLink and
@@ -306,9 +306,10 @@ class Sharded:
         d = abi.make_operand(dst.storage.ptr, dst.offset, dtypes.DOUBLE.code, False)
         a = abi.make_operand(t.storage.ptr, t.offset, t.dtype.code, t.byteorder == "big")
         comm.epoch += 1
-        rc = _native.lib().tpg_reduce_sum_p2p(st.handle, C.byref(outer.to_c()),
-                                              C.byref(inner.to_c()), C.byref(d), C.byref(a),
-                                              comm.epoch)
+        entry = (_native.lib().tpg_reduce_sum_p2p if op == "sum"
+                 else _native.lib().tpg_reduce_norm2_p2p)
+        rc = entry(st.handle, C.byref(outer.to_c()), C.byref(inner.to_c()), C.byref(d),
+                   C.byref(a), comm.epoch)
         if rc == -4:  # not eligible: nothing launched
             comm.epoch -= 1
             return None

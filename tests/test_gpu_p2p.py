@@ -52,6 +52,8 @@ def test_p2p_world1_matches_single_device():
         fused = Sharded.from_numpy(x, 0, 1, tp.gpu(0))._sum_fused_p2p(comm)
         assert fused is not None
         assert fused.item() == pytest.approx(tp.reduce("sum", tp.from_numpy(x)).item(), rel=1e-12)
+        fused = Sharded.from_numpy(x, 0, 1, tp.gpu(0))._sum_fused_p2p(comm, "norm")
+        assert fused.item() == pytest.approx(tp.reduce("norm", tp.from_numpy(x)).item(), rel=1e-12)
         comm.check()
         assert comm.info()["nranks"] == 1
     finally:

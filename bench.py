@@ -79,8 +79,16 @@ class Dist:
         except (OSError, subprocess.TimeoutExpired):
             return self.local
         if n > 0:
-            os.environ["CUDA_VISIBLE_DEVICES"] = str(self.local % n)
-            return self.local % n
+            own = self.local % n
+            if os.environ.get("TPG_BENCH_PEERS_VISIBLE") == "1":
+                # every GPU visible, this rank's first: CUDA IPC can map the
+                # peers' mailboxes (the peer-memory finish); costs a context
+                # per visible GPU in every process
+                order = [own] + [g for g in range(n) if g != own]
+                os.environ["CUDA_VISIBLE_DEVICES"] = ",".join(map(str, order))
+            else:
+                os.environ["CUDA_VISIBLE_DEVICES"] = str(own)
+            return own
         return self.local
 
     def barrier(self):
@@ -961,7 +969,8 @@ def main():
     devs = tp.list_devices()
     if not devs:
         raise SystemExit("no CUDA device visible")
-    dev = devs[dist.local % len(devs)] if len(devs) > 1 else devs[0]
+    # under torchrun each rank's own GPU is device 0 (see Dist._pin_device)
+    dev = devs[0] if dist.world > 1 else devs[dist.local % len(devs)]
     clocks = Clocks(dist.phys)
     clocks.start()
     dist.barrier()

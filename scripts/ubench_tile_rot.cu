@@ -4,6 +4,7 @@
 // 4 x 100.7 MB > 126 MB L2, one event pair around K launches):
 //   out[i + j*N] = float(X[j + (N-1-i)*N]) + R[j],  N = 4096
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o scripts/ubench_tile_rot scripts/ubench_tile_rot.cu
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -567,6 +568,53 @@ __global__ void __launch_bounds__(256, 8) k_tile_promo(const int16_t* __restrict
   }
 }
 
+// the full cfg2 op, one tile per block, with the float tile written by ONE
+// TMA bulk tensor store (box 64 i x 64 j of the column-major output) from a
+// dense [j][i] staging tile instead of 4 x 16-B st.global per thread
+__global__ void __launch_bounds__(256, 4) k_tile_tmast(const __grid_constant__ CUtensorMap omap,
+                                                       const int16_t* __restrict__ X,
+                                                       const float* __restrict__ R, int ord) {
+  __shared__ __align__(16) float sm[64][64];
+  __shared__ __align__(128) float stg[64][64];
+  const int w = blockIdx.x;
+  const int ti = ord == 0 ? w % 64 : w / 64, tj = ord == 0 ? w / 64 : w % 64;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane % 8, r0 = warp * 4 + lane / 8;
+  const int swz1 = (c * 4) & 31;
+  uint4 v[2];
+#pragma unroll
+  for (int l = 0; l < 2; ++l)
+    v[l] = __ldcs((const uint4*)(X + (size_t)(N - 1 - (ti * 64 + r0 + l * 32)) * N + tj * 64) + c);
+  float y[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) y[k] = __ldg(R + tj * 64 + c * 8 + k);
+#pragma unroll
+  for (int l = 0; l < 2; ++l) {
+    const int16_t* e = (const int16_t*)&v[l];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sm[c * 8 + k][(r0 + l * 32) ^ swz1] = (float)e[k] + y[k];
+  }
+  __syncthreads();
+  const int ig = threadIdx.x % 16;
+#pragma unroll
+  for (int pass = 0; pass < 4; ++pass) {
+    const int j = threadIdx.x / 16 + 16 * pass;
+    const int swz = ((j / 8) * 4) & 31;
+    *(float4*)&stg[j][ig * 4] = *(const float4*)&sm[j][(ig * 4) ^ swz];
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+            (uint64_t)&omap),
+        "r"(ti * 64), "r"(tj * 64), "r"((uint32_t)__cvta_generic_to_shared(&stg[0][0]))
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
 // the full cfg2 op with 8-B loads: a warp instruction reads 2 X segments
 // (16 lanes x 8 B = 128 B each), all 4 loads of a thread issued first;
 // smem [j][i ^ s(j)], s(j) = ((j >> 2) & 7) * 4 keeps float4 groups intact
@@ -756,6 +804,23 @@ int main(int argc, char** argv) {
 #define WSHAPE(SEG, NC)                                                                        \
   timeit("write shape " #SEG " rows x " #NC " cols per block",                                 \
          [&](int r, int*) { k_wshape<SEG, NC><<<4096, 256>>>(X[r], O[r]); }, false)
+  {
+    CUtensorMap maps[ROT];
+    for (int r = 0; r < ROT; ++r) {
+      cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)N};
+      cuuint64_t strides[1] = {(cuuint64_t)N * 4};
+      cuuint32_t box[2] = {64, 64};
+      cuuint32_t estr[2] = {1, 1};
+      CUresult cr = cuTensorMapEncodeTiled(&maps[r], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, O[r], dims,
+                                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                           CU_TENSOR_MAP_SWIZZLE_NONE,
+                                           CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS) { printf("tensor map failed %d\n", (int)cr); return 1; }
+    }
+    timeit("TMA-store tile ord0", [&](int r, int*) { k_tile_tmast<<<4096, 256>>>(maps[r], X[r], R, 0); }, true);
+    timeit("TMA-store tile ord1", [&](int r, int*) { k_tile_tmast<<<4096, 256>>>(maps[r], X[r], R, 1); }, true);
+  }
   timeit("promo cs ord0", [&](int r, int*) { k_tile_promo<0, 0><<<4096, 256>>>(X[r], R, O[r]); }, true);
   timeit("promo 128B ord0", [&](int r, int*) { k_tile_promo<1, 0><<<4096, 256>>>(X[r], R, O[r]); }, true);
   timeit("promo 256B ord0", [&](int r, int*) { k_tile_promo<2, 0><<<4096, 256>>>(X[r], R, O[r]); }, true);

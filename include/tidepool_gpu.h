@@ -306,6 +306,12 @@ int tpg_p2p_destroy(void);
  * TPG_E_UNSUPPORTED, nothing launched, for other layouts. */
 int tpg_reduce_sum_p2p(tpg_stream stream, const tpg_plan* outer, const tpg_plan* inner,
                        const tpg_operand* d, const tpg_operand* a, unsigned long long epoch);
+/* min / max with the fused finish (NaN iff the tensor's first element is
+ * NaN, ties keep the earliest; index_base = global plan index of this
+ * rank's first element, 0 on the rank holding element 0) */
+int tpg_reduce_minmax_p2p(tpg_stream stream, int op, const tpg_plan* outer, const tpg_plan* inner,
+                          const tpg_operand* d, const tpg_operand* a, unsigned long long epoch,
+                          int64_t index_base);
 /* the same for the 2-norm: ranks exchange sum |x|^2, one root at the end */
 int tpg_reduce_norm2_p2p(tpg_stream stream, const tpg_plan* outer, const tpg_plan* inner,
                          const tpg_operand* d, const tpg_operand* a, unsigned long long epoch);

@@ -145,6 +145,8 @@ PROTOTYPES = {
     "tpg_p2p_destroy": (_i32, []),
     "tpg_reduce_sum_p2p": (_i32, [_vp, _PLAN, _PLAN, _OP, _OP, C.c_ulonglong]),
     "tpg_reduce_norm2_p2p": (_i32, [_vp, _PLAN, _PLAN, _OP, _OP, C.c_ulonglong]),
+    "tpg_reduce_minmax_p2p": (_i32, [_vp, C.c_int, _PLAN, _PLAN, _OP, _OP, C.c_ulonglong,
+                                     _i64]),
     "tpg_shard_pack": (_i32, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_int, C.c_int]),
     "tpg_shard_unpack": (_i32, [_vp, C.c_int, C.c_int, _vp]),
 }

@@ -26,6 +26,7 @@ using namespace tpg;
 static thread_local P2pSlot** tl_p2p = nullptr;
 static thread_local int tl_p2p_rank = 0, tl_p2p_world = 0;
 static thread_local unsigned long long tl_p2p_epoch = 0;
+static thread_local int64_t tl_p2p_index_base = 0;
 
 extern "C" int tpg_reduce(tpg_stream stream, int op, double pnorm, const tpg_plan* outer,
                           const tpg_plan* inner, const tpg_operand* d, const tpg_operand* a,
@@ -90,7 +91,8 @@ extern "C" int tpg_reduce(tpg_stream stream, int op, double pnorm, const tpg_pla
     // block: require exactly the layout that selects it (full reduction of
     // a unit-stride, aligned, native-order f32 / f64 range)
     const int es = dt_size(p.sdt);
-    if ((op != TPG_RSUM && !(op == TPG_RNORM && pnorm == 2.0)) || p.O != 1 || p.ndi != 1 || p.si[0] != es || p.sswap || !p.saligned ||
+    if ((op != TPG_RSUM && op != TPG_RMIN && op != TPG_RMAX &&
+         !(op == TPG_RNORM && pnorm == 2.0)) || p.O != 1 || p.ndi != 1 || p.si[0] != es || p.sswap || !p.saligned ||
         (p.sdt != TPG_DOUBLE && p.sdt != TPG_FLOAT) || p.N == 0) {
       set_error("reduce_sum_p2p: source layout not eligible for the fused finish");
       return TPG_E_UNSUPPORTED;
@@ -99,6 +101,7 @@ extern "C" int tpg_reduce(tpg_stream stream, int op, double pnorm, const tpg_pla
     p.p2p_rank = tl_p2p_rank;
     p.p2p_world = tl_p2p_world;
     p.p2p_epoch = tl_p2p_epoch;
+    p.p2p_index_base = tl_p2p_index_base;
   }
   const int kind = dt_kind(p.sdt);
   if (p.N == 0) {
@@ -146,7 +149,8 @@ extern "C" int tpg_reduce(tpg_stream stream, int op, double pnorm, const tpg_pla
 // peers must be connected (tpg_p2p_connect); `epoch` as tpg_p2p_allreduce.
 // Returns TPG_E_UNSUPPORTED (nothing launched) for other layouts.
 static int reduce_p2p(tpg_stream stream, int op, const tpg_plan* outer, const tpg_plan* inner,
-                      const tpg_operand* d, const tpg_operand* a, unsigned long long epoch) {
+                      const tpg_operand* d, const tpg_operand* a, unsigned long long epoch,
+                      double pnorm = 2.0, int64_t index_base = 0) {
   int rank = 0, world = 0;
   P2pSlot** boxes = p2p_boxes(&rank, &world);
   if (!boxes) return arg_fail("reduce_sum_p2p: peers not connected (tpg_p2p_connect)");
@@ -154,7 +158,8 @@ static int reduce_p2p(tpg_stream stream, int op, const tpg_plan* outer, const tp
   tl_p2p_rank = rank;
   tl_p2p_world = world;
   tl_p2p_epoch = epoch;
-  const int rc = tpg_reduce(stream, op, 2.0, outer, inner, d, a, TPG_DOUBLE, TPG_STANDARD);
+  tl_p2p_index_base = index_base;
+  const int rc = tpg_reduce(stream, op, pnorm, outer, inner, d, a, TPG_DOUBLE, TPG_STANDARD);
   tl_p2p = nullptr;
   return rc;
 }
@@ -171,4 +176,18 @@ extern "C" int tpg_reduce_norm2_p2p(tpg_stream stream, const tpg_plan* outer,
                                     const tpg_plan* inner, const tpg_operand* d,
                                     const tpg_operand* a, unsigned long long epoch) {
   return reduce_p2p(stream, TPG_RNORM, outer, inner, d, a, epoch);
+}
+
+// min / max with the fused finish: the reference's rule (NaN iff the
+// tensor's first element is NaN, ties keep the earliest) across ranks --
+// the rank holding element 0 reduces with first-NaN tracking, the others
+// NaN-skipping; partials carry global plan indices (`index_base` = global
+// index of this rank's first element) and merge in rank order.
+extern "C" int tpg_reduce_minmax_p2p(tpg_stream stream, int op, const tpg_plan* outer,
+                                     const tpg_plan* inner, const tpg_operand* d,
+                                     const tpg_operand* a, unsigned long long epoch,
+                                     int64_t index_base) {
+  if (op != TPG_RMIN && op != TPG_RMAX) return arg_fail("reduce_minmax_p2p: op must be min/max");
+  return reduce_p2p(stream, op, outer, inner, d, a, epoch, index_base == 0 ? 1.0 : -1.0,
+                    index_base);
 }

@@ -56,6 +56,7 @@ struct RedParams {
   P2pSlot** p2p;
   int p2p_rank, p2p_world;
   unsigned long long p2p_epoch;
+  int64_t p2p_index_base;  // min / max: global plan index of this rank's element 0
 };
 
 __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
@@ -974,9 +975,15 @@ __global__ void __launch_bounds__(256, 2) k_red_rows_wv(RedParams p, Part* ws, u
 // publish the epoch (system-scope release), wait for every rank's slot in
 // this rank's mailbox (acquire, bounded), merge them IN RANK ORDER in
 // double-double.  Bit 31 of the status word marks a peer that never came.
-__device__ __forceinline__ Part p2p_exchange_sum(const RedParams& p, Part mine) {
+template <int OP>
+__device__ __forceinline__ Part p2p_exchange(const RedParams& p, Part mine) {
   const unsigned long long ep = p.p2p_epoch;
   const int par = (int)(ep & 1);
+  if (OP == TPG_RMIN || OP == TPG_RMAX) {
+    // local plan indices -> global ones, so ties keep the earliest element
+    const long long ix = __double_as_longlong(mine.lo);
+    if (ix >= 0) mine.lo = __longlong_as_double(ix + p.p2p_index_base);
+  }
   for (int q = 0; q < p.p2p_world; ++q) {
     P2pSlot* dst = p.p2p[q] + par * P2P_MAX_RANKS + p.p2p_rank;
     ((volatile uint64_t*)dst->payload)[0] = (uint64_t)__double_as_longlong(mine.hi);
@@ -1004,8 +1011,8 @@ __device__ __forceinline__ Part p2p_exchange_sum(const RedParams& p, Part mine) 
     Part y;
     y.hi = __longlong_as_double((long long)((const volatile uint64_t*)box[q].payload)[0]);
     y.lo = __longlong_as_double((long long)((const volatile uint64_t*)box[q].payload)[1]);
-    if (q == 0) acc = y;
-    else dd_merge(acc.hi, acc.lo, y.hi, y.lo);
+    // rank order: acc covers the earlier elements
+    acc = q == 0 ? y : part_comb<OP>(acc, y);
   }
   return acc;
 }
@@ -1034,8 +1041,7 @@ __global__ void __launch_bounds__(256, 2) k_red_rows_v(RedParams p, Part* ws, ui
     if (p.C == 1) {
       if (tid == 0) {
         Part f = r;
-        if constexpr (OP == TPG_RSUM || OP == TPG_RNORM)
-          if (p.p2p) f = p2p_exchange_sum(p, f);
+        if (p.p2p) f = p2p_exchange<OP>(p, f);
         acc_store<OP, K_FLT>(p, part_acc<OP>(f), doff, st);
       }
       continue;
@@ -1054,8 +1060,7 @@ __global__ void __launch_bounds__(256, 2) k_red_rows_v(RedParams p, Part* ws, ui
         y = part_comb<OP>(y, ld_part(&ws[o * p.C + cc]));
       Part z = block_part<OP, NT>(y, sh);
       if (tid == 0) {
-        if constexpr (OP == TPG_RSUM || OP == TPG_RNORM)
-          if (p.p2p) z = p2p_exchange_sum(p, z);
+        if (p.p2p) z = p2p_exchange<OP>(p, z);
         acc_store<OP, K_FLT>(p, part_acc<OP>(z), doff, st);
         cnt[o] = 0;
       }

@@ -234,8 +234,9 @@ class Sharded:
         if op == "norm" and p != 2.0:
             raise ValueError("device-finished norm supports p = 2 (use reduce_full)")
         has = t.nelem > 0
-        if (op in ("sum", "norm") and isinstance(comm, P2pComm)
-                and src in (dtypes.FLOAT, dtypes.DOUBLE) and self.dims[self.axis] >= self.world):
+        if (op in ("sum", "norm", "minimum", "maximum") and isinstance(comm, P2pComm)
+                and src in (dtypes.FLOAT, dtypes.DOUBLE) and self.dims[self.axis] >= self.world
+                and (op in ("sum", "norm") or self.axis == len(self.dims) - 1)):
             fused = self._sum_fused_p2p(comm, op)
             if fused is not None:
                 return fused
@@ -306,10 +307,16 @@ class Sharded:
         d = abi.make_operand(dst.storage.ptr, dst.offset, dtypes.DOUBLE.code, False)
         a = abi.make_operand(t.storage.ptr, t.offset, t.dtype.code, t.byteorder == "big")
         comm.epoch += 1
-        entry = (_native.lib().tpg_reduce_sum_p2p if op == "sum"
-                 else _native.lib().tpg_reduce_norm2_p2p)
-        rc = entry(st.handle, C.byref(outer.to_c()), C.byref(inner.to_c()), C.byref(d),
-                   C.byref(a), comm.epoch)
+        L = _native.lib()
+        args = (C.byref(outer.to_c()), C.byref(inner.to_c()), C.byref(d), C.byref(a), comm.epoch)
+        if op in ("minimum", "maximum"):
+            # global plan index of this slab's first element (slabs along the
+            # slowest axis of a column-major tensor: a constant offset)
+            base = self.lo * math.prod(self.dims[:-1])
+            rc = L.tpg_reduce_minmax_p2p(st.handle, abi.REDUCE_CODE[op], *args, base)
+        else:
+            entry = L.tpg_reduce_sum_p2p if op == "sum" else L.tpg_reduce_norm2_p2p
+            rc = entry(st.handle, *args)
         if rc == -4:  # not eligible: nothing launched
             comm.epoch -= 1
             return None

@@ -54,6 +54,9 @@ def test_p2p_world1_matches_single_device():
         assert fused.item() == pytest.approx(tp.reduce("sum", tp.from_numpy(x)).item(), rel=1e-12)
         fused = Sharded.from_numpy(x, 0, 1, tp.gpu(0))._sum_fused_p2p(comm, "norm")
         assert fused.item() == pytest.approx(tp.reduce("norm", tp.from_numpy(x)).item(), rel=1e-12)
+        for op in ("minimum", "maximum"):
+            f = Sharded.from_numpy(x, 0, 1, tp.gpu(0))._sum_fused_p2p(comm, op)
+            assert f.item() == tp.reduce(op, tp.from_numpy(x)).item()
         comm.check()
         assert comm.info()["nranks"] == 1
     finally:
@@ -84,6 +87,14 @@ def _worker(rank, world, port, q):
         x = np.random.default_rng(3).standard_normal(100_001)
         f = Sh.from_numpy(x, rank, world, tpw.gpu(0))._sum_fused_p2p(comm)
         res["fused_sum"] = None if f is None else f.item()
+        # min / max: the tie / signed-zero / NaN-first rules across ranks
+        for tag, y in (("ties", np.array([0.0, 1.0, -0.0, 5.0, 5.0, -0.0, 0.0, 5.0])),
+                       ("nan_first", np.array([np.nan, 1.0, 2.0, np.nan, 3.0, 0.5])),
+                       ("nan_rank1", np.array([1.0, 2.0, 0.5, np.nan, 3.0, 0.5])),
+                       ("rand", x)):
+            for op in ("minimum", "maximum"):
+                f = Sh.from_numpy(y, rank, world, tpw.gpu(0))._sum_fused_p2p(comm, op)
+                res[("mm", tag, op)] = None if f is None else f.item()
         comm.check()
         comm.close()
         q.put((rank, res))
@@ -112,6 +123,17 @@ def test_p2p_world2_two_processes_one_gpu():
     want = tp.reduce("sum", tp.from_numpy(xs)).item()
     assert res[0]["fused_sum"] == res[1]["fused_sum"]          # ranks agree bit for bit
     assert res[0]["fused_sum"] == pytest.approx(want, rel=1e-12)
+    for tag, y in (("ties", np.array([0.0, 1.0, -0.0, 5.0, 5.0, -0.0, 0.0, 5.0])),
+                   ("nan_first", np.array([np.nan, 1.0, 2.0, np.nan, 3.0, 0.5])),
+                   ("nan_rank1", np.array([1.0, 2.0, 0.5, np.nan, 3.0, 0.5])),
+                   ("rand", xs)):
+        for op in ("minimum", "maximum"):
+            w = tp.reduce(op, tp.from_numpy(y)).item()
+            for r in (0, 1):
+                g = res[r][("mm", tag, op)]
+                assert g is not None
+                assert (math.isnan(g) and math.isnan(w)) or (g == w and math.copysign(1, g) ==
+                                                             math.copysign(1, w)), (tag, op, r, g, w)
     for name, x in _cases():
         T = tp.from_numpy(x)
         for op in OPS:

@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "tpg_common.cuh"
 #include "tpg_internal.h"
@@ -656,16 +657,23 @@ __global__ void __launch_bounds__(256, sizeof(TX) >= 4 ? 4 : 5) k_tile_f32(EwPar
   }
 }
 
-// k_tile_tma: the same transposing float kernel fed by TMA (SURVEY cfg2,
-// the headline).  The X operand is a 2-D tensor map over its memory order
-// (reversed plan axes are handled by mirrored coordinates and index
-// flips in shared memory); 64 x 64 X tiles stream through an XS-stage
-// shared-memory ring (one mbarrier per stage, thread 0 issues the bulk
-// tensor copies XS-1 tiles ahead), so a block keeps up to XS-1 tiles of
-// loads in flight without registers.  Phase 1 converts a stage into the
-// XOR-swizzled float tile (transposed), the block barrier then frees the
-// stage for the next TMA, phase 2 writes 16-B coalesced columns.
-constexpr int XS = 4;
+// k_tile_tma: the transposing float kernel fed by TMA (SURVEY cfg2, the
+// headline; the default for 2- and 4-byte X).  The X operand is a 2-D
+// tensor map over its memory order (reversed plan axes are handled by
+// mirrored tile coordinates and index flips); each 64 x 64 X tile arrives
+// by TMA (one box per 128 B of a tile row, 128-B swizzle) in an XS-stage
+// shared-memory ring, one mbarrier per stage, thread 0 issuing XS tiles
+// ahead.  There is no float staging tile: lane l of a warp owns output row
+// i0 + l, reads the 16-B chunk of X row i0 + l holding VX adjacent output
+// columns (the swizzle spreads the 8 rows of a 128-B bank window over all
+// banks, so the 32-row column read is conflict free), converts, combines
+// with Y and stores each column as ONE 128-B line per warp instruction
+// (st.global.cs).  Measured against the register-staged k_tile_f32 and
+// 30+ other transposing shapes in scripts/ubench_cfg2_tma.cu /
+// ubench_tile_rot.cu: the fastest steady-state cfg2 kernel found.
+// Y: 0 imm, 1 broadcast along axis 0, 2 unit stride along axis 0;
+// NIN == 1: cast-copy of X.
+constexpr int XS = 6;
 
 __device__ __forceinline__ void tma_mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok = 0;
@@ -681,32 +689,33 @@ __device__ __forceinline__ void tma_mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 template <int OP, int NIN, int XI, typename TX, typename TY>
-__global__ void __launch_bounds__(256) k_tile_tma(const __grid_constant__ CUtensorMap xmap,
+__global__ void __launch_bounds__(256, 4) k_tile_tma(const __grid_constant__ CUtensorMap xmap,
                                                   EwParams p, int q, int nt0, int ntq, int ymode,
                                                   int rev0, int revq) {
   constexpr int SX = sizeof(TX);
-  constexpr int VX = 16 / SX;          // X elements per 16-B chunk
-  constexpr int LPR = TT * SX / 16;    // lanes per tile row (4, 8 or 16)
-  constexpr int RPW = 32 / LPR;        // tile rows per warp pass
-  constexpr int NLD = TT / (8 * RPW);  // 16-B chunks per thread per tile
-  constexpr int SWM = RPW > 4 ? RPW : 4;
+  static_assert(SX == 2 || SX == 4, "128-B swizzled boxes need 2- or 4-byte X");
+  constexpr int VX = 16 / SX;           // X elements per 16-B chunk
+  constexpr int BQ = 128 / SX;          // box width (elements along q)
+  constexpr int NB = TT / BQ;           // boxes per tile
+  constexpr int BOX = TT * 128;         // bytes per box
+  constexpr int STAGE = NB * BOX;       // = TT * TT * SX
+  constexpr int NCH = TT / VX;          // 16-B chunks per tile row
+  static_assert(NCH % 8 == 0, "chunks per warp");
   constexpr int Y = 3 - XI;
-  constexpr int STAGE = TT * TT * SX;
-  extern __shared__ __align__(128) uint8_t tsm[];
-  uint8_t* xring = tsm;                                   // XS stages
-  float(*sm)[TT] = (float(*)[TT])(tsm + XS * STAGE);      // 16 KiB float tile
-  uint64_t* bar = (uint64_t*)(tsm + XS * STAGE + TT * TT * 4);
+  extern __shared__ uint8_t tsm_raw[];
+  uint8_t* xring = (uint8_t*)(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bar = (uint64_t*)(xring + XS * STAGE);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = lane % LPR;
-  const int r0 = warp * RPW + lane / LPR;
   const int nwork = nt0 * ntq;
   const char* ys = NIN >= 2 ? p.base[Y] : nullptr;
   char* ds = p.base[0];
   const int64_t sdq = p.str[0][q];
   const int64_t syq = NIN >= 2 ? p.str[Y][q] : 0;
+  const int64_t sy0 = NIN >= 2 ? p.str[Y][0] : 0;
   float yimm = 0.0f;
   if (NIN >= 2 && ymode == 0) yimm = to_f<TY>(from_bits<TY>(p.imm[Y].lo));
-  // memory-order tile coordinates of work item w
+  // byte step between the VX plan columns of a chunk (memory order)
+  const int64_t dstep = revq ? -sdq : sdq, ystep = revq ? -syq : syq;
   auto issue = [&](int w, int s) {
     const int t0 = w % nt0, tq = w / nt0;
     const int mq = revq ? (ntq - 1 - tq) * TT : tq * TT;
@@ -714,11 +723,14 @@ __global__ void __launch_bounds__(256) k_tile_tma(const __grid_constant__ CUtens
     const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar[s]);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(STAGE)
                  : "memory");
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%2, %3}], [%4];" ::"r"((uint32_t)__cvta_generic_to_shared(xring + s * STAGE)),
-        "l"((uint64_t)&xmap), "r"(mq), "r"(m0), "r"(b)
-        : "memory");
+#pragma unroll
+    for (int k = 0; k < NB; ++k)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+          "[%0], [%1, {%2, %3}], [%4];" ::"r"(
+              (uint32_t)__cvta_generic_to_shared(xring + s * STAGE + k * BOX)),
+          "l"((uint64_t)&xmap), "r"(mq + k * BQ), "r"(m0), "r"(b)
+          : "memory");
   };
   if (threadIdx.x == 0) {
     for (int s = 0; s < XS; ++s)
@@ -730,83 +742,113 @@ __global__ void __launch_bounds__(256) k_tile_tma(const __grid_constant__ CUtens
   __syncthreads();
   if (threadIdx.x == 0) {
     int w = blockIdx.x;
-    for (int s = 0; s < XS - 1 && w < nwork; ++s, w += gridDim.x) issue(w, s);
+    for (int s = 0; s < XS && w < nwork; ++s, w += gridDim.x) issue(w, s);
   }
-  float yr[VX];
-  auto load_y = [&](int w) {
-    if (NIN >= 2 && ymode == 1) {
-      const int tq = w / nt0;
+  // per-thread constants: warp w owns chunks w, w + 8, ... (CPW of them) of
+  // every tile, for both 32-row groups (lane = output row i and i + 32, so
+  // each column address serves two stores, the second at +128 B):
+  // shared-memory offsets of the lane's 16-B chunk rows, and the byte offset
+  // of each chunk's first plan column from the tile origin
+  constexpr int CPW = NCH / 8;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(xring);
+  uint32_t soff[CPW][2];
+  int64_t dofs[CPW], yofs[CPW];
 #pragma unroll
-      for (int k = 0; k < VX; ++k) {
-        const int jj = revq ? TT - 1 - (c * VX + k) : c * VX + k;
-        yr[k] = to_f<TY>(__ldg((const TY*)(ys + (int64_t)(tq * TT + jj) * syq)));
-      }
+  for (int u = 0; u < CPW; ++u) {
+    const int ch = warp + 8 * u;                             // chunk (memory order)
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      const int i = 32 * g + lane;                           // plan row (output fast axis)
+      const int rm = rev0 ? TT - 1 - i : i;                  // memory row in the tile
+      soff[u][g] = (uint32_t)((ch / 8) * BOX + rm * 128 + (((ch % 8) ^ (rm & 7)) << 4));
     }
-  };
-  if ((int)blockIdx.x < nwork) load_y(blockIdx.x);
+    const int jm0 = ch * VX;                                 // memory column of the chunk
+    const int jl = revq ? TT - 1 - jm0 : jm0;                // its plan column in the tile
+    dofs[u] = (int64_t)lane * 4 + jl * sdq;
+    yofs[u] = jl * syq + (ymode == 2 ? (int64_t)lane * sy0 : 0);
+  }
+  // ymode 1 with a float row of unit stride (either sign) along q: each
+  // chunk's VX row values are one aligned 16-32 B run, read as float4s
+  // (chunks cover plan columns 8m .. 8m+7 (VX = 8) or 4m .. 4m+3 (VX = 4))
+  bool yvec = false, yrev = false;
+  if constexpr (NIN >= 2 && std::is_same<TY, float>::value) {
+    yrev = revq != (syq < 0);
+    yvec = ymode == 1 && (syq == 4 || syq == -4) &&
+           (syq > 0 ? (uintptr_t)ys % 16 == 0 : ((uintptr_t)ys + 4) % 16 == 0);
+  }
   int it = 0;
+  // tile coordinates advanced incrementally (no per-tile division)
+  int t0 = (int)blockIdx.x % nt0, tq = (int)blockIdx.x / nt0;
+  const int g0 = (int)gridDim.x % nt0, gq = (int)gridDim.x / nt0;
   for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++it) {
     const int s = it % XS;
-    tma_mbar_wait((uint32_t)__cvta_generic_to_shared(&bar[s]), (it / XS) & 1);
-    // phase 1: stage (memory order) -> float tile [j][i ^ swz] (plan order)
-    const uint8_t* stg = xring + s * STAGE;
-    const int jb = revq ? TT - 1 - c * VX : c * VX;             // plan j of element 0
-    const int swz1 = (((revq ? (TT - 1 - c * VX) : c * VX) / VX) * SWM) & 31;
+    tma_mbar_wait(sbase + XS * STAGE + s * 8, (it / XS) & 1);
+    char* dtile = ds + (int64_t)t0 * TT * 4 + (int64_t)tq * TT * sdq;
+    const char* ytile = nullptr;
+    if (NIN >= 2) ytile = ys + (int64_t)tq * TT * syq + (ymode == 2 ? (int64_t)t0 * TT * sy0 : 0);
 #pragma unroll
-    for (int l = 0; l < NLD; ++l) {
-      const int rm = r0 + l * 8 * RPW;                          // memory row
-      const int i = rev0 ? TT - 1 - rm : rm;
-      const uint4 raw = *(const uint4*)(stg + rm * (TT * SX) + c * 16);
-      const TX* e = (const TX*)&raw;
+    for (int u = 0; u < CPW; ++u) {
+      uint4 raw[2];
+#pragma unroll
+      for (int g = 0; g < 2; ++g)
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(raw[g].x), "=r"(raw[g].y), "=r"(raw[g].z), "=r"(raw[g].w)
+                     : "r"(sbase + s * STAGE + soff[u][g]));
+      char* dp = dtile + dofs[u];
+      float yv[2][VX];
+      if (NIN >= 2) {
+        if (ymode == 0) {
+#pragma unroll
+          for (int k = 0; k < VX; ++k) yv[0][k] = yv[1][k] = yimm;
+        } else if (yvec) {
+          const float* yp = (const float*)(ytile + yofs[u]) - (yrev ? VX - 1 : 0);
+          float t[VX];
+#pragma unroll
+          for (int h = 0; h < VX / 4; ++h) {
+            const float4 f = __ldg((const float4*)yp + h);
+            t[4 * h] = f.x; t[4 * h + 1] = f.y; t[4 * h + 2] = f.z; t[4 * h + 3] = f.w;
+          }
+#pragma unroll
+          for (int k = 0; k < VX; ++k) yv[0][k] = yv[1][k] = t[yrev ? VX - 1 - k : k];
+        } else {
+          const char* yp = ytile + yofs[u];
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            const char* ypg = yp + (ymode == 2 ? g * 32 * sy0 : 0);
+#pragma unroll
+            for (int k = 0; k < VX; ++k) yv[g][k] = to_f<TY>(__ldg((const TY*)(ypg + k * ystep)));
+          }
+        }
+      }
 #pragma unroll
       for (int k = 0; k < VX; ++k) {
-        const float x = to_f<TX>(e[k]);
-        float v = x;
-        if (NIN >= 2 && ymode <= 1) {
-          const float y = ymode == 0 ? yimm : yr[k];
-          v = XI == 1 ? fop<OP>(x, y) : fop<OP>(y, x);
+        float* col = (float*)(dp + k * dstep);
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          const float x = to_f<TX>(((const TX*)&raw[g])[k]);
+          float v = x;
+          if (NIN >= 2) v = XI == 1 ? fop<OP>(x, yv[g][k]) : fop<OP>(yv[g][k], x);
+          __stcs(col + 32 * g, v);
         }
-        sm[revq ? jb - k : jb + k][i ^ swz1] = v;
       }
     }
-    __syncthreads();  // stage s fully read; float tile complete
+    __syncthreads();  // stage s consumed by every warp
     if (threadIdx.x == 0) {
-      const int wn = w + (XS - 1) * gridDim.x;
-      if (wn < nwork) issue(wn, (it + XS - 1) % XS);
+      const int wn = w + XS * gridDim.x;
+      if (wn < nwork) issue(wn, s);
     }
-    const int t0 = w % nt0, tq = w / nt0;
-    if (w + (int)gridDim.x < nwork) load_y(w + gridDim.x);
-    // phase 2: float4 columns -> destination
-    const int ig = threadIdx.x % 16;
-    char* db = ds + (int64_t)(t0 * TT + ig * 4) * 4 + (int64_t)(tq * TT) * sdq;
-#pragma unroll
-    for (int pass = 0; pass < 4; ++pass) {
-      const int j = threadIdx.x / 16 + 16 * pass;
-      const int swz = ((j / VX) * SWM) & 31;
-      float4 f = *(const float4*)&sm[j][(ig * 4) ^ swz];
-      if (NIN >= 2 && ymode == 2) {
-        const int64_t sy0 = p.str[Y][0];
-        const char* yb = ys + (int64_t)(t0 * TT + ig * 4) * sy0 + (int64_t)(tq * TT + j) * syq;
-        float y[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) y[u] = to_f<TY>(__ldg((const TY*)(yb + u * sy0)));
-        if (XI == 1) {
-          f.x = fop<OP>(f.x, y[0]); f.y = fop<OP>(f.y, y[1]);
-          f.z = fop<OP>(f.z, y[2]); f.w = fop<OP>(f.w, y[3]);
-        } else {
-          f.x = fop<OP>(y[0], f.x); f.y = fop<OP>(y[1], f.y);
-          f.z = fop<OP>(y[2], f.z); f.w = fop<OP>(y[3], f.w);
-        }
-      }
-      __stcs((float4*)(db + j * sdq), f);
+    t0 += g0;
+    tq += gq;
+    if (t0 >= nt0) {
+      t0 -= nt0;
+      ++tq;
     }
-    __syncthreads();  // float tile drained before the next phase 1
   }
 }
 
 template <int SX>
 constexpr size_t tile_tma_smem() {
-  return (size_t)XS * TT * TT * SX + TT * TT * 4 + XS * 8 + 128;
+  return (size_t)XS * TT * TT * SX + XS * 8 + 1024;
 }
 
 // TMA launch of the cfg2 pattern: 2-D plan, X unit-stride (+-) along q,
@@ -815,7 +857,7 @@ constexpr size_t tile_tma_smem() {
 template <auto K, typename TX>
 bool launch_tile_tma(EwParams& p, Stream* st, int xi, int q, int64_t nt0, int64_t ntq, int ymode) {
   constexpr int SX = sizeof(TX);
-  if (SX > 4 || p.ndim != 2) return false;
+  if ((SX != 2 && SX != 4) || p.ndim != 2) return false;
   const int64_t sq = p.str[xi][q], s0 = p.str[xi][0];
   if ((sq != SX && sq != -SX) || s0 == 0 || (s0 < 0 ? -s0 : s0) % 16) return false;
   const int64_t eq = p.ext[q], e0 = p.ext[0];
@@ -826,14 +868,14 @@ bool launch_tile_tma(EwParams& p, Stream* st, int xi, int q, int64_t nt0, int64_
   CUtensorMap map;
   cuuint64_t dims[2] = {(cuuint64_t)eq, (cuuint64_t)e0};
   cuuint64_t strides[1] = {(cuuint64_t)(s0 < 0 ? -s0 : s0)};
-  cuuint32_t box[2] = {TT, TT};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / SX), TT};
   cuuint32_t estr[2] = {1, 1};
   const CUtensorMapDataType ty = SX == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                : SX == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
                                          : CU_TENSOR_MAP_DATA_TYPE_UINT32;
   if (enc(&map, ty, 2, const_cast<char*>(lo), dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
   constexpr size_t smem = tile_tma_smem<SX>();
   static int bps = 0;
@@ -853,14 +895,13 @@ bool launch_tile_tma(EwParams& p, Stream* st, int xi, int q, int64_t nt0, int64_
   return true;
 }
 
-// The TMA-fed variant is opt-in (TPG_TILE_TMA=1): measured on B200 at the
-// cfg2 shape it is slower than the register-prefetch k_tile_f32 (22.0 vs
-// 20.9 us per step, bench.py A/B), see DESIGN.md §4.
+// The TMA-fed tile kernel is the default for 2- / 4-byte X (TPG_TILE_TMA=0
+// selects the register-staged k_tile_f32 instead, for A/B runs).
 inline bool tile_tma_disabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("TPG_TILE_TMA");
-    v = (e && e[0] == '1') ? 0 : 1;
+    v = (e && e[0] == '0') ? 1 : 0;
   }
   return v == 1;
 }
@@ -1132,13 +1173,19 @@ int launch_ew(EwParams& p, Stream* st) {
             typedef typename Native<DTA>::T TA;
             typedef typename Native<(NIN >= 2 ? DTB : DTA)>::T TB;
             if (nrest == 1 && !tile_tma_disabled()) {
-              bool ok;
-              if (NIN == 1)
-                ok = launch_tile_tma<k_tile_tma<0, 1, 1, TA, TA>, TA>(p, st, 1, qa, nt0, ntq, 0);
-              else if (x == 1)
-                ok = launch_tile_tma<k_tile_tma<OP, 2, 1, TA, TB>, TA>(p, st, 1, qa, nt0, ntq, ymode);
-              else
-                ok = launch_tile_tma<k_tile_tma<OP, 2, 2, TB, TA>, TB>(p, st, 2, qa, nt0, ntq, ymode);
+              bool ok = false;
+              constexpr bool ta_ok = sizeof(TA) == 2 || sizeof(TA) == 4;
+              constexpr bool tb_ok = sizeof(TB) == 2 || sizeof(TB) == 4;
+              if constexpr (ta_ok) {
+                if (NIN == 1)
+                  ok = launch_tile_tma<k_tile_tma<0, 1, 1, TA, TA>, TA>(p, st, 1, qa, nt0, ntq, 0);
+                else if (x == 1)
+                  ok = launch_tile_tma<k_tile_tma<OP, 2, 1, TA, TB>, TA>(p, st, 1, qa, nt0, ntq, ymode);
+              }
+              if constexpr (tb_ok && NIN >= 2) {
+                if (x == 2)
+                  ok = launch_tile_tma<k_tile_tma<OP, 2, 2, TB, TA>, TB>(p, st, 2, qa, nt0, ntq, ymode);
+              }
               if (ok) {
                 TPG_LAUNCH_CHECK("tile_tma launch");
                 return TPG_OK;

@@ -1,0 +1,76 @@
+"""Where the drop-in's per-op host time goes on the box, without a profiler:
+cfg2 `tidepool.add(V, R)` back to back through the unmodified reference +
+tidepool_plugin, with perf_counter accumulators around the gpu table
+entries and the plugin allocator, and with the kernel launch stubbed.
+Prints us/op for each piece.  (Diagnostic only; not product code.)"""
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+import bench  # noqa: E402
+import ref_loader  # noqa: E402
+from paper_1810_08723_b200 import tidepool_plugin  # noqa: E402
+
+lib = None
+if "--fake" in sys.argv:
+    from fake_native import FakeNative
+    from oracle import oracle
+    lib = FakeNative(oracle.lib())
+    lib.tpg_binary = lambda *a: 0
+tp = ref_loader.load("tidepool")
+gpu = tidepool_plugin.register(tp, count=1, lib=lib)[0]
+rt = tidepool_plugin.register.runtime
+N = bench.N if lib is None else 64
+X = tp.tensor_create((N, N), tp.int16, gpu)
+R = tp.tensor_create((1, N), tp.float, gpu)
+V = tp.apply_index(tp.transpose(X), (slice(None, None, -1), slice(None)))
+st = gpu.default_stream()
+
+
+def wall(n=3000):
+    for _ in range(50):
+        tp.add(V, R)
+    st.sync()
+    t0 = time.perf_counter()
+    for _ in range(n):
+        tp.add(V, R)
+    st.sync()
+    return 1e6 * (time.perf_counter() - t0) / n
+
+
+print(f"wall                         {wall():7.2f} us/op")
+acc = {}
+
+
+def timed(name, f):
+    def g(*a, **k):
+        t0 = time.perf_counter_ns()
+        try:
+            return f(*a, **k)
+        finally:
+            acc[name] = acc.get(name, 0) + time.perf_counter_ns() - t0
+    return g
+
+
+restores = []
+for op in ("add", "copy"):
+    restores.append(tp.dispatch.override_op("core", "gpu", op, lambda f, op=op: timed(op, f)))
+orig_alloc, orig_rel = rt.allocate, rt._release
+rt.allocate = timed("allocate", orig_alloc)
+rt._release = timed("release", orig_rel)
+n = 3000
+w = wall(n)
+print(f"wall (instrumented)          {w:7.2f} us/op")
+for k, v in acc.items():
+    print(f"  {k:26s} {v / 1e3 / (n + 50):7.2f} us/op")
+for r in restores:
+    r()
+rt.allocate, rt._release = orig_alloc, orig_rel
+L = rt.L
+real = L.tpg_binary
+L.tpg_binary = lambda *a: 0
+print(f"wall, tpg_binary stubbed     {wall():7.2f} us/op")
+L.tpg_binary = real
+print(f"reference floor              {1e3 * bench._pipeline_floor(2000):7.2f} us/op")

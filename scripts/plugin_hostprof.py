@@ -31,4 +31,31 @@ st.sync()
 print(f"plugin wall {1e6 * (time.perf_counter() - t0) / n:.1f} us/op")
 print(f"reference floor {1e3 * bench._pipeline_floor(2000):.1f} us/op")
 cProfile.run("for _ in range(2000): tp.add(V, R)", "/tmp/hp")
-pstats.Stats("/tmp/hp").sort_stats("tottime").print_stats(25)
+pstats.Stats("/tmp/hp").sort_stats("tottime").print_stats(40)
+
+# raw per-call costs of the C-ABI calls one plugin op makes
+import ctypes as C  # noqa: E402
+rt = tidepool_plugin.register.runtime
+L = rt.L
+
+
+def per_call(label, f, n=20000):
+    f()
+    t0 = time.perf_counter()
+    for _ in range(n):
+        f()
+    print(f"{label:40s} {1e6 * (time.perf_counter() - t0) / n:7.2f} us")
+
+
+ev = rt._new_event()
+L.tpg_event_record(ev, st.handle)
+st.sync()
+per_call("tpg_event_query (completed)", lambda: L.tpg_event_query(ev))
+per_call("tpg_event_record", lambda: L.tpg_event_record(ev, st.handle))
+st.sync()
+f = C.c_uint32(0)
+per_call("tpg_flags_take", lambda: L.tpg_flags_take(st.handle, C.byref(f)), 2000)
+per_call("rt.allocate+release 64 MiB class", lambda: rt.allocate(0, N * N * 4), 5000)
+per_call("ctypes no-arg call (tpg_last_error)", lambda: L.tpg_last_error())
+per_call("tp.tensor_create 4096^2 f32", lambda: tp.tensor_create((N, N), tp.float, gpu), 5000)
+st.sync()

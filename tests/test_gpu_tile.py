@@ -120,20 +120,21 @@ def test_cfg2_full_size_against_numpy():
     assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("tma", ["0", "1"])
+@pytest.mark.parametrize("kern", ["tma", "regs"])
 @pytest.mark.parametrize("d", SRC, ids=[x.name for x in SRC])
-def test_tile_reversals(d, tma, monkeypatch):
-    """Both tile kernels (register prefetch, and the opt-in TMA-fed one that
-    maps reversed plan axes to mirrored tensor-map coordinates): every
-    (axis-0 reversed, unit axis reversed) combination, all three Y modes,
-    against the oracle.  TPG_TILE_TMA is read once per process, so the TMA
-    leg runs in a subprocess."""
-    if tma == "1":
+def test_tile_reversals(d, kern, monkeypatch):
+    """Both tile kernels (the default TMA-fed one, which maps reversed plan
+    axes to mirrored tensor-map coordinates, and the register-staged
+    k_tile_f32 selected by TPG_TILE_TMA=0): every (axis-0 reversed, unit
+    axis reversed) combination, all three Y modes, float rows of either
+    stride sign and alignment, against the oracle.  TPG_TILE_TMA is read once
+    per process, so the register leg runs in a subprocess."""
+    if kern == "regs":
         import subprocess
         import sys
-        env = dict(__import__("os").environ, TPG_TILE_TMA="1")
+        env = dict(__import__("os").environ, TPG_TILE_TMA="0")
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
-                            f"{__file__}::test_tile_reversals[{d.name}-0]"],
+                            f"{__file__}::test_tile_reversals[{d.name}-tma]"],
                            env=env, capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
         return
@@ -152,5 +153,10 @@ def test_tile_reversals(d, tma, monkeypatch):
                 tp.subtract(v, col)
                 tp.add(v, tp.Scalar(2.5, tp.float))
                 tp.cast(v, tp.float)
-    assert so.calls >= 20
+                # row read backwards (negative stride), and a row whose start
+                # is not 16-B aligned
+                wide = tp.from_numpy(np.asfortranarray(_arr(rng, D.FLOAT, (1, 193))))
+                tp.add(v, tp.apply_index(wide, (slice(None), slice(192, 0, -1))))
+                tp.maximum(tp.apply_index(wide, (slice(None), slice(1, None))), v)
+    assert so.calls >= 28
     assert not so.failures, so.failures[:3]

@@ -1006,7 +1006,9 @@ def main():
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                          "peak_kind": peak_kind, "traffic": traffic,
-                         "kernel": "tpg::k_tile_f32<add, i16 -> f32, f32 row> (fused cast + broadcast add)"},
+                         "kernel": ("tpg::k_tile_f32<add, i16 -> f32, f32 row> (register-staged; TPG_TILE_TMA=0)"
+                                    if os.environ.get("TPG_TILE_TMA") == "0" else
+                                    "tpg::k_tile_tma<add, i16 -> f32, f32 row> (TMA-fed, fused cast + broadcast add)")},
             "e2e": {"value": round(e2e_val, 2), "unit": "GB/s",
                     "h2d_bytes_per_step": r2["h2d"], "d2h_bytes_per_step": r2["d2h"],
                     "ms_per_step": round(e2e_total / len(e2e_ms), 3),

@@ -66,7 +66,26 @@ def build_library(verbose: bool = False, jobs: int | None = None) -> Path:
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
+    build_pyext(verbose)
     return LIB
+
+
+def build_pyext(verbose: bool = False) -> Path:
+    """The drop-in plugin's CPython host fast path (hostsrc/tpg_pyfast.c):
+    plain C against the interpreter's headers, no CUDA, no link-time
+    dependency on libtidepool_gpu.so (it receives C-ABI function addresses)."""
+    import sysconfig
+    src = PKG / "hostsrc" / "tpg_pyfast.c"
+    out = PKG / ("_tpg_pyfast" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if out.exists() and out.stat().st_mtime >= src.stat().st_mtime:
+        return out
+    cc = os.environ.get("CC", "gcc")
+    cmd = [cc, "-O2", "-shared", "-fPIC", "-Wall", "-Wno-missing-field-initializers",
+           f"-I{sysconfig.get_paths()['include']}", str(src), "-o", str(out)]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    return out
 
 
 def build_oracle(verbose: bool = False) -> Path:

@@ -863,20 +863,41 @@ bool launch_tile_tma(EwParams& p, Stream* st, int xi, int q, int64_t nt0, int64_
   const int64_t eq = p.ext[q], e0 = p.ext[0];
   const char* lo = p.base[xi] + (sq < 0 ? (eq - 1) * sq : 0) + (s0 < 0 ? (e0 - 1) * s0 : 0);
   if ((uintptr_t)lo % 16) return false;
-  auto enc = (PFN_cuTensorMapEncodeTiled_v12000)tensor_map_encoder();
-  if (!enc) return false;
-  CUtensorMap map;
-  cuuint64_t dims[2] = {(cuuint64_t)eq, (cuuint64_t)e0};
-  cuuint64_t strides[1] = {(cuuint64_t)(s0 < 0 ? -s0 : s0)};
-  cuuint32_t box[2] = {(cuuint32_t)(128 / SX), TT};
-  cuuint32_t estr[2] = {1, 1};
-  const CUtensorMapDataType ty = SX == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
-                               : SX == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
-                                         : CU_TENSOR_MAP_DATA_TYPE_UINT32;
-  if (enc(&map, ty, 2, const_cast<char*>(lo), dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return false;
+  // encoded maps are reused across launches over the same X layout (a
+  // small per-thread cache: the host cost of an op is part of its e2e time)
+  struct MapCache {
+    const char* lo;
+    int64_t eq, e0, s0;
+    CUtensorMap map;
+  };
+  static thread_local MapCache cache[8];
+  static thread_local unsigned next = 0;
+  const int64_t s0a = s0 < 0 ? -s0 : s0;
+  const CUtensorMap* mp = nullptr;
+  for (auto& c : cache)
+    if (c.lo == lo && c.eq == eq && c.e0 == e0 && c.s0 == s0a) mp = &c.map;
+  if (!mp) {
+    auto enc = (PFN_cuTensorMapEncodeTiled_v12000)tensor_map_encoder();
+    if (!enc) return false;
+    MapCache& c = cache[next++ % 8];
+    cuuint64_t dims[2] = {(cuuint64_t)eq, (cuuint64_t)e0};
+    cuuint64_t strides[1] = {(cuuint64_t)s0a};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / SX), TT};
+    cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapDataType ty = SX == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                           : CU_TENSOR_MAP_DATA_TYPE_UINT32;
+    c.lo = nullptr;
+    if (enc(&c.map, ty, 2, const_cast<char*>(lo), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+    c.lo = lo;
+    c.eq = eq;
+    c.e0 = e0;
+    c.s0 = s0a;
+    mp = &c.map;
+  }
+  const CUtensorMap& map = *mp;
   constexpr size_t smem = tile_tma_smem<SX>();
   static int bps = 0;
   if (!bps) {

@@ -72,6 +72,30 @@ def _cells(fn) -> dict:
     return {n: c.cell_contents for n, c in zip(code.co_freevars, fn.__closure__)}
 
 
+_CELL_INDEX: dict = {}  # (code object, free variable names) -> closure indices (-1: absent)
+
+
+def _cells_at(fn, names):
+    """Contents of the named closure cells of `fn` (None when absent); the
+    name -> index mapping is computed once per code object (the reference
+    creates a new store / scalar closure per call, over a handful of code
+    objects)."""
+    try:
+        code, cl = fn.__code__, fn.__closure__
+    except AttributeError:
+        return (None,) * len(names)
+    if cl is None:
+        return (None,) * len(names)
+    idx = _CELL_INDEX.get((code, names))
+    if idx is None:
+        fv = code.co_freevars
+        idx = _CELL_INDEX[(code, names)] = tuple(fv.index(n) if n in fv else -1 for n in names)
+    if len(idx) == 1:
+        i = idx[0]
+        return (cl[i].cell_contents if i >= 0 else None,)
+    return [cl[i].cell_contents if i >= 0 else None for i in idx]
+
+
 def decode_codec(ref_dtypes, fn):
     """(dtype name, byteorder) of a reference codec unpack/pack function."""
     for (d, order), pair in ref_dtypes._CODEC_CACHE.items():
@@ -152,7 +176,23 @@ def _is_dense(extents, strides, size):
     return True
 
 
+_FUSE_MEMO: dict = {}
+
+
 def _fuse_strides(copy_plan, bin_ext, bin_str, a_base, size):
+    """Memoised _fuse_strides_impl (the same copy / binary layouts recur
+    call after call)."""
+    key = (tuple(copy_plan.extents), tuple(map(tuple, copy_plan.strides)), tuple(bin_ext),
+           tuple(bin_str), a_base, size)
+    r = _FUSE_MEMO.get(key, _FUSE_MEMO)
+    if r is _FUSE_MEMO:
+        if len(_FUSE_MEMO) > 4096:
+            _FUSE_MEMO.clear()
+        r = _FUSE_MEMO[key] = _fuse_strides_impl(copy_plan, bin_ext, bin_str, a_base, size)
+    return r
+
+
+def _fuse_strides_impl(copy_plan, bin_ext, bin_str, a_base, size):
     """Re-express a binary operand that reads the (dense) destination of a
     recorded copy as a view of the copy's SOURCE.  Returns (src strides per
     binary axis, src byte offset relative to the copy's source offset) or
@@ -187,34 +227,48 @@ def _fuse_strides(copy_plan, bin_ext, bin_str, a_base, size):
 # ---------------------------------------------------------------------------
 # registration into the reference
 # ---------------------------------------------------------------------------
-class _Block:
-    """One managed allocation behind a gpu storage; returns itself to the
-    device cache when the storage's buffer object is garbage collected."""
-    __slots__ = ("rt", "ptr", "cap", "device", "events", "__weakref__")
-
-    def __init__(self, rt, ptr, cap, device):
-        self.rt, self.ptr, self.cap, self.device = rt, ptr, cap, device
-        self.events = ()
-
-    def __del__(self):
-        try:
-            self.rt._release(self)
-        except Exception:
-            pass
+def _fast_module():
+    """The plugin's C host fast path (hostsrc/tpg_pyfast.c, built in-tree by
+    build.py): managed block cache + storage buffer type."""
+    try:
+        from . import _tpg_pyfast
+    except ImportError as exc:  # built by __graft_entry__.build() / build.py
+        raise ImportError("paper_1810_08723_b200._tpg_pyfast is not built "
+                          "(python -m paper_1810_08723_b200.build)") from exc
+    return _tpg_pyfast
 
 
-import numpy as _np  # noqa: E402
+_DEVBUF = None  # _tpg_pyfast.DevBuf once the first registration loaded it
 
 
-class _DevBytes(_np.ndarray):
-    """Host view of a managed block; carries the block for the pointer
-    registry and its lifetime."""
+def _pool_functions(L):
+    """Addresses of the six C-ABI functions the block pool calls.  For a
+    ctypes library they are the exported symbols; for a duck-typed test
+    double (tests/fake_native.py) they are ctypes callbacks into it."""
+    if isinstance(L, C.CDLL):
+        names = ("tpg_malloc_managed", "tpg_free_managed", "tpg_event_create_untimed",
+                 "tpg_event_record", "tpg_event_query", "tpg_event_sync")
+        return tuple(C.cast(getattr(L, n), C.c_void_p).value for n in names), ()
+    I, P, PP = C.c_int, C.c_void_p, C.POINTER(C.c_void_p)
 
+    def malloc_managed(dev, n, out):
+        v = P()
+        rc = L.tpg_malloc_managed(dev, n, C.byref(v))
+        out[0] = v.value
+        return rc
 
-def _size_class(n: int) -> int:
-    if n <= (1 << 20):
-        return (max(n, 1) + 511) & ~511
-    return (n + (2 << 20) - 1) & ~((2 << 20) - 1)
+    def ev_create(out):
+        v = P()
+        rc = L.tpg_event_create_untimed(C.byref(v))
+        out[0] = v.value
+        return rc
+    cbs = (C.CFUNCTYPE(I, I, C.c_size_t, PP)(malloc_managed),
+           C.CFUNCTYPE(I, P)(lambda p: L.tpg_free_managed(p)),
+           C.CFUNCTYPE(I, PP)(ev_create),
+           C.CFUNCTYPE(I, P, P)(lambda e, st: L.tpg_event_record(e, st)),
+           C.CFUNCTYPE(I, P)(lambda e: L.tpg_event_query(e)),
+           C.CFUNCTYPE(I, P)(lambda e: L.tpg_event_sync(e)))
+    return tuple(C.cast(f, C.c_void_p).value for f in cbs), cbs
 
 
 class _Runtime:
@@ -227,18 +281,22 @@ class _Runtime:
         self.errors = tp.errors
         self.lock = threading.RLock()
         self.tls = threading.local()
-        self.cache: dict = {}         # (device, cap) -> [block ptr + events]
-        self.cached_bytes: dict = {}  # device -> bytes
         self.blocks: dict = {}        # ptr -> (device, cap) of live managed blocks
         self.streams: dict = {}       # device -> [GpuStream] (for free tracking)
         self.lazy: dict = {}          # dst ptr -> _Lazy
         self.lazy_by_src: dict = {}   # src ptr -> {dst ptr}
         self.status_sink = tp.ops._status
-        self.event_pool: list = []
-        self.ev_refs: dict = {}  # shared completion marker -> blocks referencing it
-        self.seq = 0             # launch epoch (bumped whenever an entry resolves its stream)
+        fast = _fast_module()
+        global _DEVBUF
+        _DEVBUF = fast.DevBuf
+        fast.set_allocation_error(tp.errors.AllocationError)
+        fns, self._pool_callbacks = _pool_functions(L)
+        self.pool = fast.BlockPool(fns, self.blocks, self.lazy, self.lazy_by_src,
+                                   self._drop_lazy, self.CACHE_BYTES, self.MAX_PENDING)
+        self.DevBuf = fast.DevBuf
+        self.defaults: dict = {}     # device -> its default GpuStream (rt.current)
+        self.event_pool: list = []   # timing events (profile hook)
         self.plans: dict = {}    # (extents, strides) -> abi.Plan (entries rebuild plans per call)
-        self.bases: dict = {}    # block ptr -> uint8 ndarray over its full capacity
         self.stats = collections.Counter()  # lazy / fused / materialised / transfer paths
         self.profile = None  # [] -> (start, stop) timing events around each standard-mode launch
 
@@ -254,88 +312,19 @@ class _Runtime:
     # -- memory --------------------------------------------------------------
     MAX_PENDING = 8  # per size class: beyond this many in-flight blocks, wait for the oldest
 
-    def _take_cached(self, key):
-        """A cached block of `key` whose last GPU use has completed (host
-        code may write a fresh storage without synchronising, e.g.
-        tensor_from_nested / scalar_tensor, tensors.py:221-243, 269-280), or
-        None.  Never waits while fewer than MAX_PENDING blocks are in flight,
-        so back-to-back ops do not serialise the host on the GPU."""
-        with self.lock:
-            pool = self.cache.get(key)
-            if not pool:
-                return None
-            for i, (ptr, events) in enumerate(pool):
-                if all(self.L.tpg_event_query(ev) == 0 for ev in events):
-                    del pool[i]
-                    break
-            else:
-                if len(pool) < self.MAX_PENDING:
-                    return None
-                ptr, events = pool.pop(0)
-                for ev in events:
-                    self.check(self.L.tpg_event_sync(ev), "event sync")
-            self.cached_bytes[key[0]] -= key[1]
-            self._unref(events)
-            return ptr
-
     def allocate(self, device, nbytes):
-        cap = _size_class(nbytes)
-        ptr = self._take_cached((device, cap))
-        if ptr is None:
-            p = C.c_void_p()
-            rc = self.L.tpg_malloc_managed(device, cap, C.byref(p))
-            if rc == -2:
-                self.trim(device, 0)
-                rc = self.L.tpg_malloc_managed(device, cap, C.byref(p))
-            self.check(rc, f"managed allocation of {nbytes} bytes")
-            ptr = p.value
-        blk = _Block(self, ptr, cap, device)
-        with self.lock:
-            self.blocks[ptr] = (device, cap)
-        # a uint8 ndarray over the block: its memoryview has format "B", so
-        # the reference's struct packing and slice assignment work on it
-        base = self.bases.get(ptr)
-        if base is None:  # one full-capacity ndarray per block, reused on recycling
-            base = self.bases[ptr] = _np.ctypeslib.as_array((C.c_ubyte * cap).from_address(ptr))
-        arr = base[:nbytes].view(_DevBytes)
-        arr._tpg_block = blk
-        return arr
+        """A storage buffer over a managed block (tpg_pyfast.c BlockPool:
+        recycled blocks are handed out only once the GPU work that last
+        used them has completed -- host code may write a fresh storage
+        without synchronising, e.g. tensor_from_nested / scalar_tensor,
+        tensors.py:221-243, 269-280)."""
+        return self.pool.allocate(device, nbytes)
 
-    def _release(self, blk):
-        ptr = blk.ptr
-        with self.lock:
-            self.blocks.pop(ptr, None)
+    def _drop_lazy(self, ptr):
+        """Pool callback when a block whose pointer has a pending lazy copy
+        (as destination or source) is freed."""
+        with self.lock:  # (a pending copy keeps its source alive: only dst records die here)
             self._drop_lazy_locked(ptr)
-        events = []
-        for st in self.streams.get(blk.device, ()):
-            # one completion marker per stream per launch epoch: blocks
-            # released with no launch in between share it
-            if st.marker is None or st.marker_seq != self.seq:
-                ev = self.event_pool.pop() if self.event_pool else self._new_event()
-                self.L.tpg_event_record(ev, st.handle)
-                st.marker, st.marker_seq = ev, self.seq
-                self.ev_refs[ev] = 0
-            self.ev_refs[st.marker] += 1
-            events.append(st.marker)
-        with self.lock:
-            self.cache.setdefault((blk.device, blk.cap), []).append((ptr, events))
-            self.cached_bytes[blk.device] = self.cached_bytes.get(blk.device, 0) + blk.cap
-            over = self.cached_bytes[blk.device] > self.CACHE_BYTES
-        if over:
-            self.trim(blk.device, self.CACHE_BYTES // 2)
-
-    def _unref(self, events):
-        for ev in events:
-            n = self.ev_refs.get(ev, 1) - 1
-            if n > 0:
-                self.ev_refs[ev] = n
-                continue
-            self.ev_refs.pop(ev, None)
-            for sts in self.streams.values():
-                for st in sts:
-                    if st.marker == ev:
-                        st.marker = None
-            self.event_pool.append(ev)
 
     def _new_timing_event(self):
         ev = C.c_void_p()
@@ -349,30 +338,15 @@ class _Runtime:
 
     def trim(self, device, keep_bytes):
         """Free cached blocks of `device` until at most keep_bytes remain."""
-        with self.lock:
-            victims = []
-            for key in list(self.cache):
-                if key[0] != device:
-                    continue
-                pool = self.cache[key]
-                while pool and self.cached_bytes.get(device, 0) > keep_bytes:
-                    victims.append(pool.pop(0))
-                    self.cached_bytes[device] -= key[1]
-        for ptr, events in victims:
-            for ev in events:
-                self.L.tpg_event_sync(ev)
-            self._unref(events)
-            self.bases.pop(ptr, None)
-            self.L.tpg_free_managed(C.c_void_p(ptr))
+        self.pool.trim(device, keep_bytes)
 
     # -- pointers --------------------------------------------------------------
     @staticmethod
     def address(mv):
         """Raw address of a storage memoryview (read-only views included)."""
         obj = mv.obj
-        blk = getattr(obj, "_tpg_block", None)
-        if blk is not None:
-            return blk.ptr
+        if type(obj) is _DEVBUF:
+            return obj.ptr
         if len(mv) == 0:
             return 0
         import numpy as np
@@ -383,11 +357,14 @@ class _Runtime:
 
     # -- streams ----------------------------------------------------------------
     def current(self, device):
-        self.seq += 1
+        self.pool.bump()  # a new launch epoch for the blocks' completion markers
         st = getattr(self.tls, "stream", None)
         if st is not None and st.device.index == device:
             return st
-        return self.devices[device].default_stream()
+        st = self.defaults.get(device)
+        if st is None:
+            st = self.defaults[device] = self.devices[device].default_stream()
+        return st
 
     def drain(self, st):
         """Stream-ordered read-and-clear of the device's status word; status
@@ -498,8 +475,8 @@ def register(tidepool_module, count: int | None = None, lib=None):
                 rt.check(L.tpg_stream_create(device.index, C.byref(h)), "stream create")
                 handle = h.value
             self.handle = handle
-            self.marker, self.marker_seq = None, -1
             rt.streams.setdefault(device.index, []).append(self)
+            rt.pool.add_stream(device.index, handle)
 
         def submit(self, task) -> None:
             prev = getattr(rt.tls, "stream", None)
@@ -575,13 +552,14 @@ def register(tidepool_module, count: int | None = None, lib=None):
             d, order = decode_codec(ref_dtypes, fn)
             return ref_dtypes.by_name(d), order
 
+    _STORE_CELLS = ("pack", "mode", "ctx")
+
     def _store(store):
-        cells = _cells(store)
-        pack = cells.get("pack")
+        pack, mode, ctx = _cells_at(store, _STORE_CELLS)
         if pack is None:
             raise errors.DeviceError("gpu table: unrecognised store closure")
         d, order = _codec(pack)
-        return d, order, cells.get("mode", "standard"), cells.get("ctx")
+        return d, order, mode if mode is not None else "standard", ctx
 
     def _operand(ptr, base, d, order, temps, extents=None, strides=None):
         """tpg_operand for a storage pointer; host memory is staged."""
@@ -644,10 +622,21 @@ def register(tidepool_module, count: int | None = None, lib=None):
             elif mode == "error":
                 raise errors.DomainError(_loss_message(to))
 
+    _STATUS_CELL = ("status",)
+
     def _sink(fn):
-        s = decode_status(fn)
-        if s is not None:
+        s = _cells_at(fn, _STATUS_CELL)[0]
+        if isinstance(s, set):
             rt.status_sink = s
+
+    compute_code = {}
+
+    def _compute(d):
+        """wire code of widen_for_compute(d) (memoised per dtype)."""
+        c = compute_code.get(d)
+        if c is None:
+            c = compute_code[d] = ref_dtypes.widen_for_compute(d).wire_code
+        return c
 
     # -- entries (SURVEY §8b signatures) -------------------------------------------
     def binary(op):
@@ -661,7 +650,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
             dev = rt.blocks[dptr][0]
             st = rt.current(dev)
             _sink(fn)
-            compute = ref_dtypes.widen_for_compute(da).wire_code
+            compute = _compute(da)
             temps = _Temps(st)
             ops, strides = [], [list(plan.strides[0])]
             for ptr, d, order, base, v in ((aptr, da, aord, bases[1], 1),
@@ -717,7 +706,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
             if op == "identity":
                 comp, fc = da.wire_code, 0
             else:
-                comp = ref_dtypes.widen_for_compute(da).wire_code
+                comp = _compute(da)
                 fc = int(unary_forces_complex(fn) and not da.is_complex)
             args = (st.handle, code, C.byref(p), C.byref(dop), C.byref(a), comp, MODE_CODE[mode],
                     fc)
@@ -771,7 +760,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
                 a = abi.make_operand(aptr, bases[1], da.wire_code, aord == "big")
             dop = abi.make_operand(dptr, bases[0], dd.wire_code, dord == "big")
             po, pi = _plan(outer), _plan(inner)
-            comp = ref_dtypes.widen_for_compute(da).wire_code
+            comp = _compute(da)
             args = (st.handle, code, float(p), C.byref(po), C.byref(pi), C.byref(dop), C.byref(a),
                     comp, MODE_CODE[mode])
             _run(st, mode, ctx, dd, lambda: L.tpg_reduce(*args))
@@ -795,7 +784,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
         b = _operand(bptr, b_base, db, bord, temps, (k, n), b_strides)
         dop = abi.make_operand(dptr, d_base, dd.wire_code, dord == "big")
         ds, as_, bs = ((C.c_int64 * 2)(*s) for s in (d_strides, a_strides, b_strides))
-        comp = ref_dtypes.widen_for_compute(da).wire_code
+        comp = _compute(da)
         _run(st, mode, ctx, dd, lambda: L.tpg_matmul(st.handle, C.byref(dop), ds, C.byref(a), as_,
                                                      C.byref(b), bs, m, n, k, comp,
                                                      MODE_CODE[mode]))
@@ -922,7 +911,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
         b = _operand(bptr, b_base, db, bord, temps, (k, n, nb), b_strides)
         dop = abi.make_operand(dptr, d_base, dd.wire_code, dord == "big")
         ds, as_, bs = ((C.c_int64 * 3)(*x) for x in (d_strides, a_strides, b_strides))
-        comp = ref_dtypes.widen_for_compute(da).wire_code
+        comp = _compute(da)
         _run(st, mode, ctx, dd, lambda: L.tpg_matmul_batched(
             st.handle, nb, C.byref(dop), ds, C.byref(a), as_, C.byref(b), bs, m, n, k, comp,
             MODE_CODE[mode]))

@@ -35,6 +35,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include "../../include/tidepool_gpu.h"
+
 typedef int (*f_malloc_managed)(int, size_t, void**);
 typedef int (*f_free_managed)(void*);
 typedef int (*f_ev_create)(void**);
@@ -47,12 +49,15 @@ typedef int (*f_ev_sync)(void*);
 typedef struct Marker {
   void* ev;
   long refs;
+  uint64_t seq; /* launch epoch it was recorded in */
+  int dev, sidx; /* owning stream */
 } Marker;
 
 typedef struct {
   void* handle;
-  Marker* marker;
+  Marker* marker;    /* newest marker recorded on the stream (NULL once freed) */
   uint64_t marker_seq;
+  uint64_t done_seq; /* every marker of this stream with seq <= done_seq completed */
 } StreamRec;
 
 typedef struct {
@@ -153,9 +158,24 @@ static void unref_markers(BlockPool* p, Entry* e) {
   e->nev = 0;
 }
 
+/* Completion of a freed block's markers.  Events on one stream complete in
+ * order, so a completed marker proves every older marker of its stream
+ * complete: the stream's NEWEST marker is queried first (one query then
+ * usually clears every pending block of the device -- the host runs behind
+ * the GPU in steady state), and a watermark makes repeat checks free. */
 static int entry_done(BlockPool* p, Entry* e) {
-  for (int i = 0; i < e->nev; ++i)
-    if (p->ev_query(e->evs[i]->ev) != 0) return 0;
+  for (int i = 0; i < e->nev; ++i) {
+    Marker* m = e->evs[i];
+    StreamRec* st = &p->streams[m->dev][m->sidx];
+    if (m->seq <= st->done_seq && st->done_seq != (uint64_t)-1) continue;
+    Marker* nw = st->marker;
+    if (nw && nw != m && nw->seq > m->seq && p->ev_query(nw->ev) == 0) {
+      st->done_seq = nw->seq;
+      continue;
+    }
+    if (p->ev_query(m->ev) != 0) return 0;
+    if (st->done_seq == (uint64_t)-1 || m->seq > st->done_seq) st->done_seq = m->seq;
+  }
   return 1;
 }
 
@@ -258,6 +278,9 @@ static void release_block(BlockPool* p, void* ptr, size_t cap, int dev) {
           free(m);
           break;
         }
+        m->seq = p->seq;
+        m->dev = dev;
+        m->sidx = s;
         p->ev_record(m->ev, st->handle);
         st->marker = m;
         st->marker_seq = p->seq;
@@ -471,6 +494,7 @@ static PyObject* pool_add_stream(BlockPool* p, PyObject* args) {
   ns[p->nstreams[dev]].handle = handle;
   ns[p->nstreams[dev]].marker = NULL;
   ns[p->nstreams[dev]].marker_seq = (uint64_t)-1;
+  ns[p->nstreams[dev]].done_seq = (uint64_t)-1; /* nothing known yet */
   p->nstreams[dev]++;
   Py_RETURN_NONE;
 }
@@ -517,6 +541,676 @@ static PyMethodDef pool_methods[] = {
     {"cached_bytes", (PyCFunction)pool_cached_bytes, METH_VARARGS, "cached bytes of a device"},
     {NULL}};
 
+
+/* ---------------------------------------------------------------- Entries
+ * The gpu table's binary entry for the common case, in C: standard mode,
+ * every operand a gpu storage of one device, no pending lazy copy that
+ * must materialise first.  Decodes the reference's closures exactly as
+ * tidepool_plugin.py does (store cells pack / mode, codec functions,
+ * scalar fn's status cell), fuses a pending lossless cast into the load
+ * (the Python _fuse_strides rule), builds the tpg_plan / tpg_operand
+ * descriptors and calls tpg_binary.  Returns None when the Python entry
+ * must handle the call (no side effect has happened then), else the
+ * C-ABI return code.
+ *
+ *   Entries(pool, binary_fn_address, rt, tls, lazy, lazy_by_src, codecs,
+ *           stats)
+ *     codecs: {codec function: (wire code, size, big endian, compute code)}
+ *     .set_default_stream(device, handle)
+ *     .binary(op_code, plan, d_buf, store, a_buf, a_unpack, b_buf,
+ *             b_unpack, fn, bases)
+ */
+typedef int (*f_binary)(void*, int, const tpg_plan*, const tpg_operand*, const tpg_operand*,
+                        const tpg_operand*, int, int);
+
+typedef struct {
+  PyObject_HEAD
+  BlockPool* pool;
+  f_binary binary;
+  PyObject *rt, *tls, *lazy, *lazy_by_src, *codecs, *stats;
+  PyObject* cell_idx; /* {(code, tag): tuple of closure indices} */
+  PyObject* lazy_cls; /* tidepool_plugin._Lazy */
+  PyObject* codec_objs; /* {codec function: (reference dtype, byteorder)} */
+  PyObject* lossless;   /* bytes[32 * 32]: lossless_castable(src wire, dst wire) */
+  PyObject* default_st[MAX_DEV]; /* default GpuStream objects */
+  void* defaults[MAX_DEV];
+  long long n_fast, n_fallback;
+} Entries;
+
+static PyTypeObject EntriesType;
+/* attribute names of a lazy-copy record (+ "lazy", the stats key) */
+static const char* const L_str[19] = {"device", "plan", "stream", "dst_ptr", "src_ptr", "ddt",
+                                      "dbig", "keep", "src_dtype", "dst_dtype", "src_order",
+                                      "cext", "cdst", "csrc", "sbase", "soff", "sdt", "sbig",
+                                      "lazy"};
+static PyObject* L_names[19];
+static PyObject *S_standard, *S_stream, *S_device, *S_index, *S_handle, *S_status_sink, *S_extents,
+    *S_strides, *S_fused, *S_src_ptr, *S_cext, *S_cdst, *S_csrc, *S_sbase, *S_soff, *S_sdt,
+    *S_sbig, *S_pack, *S_mode, *S_ctx, *S_status, *S_store_tag, *S_status_tag;
+
+static int entries_init(Entries* e, PyObject* args, PyObject* kw) {
+  PyObject *pool, *fnaddr;
+  if (!PyArg_ParseTuple(args, "O!OOOO!O!O!O", &BlockPoolType, &pool, &fnaddr, &e->rt, &e->tls,
+                        &PyDict_Type, &e->lazy, &PyDict_Type, &e->lazy_by_src, &PyDict_Type,
+                        &e->codecs, &e->stats))
+    return -1;
+  e->binary = (f_binary)PyLong_AsVoidPtr(fnaddr);
+  if (!e->binary) {
+    if (!PyErr_Occurred()) PyErr_SetString(PyExc_ValueError, "null tpg_binary address");
+    return -1;
+  }
+  Py_INCREF(pool);
+  e->pool = (BlockPool*)pool;
+  Py_INCREF(e->rt);
+  Py_INCREF(e->tls);
+  Py_INCREF(e->lazy);
+  Py_INCREF(e->lazy_by_src);
+  Py_INCREF(e->codecs);
+  Py_INCREF(e->stats);
+  e->cell_idx = PyDict_New();
+  return e->cell_idx ? 0 : -1;
+}
+
+static PyObject* entries_set_copy_support(Entries* e, PyObject* args) {
+  PyObject *cls, *objs, *ll;
+  if (!PyArg_ParseTuple(args, "OO!O!", &cls, &PyDict_Type, &objs, &PyBytes_Type, &ll)) return NULL;
+  if (PyBytes_GET_SIZE(ll) != 32 * 32) {
+    PyErr_SetString(PyExc_ValueError, "lossless table must be 32 x 32 bytes");
+    return NULL;
+  }
+  Py_INCREF(cls);
+  Py_INCREF(objs);
+  Py_INCREF(ll);
+  Py_XSETREF(e->lazy_cls, cls);
+  Py_XSETREF(e->codec_objs, objs);
+  Py_XSETREF(e->lossless, ll);
+  Py_RETURN_NONE;
+}
+
+static int entries_traverse(Entries* e, visitproc visit, void* arg) {
+  Py_VISIT(e->pool);
+  Py_VISIT(e->rt);
+  Py_VISIT(e->tls);
+  Py_VISIT(e->lazy);
+  Py_VISIT(e->lazy_by_src);
+  Py_VISIT(e->codecs);
+  Py_VISIT(e->stats);
+  Py_VISIT(e->cell_idx);
+  Py_VISIT(e->lazy_cls);
+  Py_VISIT(e->codec_objs);
+  Py_VISIT(e->lossless);
+  for (int d = 0; d < MAX_DEV; ++d) Py_VISIT(e->default_st[d]);
+  return 0;
+}
+
+static int entries_clear(Entries* e) {
+  Py_CLEAR(e->pool);
+  Py_CLEAR(e->rt);
+  Py_CLEAR(e->tls);
+  Py_CLEAR(e->lazy);
+  Py_CLEAR(e->lazy_by_src);
+  Py_CLEAR(e->codecs);
+  Py_CLEAR(e->stats);
+  Py_CLEAR(e->cell_idx);
+  Py_CLEAR(e->lazy_cls);
+  Py_CLEAR(e->codec_objs);
+  Py_CLEAR(e->lossless);
+  for (int d = 0; d < MAX_DEV; ++d) Py_CLEAR(e->default_st[d]);
+  return 0;
+}
+
+static void entries_dealloc(Entries* e) {
+  PyObject_GC_UnTrack(e);
+  entries_clear(e);
+  Py_TYPE(e)->tp_free((PyObject*)e);
+}
+
+/* closure cell contents of `fn` for `names` (borrowed refs, NULL when
+ * absent); the name -> index map is cached per code object.  Returns -1 when
+ * fn is not a Python function with a closure. */
+static int closure_cells(Entries* e, PyObject* fn, PyObject* tag, PyObject* const* names, int n,
+                         PyObject** out) {
+  if (!PyFunction_Check(fn)) return -1;
+  PyObject* clos = PyFunction_GET_CLOSURE(fn);
+  if (!clos) return -1;
+  PyObject* code = PyFunction_GET_CODE(fn);
+  PyObject* key = PyTuple_Pack(2, code, tag);
+  if (!key) return -2;
+  PyObject* idx = PyDict_GetItemWithError(e->cell_idx, key);
+  if (!idx) {
+    if (PyErr_Occurred()) {
+      Py_DECREF(key);
+      return -2;
+    }
+    PyObject* fv = PyObject_GetAttrString(code, "co_freevars");
+    if (!fv) {
+      Py_DECREF(key);
+      return -2;
+    }
+    idx = PyTuple_New(n);
+    for (int k = 0; idx && k < n; ++k) {
+      long at = -1;
+      for (Py_ssize_t i = 0; i < PyTuple_GET_SIZE(fv); ++i)
+        if (PyUnicode_Compare(PyTuple_GET_ITEM(fv, i), names[k]) == 0) at = (long)i;
+      PyTuple_SET_ITEM(idx, k, PyLong_FromLong(at));
+    }
+    Py_DECREF(fv);
+    if (!idx || PyDict_SetItem(e->cell_idx, key, idx) < 0) {
+      Py_XDECREF(idx);
+      Py_DECREF(key);
+      return -2;
+    }
+    Py_DECREF(idx); /* the dict holds it */
+  }
+  Py_DECREF(key);
+  for (int k = 0; k < n; ++k) {
+    long at = PyLong_AsLong(PyTuple_GET_ITEM(idx, k));
+    out[k] = (at >= 0 && at < PyTuple_GET_SIZE(clos))
+                 ? PyCell_GET(PyTuple_GET_ITEM(clos, at))
+                 : NULL;
+  }
+  return 0;
+}
+
+/* DevBuf behind a memoryview (or NULL) */
+static DevBuf* devbuf_of(PyObject* mv) {
+  if (!PyMemoryView_Check(mv)) return NULL;
+  PyObject* b = PyMemoryView_GET_BASE(mv);
+  return (b && Py_TYPE(b) == &DevBufType) ? (DevBuf*)b : NULL;
+}
+
+typedef struct {
+  int wire, size, big, compute;
+} CodecInfo;
+
+static int codec_info(Entries* e, PyObject* fn, CodecInfo* ci) {
+  PyObject* t = fn ? PyDict_GetItemWithError(e->codecs, fn) : NULL;
+  if (!t || !PyTuple_Check(t) || PyTuple_GET_SIZE(t) != 4) return -1;
+  ci->wire = (int)PyLong_AsLong(PyTuple_GET_ITEM(t, 0));
+  ci->size = (int)PyLong_AsLong(PyTuple_GET_ITEM(t, 1));
+  ci->big = (int)PyLong_AsLong(PyTuple_GET_ITEM(t, 2));
+  ci->compute = (int)PyLong_AsLong(PyTuple_GET_ITEM(t, 3));
+  return PyErr_Occurred() ? -1 : 0;
+}
+
+/* int64 sequence -> array; -1 on any mismatch */
+static int i64_seq(PyObject* seq, int64_t* out, int maxn) {
+  PyObject* f = PySequence_Fast(seq, "sequence");
+  if (!f) return -1;
+  Py_ssize_t n = PySequence_Fast_GET_SIZE(f);
+  if (n > maxn) {
+    Py_DECREF(f);
+    return -1;
+  }
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    out[i] = PyLong_AsLongLong(PySequence_Fast_GET_ITEM(f, i));
+    if (out[i] == -1 && PyErr_Occurred()) {
+      Py_DECREF(f);
+      return -1;
+    }
+  }
+  Py_DECREF(f);
+  return (int)n;
+}
+
+static int64_t attr_i64(PyObject* o, PyObject* name, int* bad) {
+  PyObject* v = PyObject_GetAttr(o, name);
+  if (!v) {
+    *bad = 1;
+    return 0;
+  }
+  int64_t r = PyLong_AsLongLong(v);
+  Py_DECREF(v);
+  if (r == -1 && PyErr_Occurred()) *bad = 1;
+  return r;
+}
+
+/* _fuse_strides (tidepool_plugin.py): re-express a binary operand reading a
+ * recorded copy's dense destination as a view of the copy's source. */
+static int fuse(PyObject* lz, int nd, const int64_t* bext, const int64_t* bstr, int64_t base,
+                int size, int64_t* out_str, int64_t* out_off, int64_t* sbase_out, int* sdt_out,
+                int* sbig_out) {
+  int64_t E[TPG_MAX_DIMS], T[TPG_MAX_DIMS], S[TPG_MAX_DIMS], dg[TPG_MAX_DIMS];
+  PyObject *ce = PyObject_GetAttr(lz, S_cext), *cd = PyObject_GetAttr(lz, S_cdst),
+           *cs = PyObject_GetAttr(lz, S_csrc);
+  int ne = -1, nt = -1, ns = -1;
+  if (ce && cd && cs) {
+    ne = i64_seq(ce, E, TPG_MAX_DIMS);
+    nt = i64_seq(cd, T, TPG_MAX_DIMS);
+    ns = i64_seq(cs, S, TPG_MAX_DIMS);
+  }
+  Py_XDECREF(ce);
+  Py_XDECREF(cd);
+  Py_XDECREF(cs);
+  if (ne < 0 || nt != ne || ns != ne || size <= 0 || base % size) {
+    PyErr_Clear();
+    return -1;
+  }
+  int64_t lin = base / size;
+  for (int j = 0; j < ne; ++j) {
+    if (E[j]) {
+      dg[j] = lin % E[j];
+      lin /= E[j];
+    } else {
+      dg[j] = 0;
+    }
+  }
+  if (lin) return -1;
+  unsigned used = 0;
+  for (int i = 0; i < nd; ++i) {
+    if (bext[i] == 1 || bstr[i] == 0) {
+      out_str[i] = 0;
+      continue;
+    }
+    int found = -1;
+    for (int j = 0; j < ne; ++j)
+      if (T[j] == bstr[i] && E[j] == bext[i] && dg[j] == 0 && !(used & (1u << j))) {
+        found = j;
+        break;
+      }
+    if (found < 0) return -1;
+    used |= 1u << found;
+    out_str[i] = S[found];
+  }
+  int64_t off = 0;
+  for (int j = 0; j < ne; ++j) off += dg[j] * S[j];
+  int bad = 0;
+  *out_off = attr_i64(lz, S_soff, &bad) + off;
+  *sbase_out = attr_i64(lz, S_sbase, &bad);
+  *sdt_out = (int)attr_i64(lz, S_sdt, &bad);
+  *sbig_out = (int)attr_i64(lz, S_sbig, &bad);
+  if (bad) {
+    PyErr_Clear();
+    return -1;
+  }
+  return 0;
+}
+
+static PyObject* entries_binary(Entries* e, PyObject* const* args, Py_ssize_t nargs) {
+  if (nargs != 10) {
+    PyErr_SetString(PyExc_TypeError, "binary(op, plan, d_buf, store, a_buf, a_unpack, b_buf, "
+                                     "b_unpack, fn, bases)");
+    return NULL;
+  }
+  int op = (int)PyLong_AsLong(args[0]);
+  PyObject *plan = args[1], *store = args[3], *fn = args[8], *bases = args[9];
+  if (PyErr_Occurred()) return NULL;
+#define FALLBACK()         \
+  do {                     \
+    PyErr_Clear();         \
+    e->n_fallback++;       \
+    Py_RETURN_NONE;        \
+  } while (0)
+  /* store closure: pack / mode */
+  PyObject* sc[3];
+  PyObject* const snames[3] = {S_pack, S_mode, S_ctx};
+  int r = closure_cells(e, store, S_store_tag, snames, 3, sc);
+  if (r == -2) return NULL;
+  if (r < 0 || !sc[0]) FALLBACK();
+  if (sc[1] && sc[1] != S_standard && PyUnicode_Compare(sc[1], S_standard) != 0) FALLBACK();
+  CodecInfo cd, ca, cb;
+  if (codec_info(e, sc[0], &cd) || codec_info(e, args[5], &ca) || codec_info(e, args[7], &cb))
+    FALLBACK();
+  DevBuf *bd = devbuf_of(args[2]), *ba = devbuf_of(args[4]), *bb = devbuf_of(args[6]);
+  if (!bd || !ba || !bb || ba->dev != bd->dev || bb->dev != bd->dev) FALLBACK();
+  const int dev = bd->dev;
+  /* plan */
+  int64_t ext[TPG_MAX_DIMS], str[3][TPG_MAX_DIMS];
+  PyObject *pe = PyObject_GetAttr(plan, S_extents), *ps = PyObject_GetAttr(plan, S_strides);
+  int nd = pe ? i64_seq(pe, ext, TPG_MAX_DIMS) : -1;
+  int ok = nd >= 0 && ps && PySequence_Check(ps) && PySequence_Size(ps) == 3;
+  for (int v = 0; ok && v < 3; ++v) {
+    PyObject* sv = PySequence_GetItem(ps, v);
+    ok = sv && i64_seq(sv, str[v], TPG_MAX_DIMS) == nd;
+    Py_XDECREF(sv);
+  }
+  Py_XDECREF(pe);
+  Py_XDECREF(ps);
+  if (!ok) FALLBACK();
+  if (!PyTuple_Check(bases) || PyTuple_GET_SIZE(bases) != 3) FALLBACK();
+  int64_t base[3];
+  for (int v = 0; v < 3; ++v) base[v] = PyLong_AsLongLong(PyTuple_GET_ITEM(bases, v));
+  if (PyErr_Occurred()) FALLBACK();
+  /* pending lazy copies: the destination must not have one (as dst or
+   * src); an operand with one must fuse */
+  tpg_operand od, oa, ob;
+  memset(&od, 0, sizeof od);
+  memset(&oa, 0, sizeof oa);
+  memset(&ob, 0, sizeof ob);
+  int nfused = 0;
+  if (PyDict_GET_SIZE(e->lazy) || PyDict_GET_SIZE(e->lazy_by_src)) {
+    PyObject* kd = PyLong_FromVoidPtr(bd->ptr);
+    int hit = kd && (PyDict_Contains(e->lazy, kd) == 1 || PyDict_Contains(e->lazy_by_src, kd) == 1);
+    Py_XDECREF(kd);
+    if (hit || PyErr_Occurred()) FALLBACK();
+  }
+  DevBuf* bufs[2] = {ba, bb};
+  CodecInfo* cis[2] = {&ca, &cb};
+  tpg_operand* os[2] = {&oa, &ob};
+  for (int v = 1; v <= 2; ++v) {
+    DevBuf* b = bufs[v - 1];
+    PyObject* lz = NULL;
+    if (PyDict_GET_SIZE(e->lazy)) {
+      PyObject* k = PyLong_FromVoidPtr(b->ptr);
+      lz = k ? PyDict_GetItemWithError(e->lazy, k) : NULL;
+      Py_XDECREF(k);
+      if (PyErr_Occurred()) FALLBACK();
+    }
+    tpg_operand* o = os[v - 1];
+    if (lz) {
+      int bad = 0;
+      int64_t sp = attr_i64(lz, S_src_ptr, &bad);
+      if (bad || (void*)(intptr_t)sp == bd->ptr) FALLBACK();
+      int64_t fstr[TPG_MAX_DIMS], off, sbase;
+      int sdt, sbig;
+      if (fuse(lz, nd, ext, str[v], base[v], cis[v - 1]->size, fstr, &off, &sbase, &sdt, &sbig))
+        FALLBACK();
+      memcpy(str[v], fstr, sizeof(int64_t) * nd);
+      o->base = (void*)(intptr_t)sbase;
+      o->offset = off;
+      o->dtype = sdt;
+      o->big_endian = sbig;
+      nfused++;
+    } else {
+      o->base = b->ptr;
+      o->offset = base[v];
+      o->dtype = cis[v - 1]->wire;
+      o->big_endian = cis[v - 1]->big;
+    }
+  }
+  od.base = bd->ptr;
+  od.offset = base[0];
+  od.dtype = cd.wire;
+  od.big_endian = cd.big;
+  /* stream: the thread's current gpu stream when it is on this device */
+  void* handle = dev < MAX_DEV ? e->defaults[dev] : NULL;
+  PyObject* st = PyObject_GetAttr(e->tls, S_stream);
+  if (!st) {
+    PyErr_Clear();
+  } else if (st != Py_None) {
+    int bad = 0;
+    PyObject* sdev = PyObject_GetAttr(st, S_device);
+    int64_t sidx = sdev ? attr_i64(sdev, S_index, &bad) : (bad = 1, 0);
+    Py_XDECREF(sdev);
+    if (!bad && sidx == dev) handle = (void*)(intptr_t)attr_i64(st, S_handle, &bad);
+    if (bad) {
+      Py_DECREF(st);
+      FALLBACK();
+    }
+  }
+  Py_XDECREF(st);
+  if (!handle) FALLBACK();
+  /* status set the scalar fn records into (kernels.py:72-78) */
+  PyObject* stc[1];
+  PyObject* const stn[1] = {S_status};
+  r = closure_cells(e, fn, S_status_tag, stn, 1, stc);
+  if (r == -2) return NULL;
+  if (r == 0 && stc[0] && PySet_Check(stc[0])) {
+    PyObject* cur = PyObject_GetAttr(e->rt, S_status_sink);
+    if (cur != stc[0] && PyObject_SetAttr(e->rt, S_status_sink, stc[0]) < 0) {
+      Py_XDECREF(cur);
+      return NULL;
+    }
+    Py_XDECREF(cur);
+    PyErr_Clear();
+  }
+  /* launch */
+  tpg_plan p;
+  memset(&p, 0, sizeof p);
+  p.ndim = nd;
+  p.nviews = 3;
+  for (int i = 0; i < nd; ++i) {
+    p.extent[i] = ext[i];
+    for (int v = 0; v < 3; ++v) p.stride[v][i] = str[v][i];
+  }
+  e->pool->seq++; /* rt.current(): a new launch epoch */
+  int rc = e->binary(handle, op, &p, &od, &oa, &ob, ca.compute, 0);
+  e->n_fast++;
+  if (nfused) {
+    PyObject* c = PyObject_GetItem(e->stats, S_fused);
+    long long n = c ? PyLong_AsLongLong(c) : 0;
+    Py_XDECREF(c);
+    PyErr_Clear();
+    PyObject* nv = PyLong_FromLongLong(n + nfused);
+    if (nv) PyObject_SetItem(e->stats, S_fused, nv);
+    Py_XDECREF(nv);
+    PyErr_Clear();
+  }
+  return PyLong_FromLong(rc);
+#undef FALLBACK
+}
+
+static PyObject* entries_set_default(Entries* e, PyObject* args) {
+  int dev;
+  PyObject *h, *obj;
+  if (!PyArg_ParseTuple(args, "iOO", &dev, &h, &obj)) return NULL;
+  if (dev < 0 || dev >= MAX_DEV) {
+    PyErr_SetString(PyExc_ValueError, "device index out of range");
+    return NULL;
+  }
+  e->defaults[dev] = PyLong_AsVoidPtr(h);
+  if (PyErr_Occurred()) return NULL;
+  Py_INCREF(obj);
+  Py_XSETREF(e->default_st[dev], obj);
+  Py_RETURN_NONE;
+}
+
+/* The gpu table's `copy` entry when it can be RECORDED instead of launched
+ * (tidepool_plugin._try_lazy; ops._dtype_convert, ops.py:121-124): standard
+ * mode, a lossless dtype change from a gpu source into a fresh dense gpu
+ * destination of the same device, neither with a pending copy.  Returns
+ * True when recorded, None when the Python entry must handle the call. */
+static PyObject* entries_copy(Entries* e, PyObject* const* args, Py_ssize_t nargs) {
+  if (nargs != 7) {
+    PyErr_SetString(PyExc_TypeError, "copy(plan, d_buf, store, a_buf, a_unpack, fn, bases)");
+    return NULL;
+  }
+  PyObject *plan = args[0], *store = args[2], *a_unpack = args[4], *bases = args[6];
+#define FALLBACK()   \
+  do {               \
+    PyErr_Clear();   \
+    e->n_fallback++; \
+    Py_RETURN_NONE;  \
+  } while (0)
+  if (!e->lazy_cls) FALLBACK();
+  PyObject* sc[3];
+  PyObject* const snames[3] = {S_pack, S_mode, S_ctx};
+  int r = closure_cells(e, store, S_store_tag, snames, 3, sc);
+  if (r == -2) return NULL;
+  if (r < 0 || !sc[0]) FALLBACK();
+  if (sc[1] && sc[1] != S_standard && PyUnicode_Compare(sc[1], S_standard) != 0) FALLBACK();
+  CodecInfo cd, ca;
+  if (codec_info(e, sc[0], &cd) || codec_info(e, a_unpack, &ca)) FALLBACK();
+  PyObject* dobj = PyDict_GetItemWithError(e->codec_objs, sc[0]);
+  PyObject* aobj = PyDict_GetItemWithError(e->codec_objs, a_unpack);
+  if (!dobj || !aobj || !PyTuple_Check(dobj) || !PyTuple_Check(aobj)) FALLBACK();
+  PyObject *dd = PyTuple_GET_ITEM(dobj, 0), *da = PyTuple_GET_ITEM(aobj, 0);
+  if (dd == da) FALLBACK();
+  if (cd.wire < 0 || cd.wire >= 32 || ca.wire < 0 || ca.wire >= 32 ||
+      !PyBytes_AS_STRING(e->lossless)[ca.wire * 32 + cd.wire])
+    FALLBACK();
+  DevBuf *bd = devbuf_of(args[1]), *ba = devbuf_of(args[3]);
+  if (!bd || !ba || ba->dev != bd->dev || ba->ptr == bd->ptr) FALLBACK();
+  const int dev = bd->dev;
+  if (!PyTuple_Check(bases) || PyTuple_GET_SIZE(bases) != 2) FALLBACK();
+  int64_t b0 = PyLong_AsLongLong(PyTuple_GET_ITEM(bases, 0));
+  int64_t b1 = PyLong_AsLongLong(PyTuple_GET_ITEM(bases, 1));
+  if (PyErr_Occurred() || b0 != 0) FALLBACK();
+  /* dense destination, non-empty (a fresh tensor_create layout) */
+  int64_t ext[TPG_MAX_DIMS], s0[TPG_MAX_DIMS], s1[TPG_MAX_DIMS];
+  PyObject *pe = PyObject_GetAttr(plan, S_extents), *ps = PyObject_GetAttr(plan, S_strides);
+  int nd = pe ? i64_seq(pe, ext, TPG_MAX_DIMS) : -1;
+  int ok = nd >= 0 && ps && PySequence_Check(ps) && PySequence_Size(ps) == 2;
+  PyObject *v0 = NULL, *v1 = NULL;
+  if (ok) {
+    v0 = PySequence_GetItem(ps, 0);
+    v1 = PySequence_GetItem(ps, 1);
+    ok = v0 && v1 && i64_seq(v0, s0, TPG_MAX_DIMS) == nd && i64_seq(v1, s1, TPG_MAX_DIMS) == nd;
+  }
+  int64_t step = cd.size, total = 1;
+  for (int i = 0; ok && i < nd; ++i) {
+    total *= ext[i];
+    if (ext[i] == 1) continue;
+    if (s0[i] != step) ok = 0;
+    step *= ext[i];
+  }
+  if (!ok || total == 0) {
+    Py_XDECREF(pe);
+    Py_XDECREF(ps);
+    Py_XDECREF(v0);
+    Py_XDECREF(v1);
+    FALLBACK();
+  }
+  /* neither side may have a pending copy */
+  PyObject *kd = PyLong_FromVoidPtr(bd->ptr), *ka = PyLong_FromVoidPtr(ba->ptr);
+  int busy = !kd || !ka || PyDict_Contains(e->lazy, kd) == 1 ||
+             PyDict_Contains(e->lazy_by_src, kd) == 1 || PyDict_Contains(e->lazy, ka) == 1;
+  /* the stream the copy is recorded on (rt.current) */
+  PyObject* st = busy ? NULL : PyObject_GetAttr(e->tls, S_stream);
+  if (!busy && !st) PyErr_Clear();
+  if (!busy && st == Py_None) Py_CLEAR(st);
+  if (!busy && st) {
+    int bad = 0;
+    PyObject* sdev = PyObject_GetAttr(st, S_device);
+    int64_t sidx = sdev ? attr_i64(sdev, S_index, &bad) : (bad = 1, 0);
+    Py_XDECREF(sdev);
+    if (bad) busy = 1;
+    else if (sidx != dev) Py_CLEAR(st);
+  }
+  if (!busy && !st) {
+    st = e->default_st[dev];
+    Py_XINCREF(st);
+    if (!st) busy = 1;
+  }
+  if (busy) {
+    Py_XDECREF(kd);
+    Py_XDECREF(ka);
+    Py_XDECREF(st);
+    Py_XDECREF(pe);
+    Py_XDECREF(ps);
+    Py_XDECREF(v0);
+    Py_XDECREF(v1);
+    FALLBACK();
+  }
+  e->pool->seq++; /* rt.current() */
+  PyObject* lz = PyObject_CallNoArgs(e->lazy_cls);
+  int err = !lz;
+  PyObject* vals[][2] = {
+      {(Py_INCREF(L_names[0]), L_names[0]), PyLong_FromLong(dev)},
+      {(Py_INCREF(L_names[1]), L_names[1]), (Py_INCREF(plan), plan)},
+      {(Py_INCREF(L_names[2]), L_names[2]), (Py_INCREF(st), st)},
+      {(Py_INCREF(L_names[3]), L_names[3]), (Py_INCREF(kd), kd)},
+      {(Py_INCREF(L_names[4]), L_names[4]), (Py_INCREF(ka), ka)},
+      {(Py_INCREF(L_names[5]), L_names[5]), PyLong_FromLong(cd.wire)},
+      {(Py_INCREF(L_names[6]), L_names[6]), PyLong_FromLong(cd.big)},
+      {(Py_INCREF(L_names[7]), L_names[7]), (Py_INCREF(args[3]), args[3])},
+      {(Py_INCREF(L_names[8]), L_names[8]), (Py_INCREF(da), da)},
+      {(Py_INCREF(L_names[9]), L_names[9]), (Py_INCREF(dd), dd)},
+      {(Py_INCREF(L_names[10]), L_names[10]),
+       (Py_INCREF(PyTuple_GET_ITEM(aobj, 1)), PyTuple_GET_ITEM(aobj, 1))},
+      {(Py_INCREF(L_names[11]), L_names[11]), PySequence_Tuple(pe)},
+      {(Py_INCREF(L_names[12]), L_names[12]), PySequence_Tuple(v0)},
+      {(Py_INCREF(L_names[13]), L_names[13]), PySequence_Tuple(v1)},
+      {(Py_INCREF(L_names[14]), L_names[14]), (Py_INCREF(ka), ka)},
+      {(Py_INCREF(L_names[15]), L_names[15]), PyLong_FromLongLong(b1)},
+      {(Py_INCREF(L_names[16]), L_names[16]), PyLong_FromLong(ca.wire)},
+      {(Py_INCREF(L_names[17]), L_names[17]), PyLong_FromLong(ca.big)},
+  };
+  const int nv = (int)(sizeof vals / sizeof vals[0]);
+  for (int i = 0; i < nv; ++i) {
+    if (!err && (!vals[i][0] || !vals[i][1] || PyObject_SetAttr(lz, vals[i][0], vals[i][1]) < 0))
+      err = 1;
+    Py_XDECREF(vals[i][0]);
+    Py_XDECREF(vals[i][1]);
+  }
+  PyObject* set = NULL;
+  if (!err) err = PyDict_SetItem(e->lazy, kd, lz) < 0;
+  if (!err) {
+    set = PyDict_GetItemWithError(e->lazy_by_src, ka);
+    if (set) {
+      err = PySet_Add(set, kd) < 0;
+    } else if (!PyErr_Occurred()) {
+      set = PySet_New(NULL);
+      err = !set || PySet_Add(set, kd) < 0 || PyDict_SetItem(e->lazy_by_src, ka, set) < 0;
+      Py_XDECREF(set);
+    } else {
+      err = 1;
+    }
+  }
+  if (!err) {
+    PyObject* key = (Py_INCREF(L_names[18]), L_names[18]);
+    PyObject* c = key ? PyObject_GetItem(e->stats, key) : NULL;
+    long long n = c ? PyLong_AsLongLong(c) : 0;
+    Py_XDECREF(c);
+    PyErr_Clear();
+    PyObject* nvv = PyLong_FromLongLong(n + 1);
+    if (key && nvv) PyObject_SetItem(e->stats, key, nvv);
+    Py_XDECREF(nvv);
+    Py_XDECREF(key);
+    PyErr_Clear();
+  }
+  Py_XDECREF(lz);
+  Py_DECREF(kd);
+  Py_DECREF(ka);
+  Py_DECREF(st);
+  Py_XDECREF(pe);
+  Py_XDECREF(ps);
+  Py_XDECREF(v0);
+  Py_XDECREF(v1);
+  if (err) return NULL;
+  e->n_fast++;
+  Py_RETURN_TRUE;
+#undef FALLBACK
+}
+
+static PyObject* entries_counts(Entries* e, PyObject* unused) {
+  return Py_BuildValue("{s:L,s:L}", "fast", e->n_fast, "fallback", e->n_fallback);
+}
+
+static PyMethodDef entries_methods[] = {
+    {"binary", (PyCFunction)(void (*)(void))entries_binary, METH_FASTCALL,
+     "binary(op, plan, d_buf, store, a_buf, a_unpack, b_buf, b_unpack, fn, bases) -> rc | None"},
+    {"set_default_stream", (PyCFunction)entries_set_default, METH_VARARGS,
+     "set_default_stream(device, handle, stream object)"},
+    {"copy", (PyCFunction)(void (*)(void))entries_copy, METH_FASTCALL,
+     "copy(plan, d_buf, store, a_buf, a_unpack, fn, bases) -> True | None"},
+    {"set_copy_support", (PyCFunction)entries_set_copy_support, METH_VARARGS,
+     "set_copy_support(lazy class, {codec fn: (dtype, order)}, lossless table bytes)"},
+    {"counts", (PyCFunction)entries_counts, METH_NOARGS, "fast / fallback call counts"},
+    {NULL}};
+
+static int intern_names(void) {
+#define IN(var, str) \
+  if (!(var = PyUnicode_InternFromString(str))) return -1;
+  IN(S_standard, "standard");
+  IN(S_stream, "stream");
+  IN(S_device, "device");
+  IN(S_index, "index");
+  IN(S_handle, "handle");
+  IN(S_status_sink, "status_sink");
+  IN(S_extents, "extents");
+  IN(S_strides, "strides");
+  IN(S_fused, "fused");
+  IN(S_src_ptr, "src_ptr");
+  IN(S_cext, "cext");
+  IN(S_cdst, "cdst");
+  IN(S_csrc, "csrc");
+  IN(S_sbase, "sbase");
+  IN(S_soff, "soff");
+  IN(S_sdt, "sdt");
+  IN(S_sbig, "sbig");
+  IN(S_pack, "pack");
+  IN(S_mode, "mode");
+  IN(S_ctx, "ctx");
+  IN(S_status, "status");
+  IN(S_store_tag, "#store");
+  IN(S_status_tag, "#status");
+#undef IN
+  for (int i = 0; i < 19; ++i)
+    if (!(L_names[i] = PyUnicode_InternFromString(L_str[i]))) return -1;
+  return 0;
+}
+
 static PyObject* set_alloc_error(PyObject* m, PyObject* cls) {
   Py_XDECREF(AllocError);
   Py_INCREF(cls);
@@ -560,11 +1254,26 @@ PyMODINIT_FUNC PyInit__tpg_pyfast(void) {
   BlockPoolType.tp_methods = pool_methods;
   if (PyType_Ready(&BlockPoolType) < 0) return NULL;
 
+  if (intern_names() < 0) return NULL;
+  EntriesType.tp_name = "_tpg_pyfast.Entries";
+  EntriesType.tp_basicsize = sizeof(Entries);
+  EntriesType.tp_flags = Py_TPFLAGS_DEFAULT | Py_TPFLAGS_HAVE_GC;
+  EntriesType.tp_doc = "C fast path of the gpu table's binary entry";
+  EntriesType.tp_new = PyType_GenericNew;
+  EntriesType.tp_init = (initproc)entries_init;
+  EntriesType.tp_dealloc = (destructor)entries_dealloc;
+  EntriesType.tp_traverse = (traverseproc)entries_traverse;
+  EntriesType.tp_clear = (inquiry)entries_clear;
+  EntriesType.tp_methods = entries_methods;
+  if (PyType_Ready(&EntriesType) < 0) return NULL;
+
   PyObject* m = PyModule_Create(&moddef);
   if (!m) return NULL;
   Py_INCREF(&DevBufType);
   PyModule_AddObject(m, "DevBuf", (PyObject*)&DevBufType);
   Py_INCREF(&BlockPoolType);
   PyModule_AddObject(m, "BlockPool", (PyObject*)&BlockPoolType);
+  Py_INCREF(&EntriesType);
+  PyModule_AddObject(m, "Entries", (PyObject*)&EntriesType);
   return m;
 }

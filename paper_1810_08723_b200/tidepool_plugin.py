@@ -241,6 +241,22 @@ def _fast_module():
 _DEVBUF = None  # _tpg_pyfast.DevBuf once the first registration loaded it
 
 
+def _binary_function(L, abi):
+    """Address of tpg_binary for the C entry (a ctypes callback into a
+    duck-typed test double)."""
+    if isinstance(L, C.CDLL):
+        return C.cast(L.tpg_binary, C.c_void_p).value
+    PP, PO = C.POINTER(abi.Plan), C.POINTER(abi.Operand)
+    cb = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, PP, PO, PO, PO, C.c_int, C.c_int)(
+        lambda st, op, p, d, a, b, comp, mode: L.tpg_binary(st, op, p.contents, d.contents,
+                                                            a.contents, b.contents, comp, mode))
+    _CALLBACKS.append(cb)
+    return C.cast(cb, C.c_void_p).value
+
+
+_CALLBACKS: list = []  # ctypes callbacks handed to C (kept alive)
+
+
 def _pool_functions(L):
     """Addresses of the six C-ABI functions the block pool calls.  For a
     ctypes library they are the exported symbols; for a duck-typed test
@@ -421,8 +437,10 @@ class _Runtime:
 
 class _Lazy:
     """A recorded dtype-converting gpu->gpu copy (ops._dtype_convert)."""
-    __slots__ = ("device", "plan", "dst_ptr", "dst_op", "src_ptr", "src_op", "keep", "src_dtype",
-                 "dst_dtype", "src_order", "stream")
+    __slots__ = ("device", "plan", "dst_ptr", "ddt", "dbig", "src_ptr", "keep", "src_dtype",
+                 "dst_dtype", "src_order", "stream",
+                 # plain-int copies read by the C binary entry (tpg_pyfast.c)
+                 "cext", "cdst", "csrc", "sbase", "soff", "sdt", "sbig")
 
     def launch(self, rt):
         """Launch on the stream the copy entry ran on (the destination
@@ -430,8 +448,10 @@ class _Lazy:
         consumer on another stream of this thread waits for it."""
         st = self.stream
         p = rt.abi.make_plan(self.plan.extents, self.plan.strides)
-        rt.check(rt.L.tpg_unary(st.handle, 10, C.byref(p), C.byref(self.dst_op),
-                                C.byref(self.src_op), self.src_op.dtype, 0, 0), "copy")
+        d = rt.abi.make_operand(self.dst_ptr, 0, self.ddt, self.dbig)
+        a = rt.abi.make_operand(self.sbase, self.soff, self.sdt, self.sbig)
+        rt.check(rt.L.tpg_unary(st.handle, 10, C.byref(p), C.byref(d), C.byref(a), self.sdt, 0,
+                                0), "copy")
         cur = getattr(rt.tls, "stream", None)
         if cur is not None and cur is not st and cur.device.index == self.device:
             rt.check(rt.L.tpg_stream_wait(cur.handle, st.handle), "stream wait")
@@ -461,6 +481,19 @@ def register(tidepool_module, count: int | None = None, lib=None):
     codec_of = {}
     for (d, order), pair in ref_dtypes._CODEC_CACHE.items():
         codec_of[pair[0]] = codec_of[pair[1]] = (d, order)
+    fast_codecs = {f: (d.wire_code, d.size, int(order == "big"),
+                       ref_dtypes.widen_for_compute(d).wire_code)
+                   for f, (d, order) in codec_of.items()}
+    rt.entries = _fast_module().Entries(rt.pool, _binary_function(L, abi), rt, rt.tls, rt.lazy,
+                                        rt.lazy_by_src, fast_codecs, rt.stats)
+    fast_binary = rt.entries.binary
+    lossless_table = bytearray(32 * 32)
+    for a_ in ref_dtypes.ALL_DTYPES:
+        for b_ in ref_dtypes.ALL_DTYPES:
+            lossless_table[a_.wire_code * 32 + b_.wire_code] = \
+                int(bool(ref_dtypes.lossless_castable(a_, b_)))
+    rt.entries.set_copy_support(_Lazy, dict(codec_of), bytes(lossless_table))
+    fast_copy = rt.entries.copy
 
     # -- devices and streams ------------------------------------------------------
     class GpuStream(ref_devices.Stream):
@@ -480,6 +513,9 @@ def register(tidepool_module, count: int | None = None, lib=None):
 
         def submit(self, task) -> None:
             prev = getattr(rt.tls, "stream", None)
+            if prev is None and rt.defaults.get(self.device.index) is self:
+                task()  # rt.current() resolves to this stream anyway
+                return
             rt.tls.stream = self
             try:
                 task()
@@ -501,6 +537,8 @@ def register(tidepool_module, count: int | None = None, lib=None):
                     h = C.c_void_p()
                     rt.check(L.tpg_default_stream(self.index, C.byref(h)), "default stream")
                     self._default_stream = GpuStream(self, h.value)
+                    rt.entries.set_default_stream(self.index, h.value, self._default_stream)
+                    rt.defaults[self.index] = self._default_stream
                 return self._default_stream
 
         def allocate(self, nbytes):
@@ -643,6 +681,13 @@ def register(tidepool_module, count: int | None = None, lib=None):
         code = abi.BINARY_CODE[op]
 
         def h(plan, d_buf, store, a_buf, a_unpack, b_buf, b_unpack, fn, bases):
+            if rt.profile is None:  # C fast path (standard mode, all-gpu operands)
+                rc = fast_binary(code, plan, d_buf, store, a_buf, a_unpack, b_buf, b_unpack, fn,
+                                 bases)
+                if rc is not None:
+                    if rc:
+                        rt.check(rc, "kernel")
+                    return
             dd, dord, mode, ctx = _store(store)
             da, aord = _codec(a_unpack)
             db, bord = _codec(b_unpack)
@@ -665,8 +710,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
                         keep = rt.lazy.get(ptr) is lz
                     if keep:
                         rt.stats["fused"] += 1
-                        o = abi.make_operand(lz.src_op.base, lz.src_op.offset + off,
-                                             lz.src_op.dtype, lz.src_op.big_endian)
+                        o = abi.make_operand(lz.sbase, lz.soff + off, lz.sdt, lz.sbig)
                         ops.append(o)
                         strides.append(s)
                         continue
@@ -687,6 +731,9 @@ def register(tidepool_module, count: int | None = None, lib=None):
         code = abi.UNARY_CODE[op]
 
         def h(plan, d_buf, store, a_buf, a_unpack, fn, bases):
+            if op == "identity" and rt.profile is None and \
+                    fast_copy(plan, d_buf, store, a_buf, a_unpack, fn, bases):
+                return  # recorded as a lazy cast (tpg_pyfast.c: the _try_lazy rule)
             dd, dord, mode, ctx = _store(store)
             da, aord = _codec(a_unpack)
             dptr, aptr = rt.address(d_buf), rt.address(a_buf)
@@ -715,12 +762,20 @@ def register(tidepool_module, count: int | None = None, lib=None):
         h.__name__ = f"gpu_{op}"
         return h
 
+    lossless = {}
+
+    def _lossless(a, b):
+        r = lossless.get((a, b))
+        if r is None:
+            r = lossless[(a, b)] = bool(ref_dtypes.lossless_castable(a, b))
+        return r
+
     def _try_lazy(plan, dptr, dd, dord, mode, aptr, da, aord, bases, a_buf, dev):
         """Record a lossless gpu->gpu dtype conversion into a fresh dense
         tensor instead of launching it (ops._dtype_convert, ops.py:121-124)."""
         if (mode != "standard" or da is dd or bases[0] != 0 or not rt.is_gpu(aptr)
                 or aptr == dptr or rt.blocks[aptr][0] != dev or aptr in rt.lazy
-                or not ref_dtypes.lossless_castable(da, dd)
+                or not _lossless(da, dd)
                 or not _is_dense(plan.extents, plan.strides[0], dd.size)
                 or plan.total == 0):
             return False
@@ -728,10 +783,11 @@ def register(tidepool_module, count: int | None = None, lib=None):
         lz.device, lz.plan = dev, plan
         lz.stream = rt.current(dev)
         lz.dst_ptr, lz.src_ptr = dptr, aptr
-        lz.dst_op = abi.make_operand(dptr, 0, dd.wire_code, dord == "big")
-        lz.src_op = abi.make_operand(aptr, bases[1], da.wire_code, aord == "big")
+        lz.ddt, lz.dbig = dd.wire_code, int(dord == "big")
         lz.keep = a_buf  # the source storage stays alive while the copy is pending
         lz.src_dtype, lz.dst_dtype, lz.src_order = da, dd, aord
+        lz.cext, lz.cdst, lz.csrc = tuple(plan.extents), tuple(plan.strides[0]), tuple(plan.strides[1])
+        lz.sbase, lz.soff, lz.sdt, lz.sbig = aptr, bases[1], da.wire_code, int(aord == "big")
         rt.before_write(dptr)
         rt.stats["lazy"] += 1
         with rt.lock:

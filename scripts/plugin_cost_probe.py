@@ -73,3 +73,43 @@ L.tpg_binary = lambda *a: 0
 print(f"wall, tpg_binary stubbed     {wall():7.2f} us/op")
 L.tpg_binary = real
 print(f"reference floor              {1e3 * bench._pipeline_floor(2000):7.2f} us/op")
+
+# host cost of the launch itself: tpg_binary through ctypes on a small
+# cfg2-shaped problem (same kernel path; the kernel is short so the launch
+# queue never fills), next to a bare ctypes call and an event record
+import ctypes as C  # noqa: E402
+from paper_1810_08723_b200 import abi  # noqa: E402
+
+n = 256
+Xs = tp.tensor_create((n, n), tp.int16, gpu)
+Rs = tp.tensor_create((1, n), tp.float, gpu)
+Os = tp.tensor_create((n, n), tp.float, gpu)
+xp, rp, op_ = (rt.address(t.storage.view()) for t in (Xs, Rs, Os))
+plan = abi.make_plan([n, n], [[4, 4 * n], [-2 * n, 2], [0, 4]])
+d = abi.make_operand(op_, 0, 10, False)
+a = abi.make_operand(xp, (n - 1) * 2 * n, 3, False)
+b = abi.make_operand(rp, 0, 10, False)
+args = (st.handle, 0, C.byref(plan), C.byref(d), C.byref(a), C.byref(b), 10, 0)
+
+
+def per_call(label, f, k=3000):
+    for _ in range(50):
+        f()
+    st.sync()
+    t0 = time.perf_counter()
+    for i in range(k):
+        f()
+        if i % 200 == 199:
+            st.sync()
+    st.sync()
+    print(f"{label:44s} {1e6 * (time.perf_counter() - t0) / k:7.2f} us/call")
+
+
+per_call("ctypes tpg_binary 256^2 cfg2 shape", lambda: L.tpg_binary(*args))
+per_call("ctypes tpg_last_error (bare call)", lambda: L.tpg_last_error())
+ev = C.c_void_p()
+L.tpg_event_create_untimed(C.byref(ev))
+per_call("ctypes tpg_event_record", lambda: L.tpg_event_record(ev, st.handle))
+per_call("ctypes tpg_event_query", lambda: L.tpg_event_query(ev))
+per_call("ctypes tpg_memset 4 B", lambda: L.tpg_memset(C.c_void_p(op_), 0, 4, st.handle))
+print("entries", rt.entries.counts())

@@ -201,13 +201,23 @@ static void blocks_del(BlockPool* p, void* ptr) {
     return;
   }
   if (PyDict_DelItem(p->blocks, k) < 0) PyErr_Clear();
-  /* a pending lazy copy into / out of this block is dead with it */
-  if (p->drop_lazy != Py_None &&
-      (PyDict_Contains(p->lazy, k) == 1 || PyDict_Contains(p->lazy_by_src, k) == 1)) {
-    PyObject* r = PyObject_CallOneArg(p->drop_lazy, k);
-    if (!r) PyErr_WriteUnraisable(p->drop_lazy);
-    Py_XDECREF(r);
+  /* a pending lazy copy INTO this block is dead with it (a pending copy
+   * keeps its source alive, so only destination records die here):
+   * tidepool_plugin._Runtime._drop_lazy_locked, in C */
+  PyObject* rec = PyDict_GetItemWithError(p->lazy, k);
+  if (rec) {
+    Py_INCREF(rec);
+    if (PyDict_DelItem(p->lazy, k) < 0) PyErr_Clear();
+    PyObject* src = PyObject_GetAttrString(rec, "src_ptr");
+    PyObject* set = src ? PyDict_GetItemWithError(p->lazy_by_src, src) : NULL;
+    if (set && PySet_Check(set)) {
+      if (PySet_Discard(set, k) < 0) PyErr_Clear();
+      if (PySet_GET_SIZE(set) == 0 && PyDict_DelItem(p->lazy_by_src, src) < 0) PyErr_Clear();
+    }
+    Py_XDECREF(src);
+    Py_DECREF(rec);
   }
+  PyErr_Clear();
   Py_DECREF(k);
 }
 
@@ -478,6 +488,81 @@ static PyObject* pool_allocate(BlockPool* p, PyObject* args) {
   return (PyObject*)b;
 }
 
+/* Device.allocate for one gpu device (devices.py:149-160 semantics:
+ * negative sizes raise AllocationError, alloc_count counts calls),
+ * installed as the device instance's `allocate` attribute. */
+typedef struct {
+  PyObject_HEAD
+  BlockPool* pool;
+  PyObject* device;
+  int index;
+} Allocator;
+
+static PyTypeObject AllocatorType;
+static PyObject *S_alloc_count, *ONE;
+
+static PyObject* allocator_call(Allocator* a, PyObject* args, PyObject* kw) {
+  Py_ssize_t n;
+  if (!PyArg_ParseTuple(args, "n", &n)) return NULL;
+  if (n < 0) {
+    PyErr_SetString(AllocError ? AllocError : PyExc_MemoryError, "negative allocation size");
+    return NULL;
+  }
+  PyObject* c = PyObject_GetAttr(a->device, S_alloc_count);
+  if (!c) return NULL;
+  PyObject* c1 = PyNumber_Add(c, ONE);
+  Py_DECREF(c);
+  if (!c1 || PyObject_SetAttr(a->device, S_alloc_count, c1) < 0) {
+    Py_XDECREF(c1);
+    return NULL;
+  }
+  Py_DECREF(c1);
+  PyObject* t = Py_BuildValue("(in)", a->index, n);
+  if (!t) return NULL;
+  PyObject* r = pool_allocate(a->pool, t);
+  Py_DECREF(t);
+  return r;
+}
+
+static void allocator_dealloc(Allocator* a) {
+  PyObject_GC_UnTrack(a);
+  Py_CLEAR(a->pool);
+  Py_CLEAR(a->device);
+  Py_TYPE(a)->tp_free((PyObject*)a);
+}
+
+static int allocator_traverse(Allocator* a, visitproc visit, void* arg) {
+  Py_VISIT(a->pool);
+  Py_VISIT(a->device);
+  return 0;
+}
+
+static int allocator_clear(Allocator* a) {
+  Py_CLEAR(a->pool);
+  Py_CLEAR(a->device);
+  return 0;
+}
+
+static PyObject* pool_allocator(BlockPool* p, PyObject* args) {
+  int dev;
+  PyObject* device;
+  if (!PyArg_ParseTuple(args, "iO", &dev, &device)) return NULL;
+  if (dev < 0 || dev >= MAX_DEV) {
+    PyErr_SetString(PyExc_ValueError, "device index out of range");
+    return NULL;
+  }
+  Allocator* a = PyObject_GC_New(Allocator, &AllocatorType);
+  if (!a) return NULL;
+  Py_INCREF(p);
+  a->pool = p;
+  /* device -> allocator -> device is a cycle; both are GC-tracked */
+  Py_INCREF(device);
+  a->device = device;
+  a->index = dev;
+  PyObject_GC_Track(a);
+  return (PyObject*)a;
+}
+
 static PyObject* pool_add_stream(BlockPool* p, PyObject* args) {
   int dev;
   PyObject* h;
@@ -535,6 +620,8 @@ static PyObject* pool_cached_bytes(BlockPool* p, PyObject* args) {
 static PyMethodDef pool_methods[] = {
     {"allocate", (PyCFunction)pool_allocate, METH_VARARGS, "allocate(device, nbytes) -> DevBuf"},
     {"add_stream", (PyCFunction)pool_add_stream, METH_VARARGS, "add_stream(device, handle)"},
+    {"allocator", (PyCFunction)pool_allocator, METH_VARARGS,
+     "allocator(device index, device object) -> callable(nbytes) (Device.allocate)"},
     {"bump", (PyCFunction)pool_bump, METH_NOARGS, "start a new launch epoch"},
     {"trim", (PyCFunction)pool_trim, METH_VARARGS, "trim(device, keep_bytes)"},
     {"stats", (PyCFunction)pool_stats, METH_NOARGS, "counters"},
@@ -1255,6 +1342,17 @@ PyMODINIT_FUNC PyInit__tpg_pyfast(void) {
   if (PyType_Ready(&BlockPoolType) < 0) return NULL;
 
   if (intern_names() < 0) return NULL;
+  if (!(S_alloc_count = PyUnicode_InternFromString("alloc_count"))) return NULL;
+  if (!(ONE = PyLong_FromLong(1))) return NULL;
+  AllocatorType.tp_name = "_tpg_pyfast.Allocator";
+  AllocatorType.tp_basicsize = sizeof(Allocator);
+  AllocatorType.tp_flags = Py_TPFLAGS_DEFAULT | Py_TPFLAGS_HAVE_GC;
+  AllocatorType.tp_doc = "Device.allocate of one gpu device";
+  AllocatorType.tp_call = (ternaryfunc)allocator_call;
+  AllocatorType.tp_dealloc = (destructor)allocator_dealloc;
+  AllocatorType.tp_traverse = (traverseproc)allocator_traverse;
+  AllocatorType.tp_clear = (inquiry)allocator_clear;
+  if (PyType_Ready(&AllocatorType) < 0) return NULL;
   EntriesType.tp_name = "_tpg_pyfast.Entries";
   EntriesType.tp_basicsize = sizeof(Entries);
   EntriesType.tp_flags = Py_TPFLAGS_DEFAULT | Py_TPFLAGS_HAVE_GC;

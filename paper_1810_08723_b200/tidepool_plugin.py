@@ -530,6 +530,9 @@ def register(tidepool_module, count: int | None = None, lib=None):
     class GpuDevice(ref_devices.Device):
         def __init__(self, index):
             super().__init__(gpu_type, index)
+            # Device.allocate in C (tpg_pyfast.c Allocator: the same checks
+            # and alloc_count accounting as allocate() below)
+            self.allocate = rt.pool.allocator(index, self)
 
         def default_stream(self):
             with self._lock:

@@ -336,3 +336,44 @@ def test_matmul_batched_extension_matches_reference_slices(env):
         gq = tp.apply_index(got, (slice(None), slice(None), q))
         assert all(_eq(x, y, 1e-12) for x, y in zip(tp.tensors.read_values(gq),
                                                    tp.tensors.read_values(want))), q
+
+
+def test_c_entry_fast_paths_match_the_python_entries(env):
+    """The C fast paths of the binary and lazy-copy entries
+    (hostsrc/tpg_pyfast.c) take the standard all-gpu calls and hand every
+    other call (error mode, profiling) to the Python entries before any side
+    effect; on random mixed-dtype / broadcast / reversed programs both paths
+    produce the same bytes as the cpu device."""
+    tp, gpu, fake, rt = env
+    rng = random.Random(29)
+    dts = [tp.int8, tp.int16, tp.uint16, tp.int32, tp.float, tp.double, tp.half]
+    ops = ["add", "subtract", "multiply", "minimum", "maximum"]
+    c0 = rt.entries.counts()
+    for it in range(24):
+        da, db = rng.choice(dts), rng.choice(dts)
+        r, c = rng.randint(1, 9), rng.randint(1, 9)
+        xa = [[rng.randint(-50, 50) for _ in range(c)] for _ in range(r)]
+        xb = [[rng.randint(-50, 50) for _ in range(c)]]  # broadcast row
+        A, B = tp.from_nested(xa, da), tp.from_nested(xb, db)
+        if rng.random() < 0.5:
+            A = tp.apply_index(A, (slice(None, None, -1), slice(None)))
+        op = getattr(tp, rng.choice(ops))
+        want = op(A, B)
+        Ag, Bg = tp.cast(A, device=gpu), tp.cast(B, device=gpu)
+        got_fast = op(Ag, Bg)
+        rt.profile = []          # profiling forces the Python entries
+        try:
+            got_py = op(Ag, Bg)
+        finally:
+            rt.profile = None
+        assert tp.tensors.read_values(got_fast) == tp.tensors.read_values(want), it
+        assert got_fast.storage.snapshot() == want.storage.snapshot(), it
+        assert got_py.storage.snapshot() == want.storage.snapshot(), it
+    c1 = rt.entries.counts()
+    assert c1["fast"] > c0["fast"]
+    # error mode goes to the Python entry (CastContext semantics live there)
+    x = _on(tp, gpu, [100, 100], tp.int8)
+    before = rt.entries.counts()["fallback"]
+    with pytest.raises(tp.errors.DomainError):
+        tp.add(x, x, mode="error")
+    assert rt.entries.counts()["fallback"] > before

@@ -1,6 +1,8 @@
 #!/bin/bash
 # A/B: epilogue accumulator-wait back-off (TPG_GEMM_EPI_SLEEP ns) vs spinning,
 # sustained cfg4 gemms with SM clock / power (scripts/gemm_vs_cublas.py).
+# (The TPG_GEMM_EPI_SLEEP switch existed only for this A/B; it was removed after it
+# showed no effect -- profiles/r02s_gemm_epilogue_backoff_ab.txt.)
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 for ns in 0 500 2000 0 500 2000; do

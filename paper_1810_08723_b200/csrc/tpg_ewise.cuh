@@ -867,7 +867,7 @@ bool launch_tile_tma(EwParams& p, Stream* st, int xi, int q, int64_t nt0, int64_
   // small per-thread cache: the host cost of an op is part of its e2e time)
   struct MapCache {
     const char* lo;
-    int64_t eq, e0, s0;
+    int64_t eq, e0, s0, sx;
     CUtensorMap map;
   };
   static thread_local MapCache cache[8];
@@ -875,7 +875,7 @@ bool launch_tile_tma(EwParams& p, Stream* st, int xi, int q, int64_t nt0, int64_
   const int64_t s0a = s0 < 0 ? -s0 : s0;
   const CUtensorMap* mp = nullptr;
   for (auto& c : cache)
-    if (c.lo == lo && c.eq == eq && c.e0 == e0 && c.s0 == s0a) mp = &c.map;
+    if (c.lo == lo && c.eq == eq && c.e0 == e0 && c.s0 == s0a && c.sx == SX) mp = &c.map;
   if (!mp) {
     auto enc = (PFN_cuTensorMapEncodeTiled_v12000)tensor_map_encoder();
     if (!enc) return false;
@@ -895,6 +895,7 @@ bool launch_tile_tma(EwParams& p, Stream* st, int xi, int q, int64_t nt0, int64_
     c.eq = eq;
     c.e0 = e0;
     c.s0 = s0a;
+    c.sx = SX;
     mp = &c.map;
   }
   const CUtensorMap& map = *mp;

@@ -220,6 +220,72 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+
+// product-like variant: runtime column stride (sdq bytes), each lane owns
+// one 16-B chunk (8 columns) of RG = TI/32 row groups, so one column address
+// serves RG stores (+128 B immediates); warps own chunks w, w+8, ...
+template <int TI, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+    k_tma_rg(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ R,
+             float* __restrict__ out, long sdq) {
+  constexpr int TJ = 64, RG = TI / 32;
+  constexpr int BOX_BYTES = TI * 128;
+  constexpr int STAGE_BYTES = BOX_BYTES;
+  constexpr int NTI = N / TI, NTJ = N / TJ, NT = NTI * NTJ;
+  extern __shared__ __align__(1024) uint8_t dyn[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)dyn + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full[STAGES];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto issue = [&](int t, int s) {
+    const int ti = t % NTI, tj = t / NTI;
+    mbar_expect(&full[s], STAGE_BYTES);
+    tma_load_2d(sm + s * STAGE_BYTES, &xmap, tj * TJ, N - (ti + 1) * TI, &full[s]);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int s = 0; s < STAGES; ++s) {
+      const int t = blockIdx.x + s * gridDim.x;
+      if (t < NT) issue(t, s);
+    }
+  const int c = warp;  // chunk
+  uint32_t soff[RG];
+#pragma unroll
+  for (int g = 0; g < RG; ++g) {
+    const int rl = TI - 1 - (32 * g + lane);
+    soff[g] = rl * 128 + ((c ^ (rl & 7)) << 4);
+  }
+  int k = 0;
+  for (int t = blockIdx.x; t < NT; t += gridDim.x, ++k) {
+    const int s = k % STAGES;
+    mbar_wait(&full[s], (k / STAGES) & 1);
+    const int ti = t % NTI, tj = t / NTI;
+    const uint8_t* st = sm + s * STAGE_BYTES;
+    uint4 v[RG];
+#pragma unroll
+    for (int g = 0; g < RG; ++g) v[g] = *(const uint4*)(st + soff[g]);
+    const int j0 = tj * TJ + 8 * c;
+    const float4 y0 = __ldg((const float4*)(R + j0));
+    const float4 y1 = __ldg((const float4*)(R + j0 + 4));
+    const float y[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+    char* dp = (char*)out + (size_t)j0 * sdq + (size_t)(ti * TI + lane) * 4;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float* col = (float*)(dp + q * sdq);
+#pragma unroll
+      for (int g = 0; g < RG; ++g) __stcs(col + 32 * g, (float)((const int16_t*)&v[g])[q] + y[q]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int tn = t + STAGES * gridDim.x;
+      if (tn < NT) issue(tn, s);
+    }
+  }
+}
+
 int main(int argc, char** argv) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -301,6 +367,28 @@ int main(int argc, char** argv) {
     maps(TI);                                                                               \
     timeit("tma-v4 " #TI "x" #TJ " stages" #S " ord" #ORD " cta/sm" #CPS,                   \
            [&](int r) { kern<<<sms * CPS, 256, smem>>>(xm[r], R, O[r]); });                 \
+  }
+#define RUNRG(TI, S, CPS)                                                                    \
+  {                                                                                         \
+    auto kern = k_tma_rg<TI, S>;                                                            \
+    const int smem = S * TI * 128 + 1024;                                                   \
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));      \
+    maps(TI);                                                                               \
+    timeit("rg " #TI "x64 stages" #S " cta/sm" #CPS " (runtime stride)",                    \
+           [&](int r) { kern<<<sms * CPS, 256, smem>>>(xm[r], R, O[r], (long)N * 4); });    \
+  }
+  if (argc > 1 && argv[1][0] == '4') {  // sweep 4: row groups per lane, runtime stride
+    RUNRG(64, 6, 4);
+    RUNRG(128, 6, 2);
+    RUNRG(128, 5, 2);
+    RUNRG(128, 4, 3);
+    RUNRG(128, 3, 4);
+    RUNRG(256, 3, 2);
+    RUNRG(256, 6, 1);
+    RUNRG(64, 5, 5);
+    RUNRG(64, 6, 4);
+    RUN(64, 64, 6, 0, 1, 4);
+    return 0;
   }
   if (argc > 1 && argv[1][0] == '3') {  // sweep 3: deeper rings
     RUN(64, 64, 6, 0, 1, 4);

@@ -412,7 +412,7 @@ def bench_cfg2(L, steps, warmup, dev=0):
             "launches": steps + launches[0]}
 
 
-def bench_plugin(L, steps=20, warmup=3):
+def bench_plugin(L, steps=400, warmup=30):
     """cfg2 through the UNMODIFIED reference `tidepool` with the gpu table
     registered (the north_star drop-in): `tidepool.add(V, R)` on gpu0, where
     the reference pipeline converts V int16 -> float (ops._dtype_convert)
@@ -421,7 +421,8 @@ def bench_plugin(L, steps=20, warmup=3):
     reference pipeline's own host cost with a no-op table (the floor of any
     table implementation), and an e2e step from host numpy data to a host
     result through the reference API.  Skipped when the reference is not
-    importable (baseline/_ref)."""
+    importable (baseline/_ref).  The warm-up covers the block cache's
+    ramp-up (up to 8 blocks per size class in flight)."""
     sys.path.insert(0, str(ROOT / "tests"))
     import ref_loader
     tp = ref_loader.load("tidepool_bench_plugin")

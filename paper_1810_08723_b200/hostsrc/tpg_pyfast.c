@@ -8,8 +8,7 @@
  * device's allocate + release cost ~9 us per storage on the box
  * (profiles/r02s_plugin_cost_probe.txt); here they are a few hundred ns.
  *
- *   BlockPool(fns, blocks, lazy, lazy_by_src, drop_lazy, cache_bytes,
- *             max_pending)
+ *   BlockPool(fns, blocks, lazy, lazy_by_src, cache_bytes, max_pending)
  *     fns = addresses of tpg_malloc_managed, tpg_free_managed,
  *           tpg_event_create_untimed, tpg_event_record, tpg_event_query,
  *           tpg_event_sync (include/tidepool_gpu.h)
@@ -87,7 +86,6 @@ typedef struct {
   PyObject* blocks;       /* dict ptr -> (device, cap) */
   PyObject* lazy;         /* dict dst ptr -> record */
   PyObject* lazy_by_src;  /* dict src ptr -> set */
-  PyObject* drop_lazy;    /* callable(ptr) */
   long long cache_limit;
   int max_pending;
   uint64_t seq;
@@ -379,11 +377,11 @@ static PyGetSetDef devbuf_getset[] = {
 /* ------------------------------------------------------------- BlockPool */
 
 static int pool_init(BlockPool* p, PyObject* args, PyObject* kw) {
-  PyObject *fns, *blocks, *lazy, *lbs, *drop;
+  PyObject *fns, *blocks, *lazy, *lbs;
   long long limit;
   int maxp;
-  if (!PyArg_ParseTuple(args, "OO!O!O!OLi", &fns, &PyDict_Type, &blocks, &PyDict_Type, &lazy,
-                        &PyDict_Type, &lbs, &drop, &limit, &maxp))
+  if (!PyArg_ParseTuple(args, "OO!O!O!Li", &fns, &PyDict_Type, &blocks, &PyDict_Type, &lazy,
+                        &PyDict_Type, &lbs, &limit, &maxp))
     return -1;
   if (!PyTuple_Check(fns) || PyTuple_GET_SIZE(fns) != 6) {
     PyErr_SetString(PyExc_TypeError, "fns: 6 function addresses");
@@ -406,11 +404,9 @@ static int pool_init(BlockPool* p, PyObject* args, PyObject* kw) {
   Py_INCREF(blocks);
   Py_INCREF(lazy);
   Py_INCREF(lbs);
-  Py_INCREF(drop);
   p->blocks = blocks;
   p->lazy = lazy;
   p->lazy_by_src = lbs;
-  p->drop_lazy = drop;
   p->cache_limit = limit;
   p->max_pending = maxp;
   return 0;
@@ -420,7 +416,6 @@ static int pool_traverse(BlockPool* p, visitproc visit, void* arg) {
   Py_VISIT(p->blocks);
   Py_VISIT(p->lazy);
   Py_VISIT(p->lazy_by_src);
-  Py_VISIT(p->drop_lazy);
   return 0;
 }
 
@@ -428,7 +423,6 @@ static int pool_clear(BlockPool* p) {
   Py_CLEAR(p->blocks);
   Py_CLEAR(p->lazy);
   Py_CLEAR(p->lazy_by_src);
-  Py_CLEAR(p->drop_lazy);
   return 0;
 }
 

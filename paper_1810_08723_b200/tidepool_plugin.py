@@ -308,7 +308,7 @@ class _Runtime:
         fast.set_allocation_error(tp.errors.AllocationError)
         fns, self._pool_callbacks = _pool_functions(L)
         self.pool = fast.BlockPool(fns, self.blocks, self.lazy, self.lazy_by_src,
-                                   self._drop_lazy, self.CACHE_BYTES, self.MAX_PENDING)
+                                   self.CACHE_BYTES, self.MAX_PENDING)
         self.DevBuf = fast.DevBuf
         self.defaults: dict = {}     # device -> its default GpuStream (rt.current)
         self.event_pool: list = []   # timing events (profile hook)
@@ -335,12 +335,6 @@ class _Runtime:
         without synchronising, e.g. tensor_from_nested / scalar_tensor,
         tensors.py:221-243, 269-280)."""
         return self.pool.allocate(device, nbytes)
-
-    def _drop_lazy(self, ptr):
-        """Pool callback when a block whose pointer has a pending lazy copy
-        (as destination or source) is freed."""
-        with self.lock:  # (a pending copy keeps its source alive: only dst records die here)
-            self._drop_lazy_locked(ptr)
 
     def _new_timing_event(self):
         ev = C.c_void_p()

@@ -377,3 +377,35 @@ def test_c_entry_fast_paths_match_the_python_entries(env):
     with pytest.raises(tp.errors.DomainError):
         tp.add(x, x, mode="error")
     assert rt.entries.counts()["fallback"] > before
+
+
+def test_threads_share_the_drop_in(env):
+    """Several Python threads run reference ops on gpu0 at once (the C entry
+    paths, the lazy-cast records and the block pool are shared state under
+    the GIL; a recycled block waits for its last GPU use): every result
+    equals the cpu device's."""
+    import threading
+    tp, gpu, fake, rt = env
+    errors = []
+
+    def worker(seed):
+        try:
+            rng = random.Random(seed)
+            for it in range(15):
+                n = rng.randint(1, 40)
+                xs = [[rng.randint(-99, 99) for _ in range(n)] for _ in range(3)]
+                row = [[rng.uniform(-2, 2) for _ in range(n)]]
+                X, R = tp.from_nested(xs, tp.int16), tp.from_nested(row, tp.float)
+                want = tp.multiply(tp.add(X, R), R)
+                Xg, Rg = tp.cast(X, device=gpu), tp.cast(R, device=gpu)
+                got = tp.multiply(tp.add(Xg, Rg), Rg)
+                if got.storage.snapshot() != want.storage.snapshot():
+                    errors.append((seed, it))
+        except Exception as exc:  # noqa: BLE001 - reported below
+            errors.append((seed, repr(exc)))
+    ts = [threading.Thread(target=worker, args=(s,)) for s in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors[:3]

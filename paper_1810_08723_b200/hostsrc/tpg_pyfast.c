@@ -45,6 +45,17 @@ typedef int (*f_ev_sync)(void*);
 
 #define MAX_DEV 64
 
+#include <time.h>
+/* host-time counters of the C paths (pool allocate / release, binary and
+ * copy entries): exposed by counters() so the per-op host cost can be split
+ * exactly (scripts/plugin_cost_probe.py) */
+static long long T_alloc, T_release, T_binary, T_copy, T_launch;
+static inline long long now_ns(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (long long)ts.tv_sec * 1000000000ll + ts.tv_nsec;
+}
+
 typedef struct Marker {
   void* ev;
   long refs;
@@ -267,7 +278,13 @@ static void* take(BlockPool* p, int dev, size_t cap) {
 
 /* ---------------------------------------------------------------- DevBuf */
 
+static void release_block_(BlockPool* p, void* ptr, size_t cap, int dev);
 static void release_block(BlockPool* p, void* ptr, size_t cap, int dev) {
+  const long long t0 = now_ns();
+  release_block_(p, ptr, cap, dev);
+  T_release += now_ns() - t0;
+}
+static void release_block_(BlockPool* p, void* ptr, size_t cap, int dev) {
   p->n_release++;
   blocks_del(p, ptr);
   SizeClass* c = find_class(p, dev, cap, 1);
@@ -433,7 +450,14 @@ static void pool_dealloc(BlockPool* p) {
   Py_TYPE(p)->tp_free((PyObject*)p);
 }
 
+static PyObject* pool_allocate_(BlockPool* p, PyObject* args);
 static PyObject* pool_allocate(BlockPool* p, PyObject* args) {
+  const long long t0 = now_ns();
+  PyObject* r = pool_allocate_(p, args);
+  T_alloc += now_ns() - t0;
+  return r;
+}
+static PyObject* pool_allocate_(BlockPool* p, PyObject* args) {
   int dev;
   Py_ssize_t n;
   if (!PyArg_ParseTuple(args, "in", &dev, &n)) return NULL;
@@ -755,6 +779,22 @@ static int closure_cells(Entries* e, PyObject* fn, PyObject* tag, PyObject* cons
   PyObject* clos = PyFunction_GET_CLOSURE(fn);
   if (!clos) return -1;
   PyObject* code = PyFunction_GET_CODE(fn);
+  /* small front cache keyed by object identity (entries hold references,
+   * so a cached code object cannot be freed and its address reused) */
+  static struct {
+    PyObject *code, *tag;
+    int n;
+    long at[4];
+  } fc[16];
+  const unsigned h = (unsigned)(((uintptr_t)code >> 4) ^ ((uintptr_t)tag >> 4)) & 15u;
+  if (fc[h].code == code && fc[h].tag == tag && fc[h].n == n) {
+    for (int k = 0; k < n; ++k) {
+      const long at = fc[h].at[k];
+      out[k] = (at >= 0 && at < PyTuple_GET_SIZE(clos)) ? PyCell_GET(PyTuple_GET_ITEM(clos, at))
+                                                         : NULL;
+    }
+    return 0;
+  }
   PyObject* key = PyTuple_Pack(2, code, tag);
   if (!key) return -2;
   PyObject* idx = PyDict_GetItemWithError(e->cell_idx, key);
@@ -784,8 +824,14 @@ static int closure_cells(Entries* e, PyObject* fn, PyObject* tag, PyObject* cons
     Py_DECREF(idx); /* the dict holds it */
   }
   Py_DECREF(key);
+  if (n <= 4) {
+    Py_XSETREF(fc[h].code, (Py_INCREF(code), code));
+    Py_XSETREF(fc[h].tag, (Py_INCREF(tag), tag));
+    fc[h].n = n;
+  }
   for (int k = 0; k < n; ++k) {
     long at = PyLong_AsLong(PyTuple_GET_ITEM(idx, k));
+    if (n <= 4) fc[h].at[k] = at;
     out[k] = (at >= 0 && at < PyTuple_GET_SIZE(clos))
                  ? PyCell_GET(PyTuple_GET_ITEM(clos, at))
                  : NULL;
@@ -907,7 +953,14 @@ static int fuse(PyObject* lz, int nd, const int64_t* bext, const int64_t* bstr, 
   return 0;
 }
 
+static PyObject* entries_binary_(Entries* e, PyObject* const* args, Py_ssize_t nargs);
 static PyObject* entries_binary(Entries* e, PyObject* const* args, Py_ssize_t nargs) {
+  const long long t0 = now_ns();
+  PyObject* r = entries_binary_(e, args, nargs);
+  T_binary += now_ns() - t0;
+  return r;
+}
+static PyObject* entries_binary_(Entries* e, PyObject* const* args, Py_ssize_t nargs) {
   if (nargs != 10) {
     PyErr_SetString(PyExc_TypeError, "binary(op, plan, d_buf, store, a_buf, a_unpack, b_buf, "
                                      "b_unpack, fn, bases)");
@@ -1045,7 +1098,9 @@ static PyObject* entries_binary(Entries* e, PyObject* const* args, Py_ssize_t na
     for (int v = 0; v < 3; ++v) p.stride[v][i] = str[v][i];
   }
   e->pool->seq++; /* rt.current(): a new launch epoch */
+  const long long tl = now_ns();
   int rc = e->binary(handle, op, &p, &od, &oa, &ob, ca.compute, 0);
+  T_launch += now_ns() - tl;
   e->n_fast++;
   if (nfused) {
     PyObject* c = PyObject_GetItem(e->stats, S_fused);
@@ -1059,6 +1114,109 @@ static PyObject* entries_binary(Entries* e, PyObject* const* args, Py_ssize_t na
   }
   return PyLong_FromLong(rc);
 #undef FALLBACK
+}
+
+static PyObject* entries_copy(Entries* e, PyObject* const* args, Py_ssize_t nargs);
+
+/* A gpu table entry callable in C: tries the fast path (when the plugin's
+ * profiling hook is off) and otherwise calls the Python entry `slow` with
+ * the same arguments.  kind 0 = binary (9 table arguments), 1 = copy (7). */
+typedef struct {
+  PyObject_HEAD
+  Entries* e;
+  int kind;
+  PyObject* opobj; /* binary op code */
+  PyObject* slow;
+} FastEntry;
+
+static PyTypeObject FastEntryType;
+static PyObject *S_profile, *S_check, *S_kernel;
+
+static PyObject* fastentry_call(FastEntry* f, PyObject* args, PyObject* kw) {
+  if ((!kw || (PyDict_Check(kw) && PyDict_GET_SIZE(kw) == 0)) && PyTuple_Check(args)) {
+    PyObject* prof = PyObject_GetAttr(f->e->rt, S_profile);
+    const int off = prof == Py_None;
+    if (!prof) PyErr_Clear();
+    Py_XDECREF(prof);
+    const Py_ssize_t n = PyTuple_GET_SIZE(args);
+    PyObject* r = NULL;
+    int tried = 0;
+    if (off && f->kind == 0 && n == 9) {
+      PyObject* a[10];
+      a[0] = f->opobj;
+      for (int i = 0; i < 9; ++i) a[i + 1] = PyTuple_GET_ITEM(args, i);
+      r = entries_binary(f->e, a, 10);
+      tried = 1;
+    } else if (off && f->kind == 1 && n == 7) {
+      r = entries_copy(f->e, ((PyTupleObject*)args)->ob_item, 7);
+      tried = 1;
+    }
+    if (tried) {
+      if (!r) return NULL;
+      if (r != Py_None) {
+        if (f->kind == 0) {
+          const long rc = PyLong_AsLong(r);
+          Py_DECREF(r);
+          if (rc) {
+            PyObject* rco = PyLong_FromLong(rc);
+            PyObject* res = rco ? PyObject_CallMethodObjArgs(f->e->rt, S_check, rco, S_kernel, NULL)
+                                : NULL;
+            Py_XDECREF(rco);
+            return res;  /* rt.check raises the reference's DeviceError */
+          }
+          Py_RETURN_NONE;
+        }
+        Py_DECREF(r);
+        Py_RETURN_NONE;  /* copy recorded */
+      }
+      Py_DECREF(r);
+    }
+  }
+  return PyObject_Call(f->slow, args, kw);
+}
+
+static void fastentry_dealloc(FastEntry* f) {
+  PyObject_GC_UnTrack(f);
+  Py_CLEAR(f->e);
+  Py_CLEAR(f->opobj);
+  Py_CLEAR(f->slow);
+  Py_TYPE(f)->tp_free((PyObject*)f);
+}
+static int fastentry_traverse(FastEntry* f, visitproc visit, void* arg) {
+  Py_VISIT(f->e);
+  Py_VISIT(f->opobj);
+  Py_VISIT(f->slow);
+  return 0;
+}
+static int fastentry_clear(FastEntry* f) {
+  Py_CLEAR(f->e);
+  Py_CLEAR(f->opobj);
+  Py_CLEAR(f->slow);
+  return 0;
+}
+
+static PyObject* entries_entry(Entries* e, PyObject* args) {
+  int kind, op;
+  PyObject* slow;
+  if (!PyArg_ParseTuple(args, "iiO", &kind, &op, &slow)) return NULL;
+  if (kind != 0 && kind != 1) {
+    PyErr_SetString(PyExc_ValueError, "kind: 0 binary, 1 copy");
+    return NULL;
+  }
+  FastEntry* f = PyObject_GC_New(FastEntry, &FastEntryType);
+  if (!f) return NULL;
+  Py_INCREF(e);
+  f->e = e;
+  f->kind = kind;
+  f->opobj = PyLong_FromLong(op);
+  Py_INCREF(slow);
+  f->slow = slow;
+  PyObject_GC_Track(f);
+  if (!f->opobj) {
+    Py_DECREF(f);
+    return NULL;
+  }
+  return (PyObject*)f;
 }
 
 static PyObject* entries_set_default(Entries* e, PyObject* args) {
@@ -1081,7 +1239,14 @@ static PyObject* entries_set_default(Entries* e, PyObject* args) {
  * mode, a lossless dtype change from a gpu source into a fresh dense gpu
  * destination of the same device, neither with a pending copy.  Returns
  * True when recorded, None when the Python entry must handle the call. */
+static PyObject* entries_copy_(Entries* e, PyObject* const* args, Py_ssize_t nargs);
 static PyObject* entries_copy(Entries* e, PyObject* const* args, Py_ssize_t nargs) {
+  const long long t0 = now_ns();
+  PyObject* r = entries_copy_(e, args, nargs);
+  T_copy += now_ns() - t0;
+  return r;
+}
+static PyObject* entries_copy_(Entries* e, PyObject* const* args, Py_ssize_t nargs) {
   if (nargs != 7) {
     PyErr_SetString(PyExc_TypeError, "copy(plan, d_buf, store, a_buf, a_unpack, fn, bases)");
     return NULL;
@@ -1245,7 +1410,9 @@ static PyObject* entries_copy(Entries* e, PyObject* const* args, Py_ssize_t narg
 }
 
 static PyObject* entries_counts(Entries* e, PyObject* unused) {
-  return Py_BuildValue("{s:L,s:L}", "fast", e->n_fast, "fallback", e->n_fallback);
+  return Py_BuildValue("{s:L,s:L,s:L,s:L,s:L,s:L,s:L}", "fast", e->n_fast, "fallback",
+                       e->n_fallback, "ns_allocate", T_alloc, "ns_release", T_release,
+                       "ns_binary", T_binary, "ns_copy", T_copy, "ns_launch", T_launch);
 }
 
 static PyMethodDef entries_methods[] = {
@@ -1258,6 +1425,8 @@ static PyMethodDef entries_methods[] = {
     {"set_copy_support", (PyCFunction)entries_set_copy_support, METH_VARARGS,
      "set_copy_support(lazy class, {codec fn: (dtype, order)}, lossless table bytes)"},
     {"counts", (PyCFunction)entries_counts, METH_NOARGS, "fast / fallback call counts"},
+    {"entry", (PyCFunction)entries_entry, METH_VARARGS,
+     "entry(kind, op code, python entry) -> table callable (kind 0 binary, 1 copy)"},
     {NULL}};
 
 static int intern_names(void) {
@@ -1358,6 +1527,18 @@ PyMODINIT_FUNC PyInit__tpg_pyfast(void) {
   EntriesType.tp_clear = (inquiry)entries_clear;
   EntriesType.tp_methods = entries_methods;
   if (PyType_Ready(&EntriesType) < 0) return NULL;
+  if (!(S_profile = PyUnicode_InternFromString("profile"))) return NULL;
+  if (!(S_check = PyUnicode_InternFromString("check"))) return NULL;
+  if (!(S_kernel = PyUnicode_InternFromString("kernel"))) return NULL;
+  FastEntryType.tp_name = "_tpg_pyfast.FastEntry";
+  FastEntryType.tp_basicsize = sizeof(FastEntry);
+  FastEntryType.tp_flags = Py_TPFLAGS_DEFAULT | Py_TPFLAGS_HAVE_GC;
+  FastEntryType.tp_doc = "gpu table entry: C fast path, Python entry otherwise";
+  FastEntryType.tp_call = (ternaryfunc)fastentry_call;
+  FastEntryType.tp_dealloc = (destructor)fastentry_dealloc;
+  FastEntryType.tp_traverse = (traverseproc)fastentry_traverse;
+  FastEntryType.tp_clear = (inquiry)fastentry_clear;
+  if (PyType_Ready(&FastEntryType) < 0) return NULL;
 
   PyObject* m = PyModule_Create(&moddef);
   if (!m) return NULL;

@@ -480,14 +480,12 @@ def register(tidepool_module, count: int | None = None, lib=None):
                    for f, (d, order) in codec_of.items()}
     rt.entries = _fast_module().Entries(rt.pool, _binary_function(L, abi), rt, rt.tls, rt.lazy,
                                         rt.lazy_by_src, fast_codecs, rt.stats)
-    fast_binary = rt.entries.binary
     lossless_table = bytearray(32 * 32)
     for a_ in ref_dtypes.ALL_DTYPES:
         for b_ in ref_dtypes.ALL_DTYPES:
             lossless_table[a_.wire_code * 32 + b_.wire_code] = \
                 int(bool(ref_dtypes.lossless_castable(a_, b_)))
     rt.entries.set_copy_support(_Lazy, dict(codec_of), bytes(lossless_table))
-    fast_copy = rt.entries.copy
 
     # -- devices and streams ------------------------------------------------------
     class GpuStream(ref_devices.Stream):
@@ -678,13 +676,6 @@ def register(tidepool_module, count: int | None = None, lib=None):
         code = abi.BINARY_CODE[op]
 
         def h(plan, d_buf, store, a_buf, a_unpack, b_buf, b_unpack, fn, bases):
-            if rt.profile is None:  # C fast path (standard mode, all-gpu operands)
-                rc = fast_binary(code, plan, d_buf, store, a_buf, a_unpack, b_buf, b_unpack, fn,
-                                 bases)
-                if rc is not None:
-                    if rc:
-                        rt.check(rc, "kernel")
-                    return
             dd, dord, mode, ctx = _store(store)
             da, aord = _codec(a_unpack)
             db, bord = _codec(b_unpack)
@@ -722,15 +713,14 @@ def register(tidepool_module, count: int | None = None, lib=None):
             _run(st, mode, ctx, dd, lambda: L.tpg_binary(*args), lambda: L.tpg_binary_check(*args))
             temps.done()
         h.__name__ = f"gpu_{op}"
-        return h
+        # the table entry: C fast path (standard mode, gpu operands of one
+        # device; tpg_pyfast.c FastEntry), this Python entry otherwise
+        return rt.entries.entry(0, code, h)
 
     def unary(op):
         code = abi.UNARY_CODE[op]
 
         def h(plan, d_buf, store, a_buf, a_unpack, fn, bases):
-            if op == "identity" and rt.profile is None and \
-                    fast_copy(plan, d_buf, store, a_buf, a_unpack, fn, bases):
-                return  # recorded as a lazy cast (tpg_pyfast.c: the _try_lazy rule)
             dd, dord, mode, ctx = _store(store)
             da, aord = _codec(a_unpack)
             dptr, aptr = rt.address(d_buf), rt.address(a_buf)
@@ -976,7 +966,9 @@ def register(tidepool_module, count: int | None = None, lib=None):
     for op in abi.UNARY_CODE:
         if op != "identity":
             table[op] = unary(op)
-    table["copy"] = unary("identity")
+    # copy: lossless gpu->gpu conversions are recorded in C (the _try_lazy
+    # rule, tpg_pyfast.c FastEntry kind 1), everything else in Python
+    table["copy"] = rt.entries.entry(1, 0, unary("identity"))
     for op in abi.REDUCE_CODE:
         table[f"reduce_{op}" if op in ("minimum", "maximum") else op] = reduce_(op)
     table.update(matmul=matmul, fill=fill, arange=arange, byteswap=byteswap, gather=gather,

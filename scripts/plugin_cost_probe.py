@@ -40,7 +40,13 @@ def wall(n=3000):
     return 1e6 * (time.perf_counter() - t0) / n
 
 
-print(f"wall                         {wall():7.2f} us/op")
+print(f"wall (first 3000 calls)      {wall():7.2f} us/op")
+c0 = rt.entries.counts()
+n0 = 3000
+print(f"wall (steady state)          {wall(n0):7.2f} us/op")
+c1 = rt.entries.counts()
+for k in ("ns_allocate", "ns_release", "ns_binary", "ns_copy", "ns_launch"):
+    print(f"  C {k[3:]:24s} {(c1[k] - c0[k]) / 1e3 / (n0 + 50):7.2f} us/op")
 acc = {}
 
 

@@ -158,6 +158,15 @@ int tpg_free_managed(void* ptr);
 /* completion tracking for recycled blocks: 0 = complete, 1 = pending */
 int tpg_event_create_untimed(tpg_event* ev);
 int tpg_event_query(tpg_event ev);
+/* completion words (the drop-in's block cache checks reuse without a
+ * cudaEventQuery per allocation): a 64-bit word in pinned, device-mapped
+ * host memory that tpg_stream_mark sets to `value` in stream order, after
+ * all earlier work of the stream has completed (cuStreamWriteValue64).
+ * tpg_stream_mark returns TPG_E_UNSUPPORTED where stream memory operations
+ * are unavailable (the caller then uses events). */
+int tpg_mark_word_create(uint64_t** word);
+int tpg_mark_word_free(uint64_t* word);
+int tpg_stream_mark(tpg_stream stream, uint64_t* word, uint64_t value);
 
 /* Peer access between all visible device pairs that support it (NVLink /
  * NVSwitch); *enabled = number of (a, b) pairs enabled. */

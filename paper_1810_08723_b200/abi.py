@@ -109,6 +109,9 @@ PROTOTYPES = {
     "tpg_free_managed": (_i32, [_vp]),
     "tpg_event_create_untimed": (_i32, [P(_vp)]),
     "tpg_event_query": (_i32, [_vp]),
+    "tpg_mark_word_create": (_i32, [P(_vp)]),
+    "tpg_mark_word_free": (_i32, [_vp]),
+    "tpg_stream_mark": (_i32, [_vp, _vp, C.c_uint64]),
     "tpg_l2_flush": (_i32, [_vp, C.c_size_t, _vp]),
     "tpg_enable_peer_all": (_i32, [P(C.c_int)]),
     "tpg_graph_begin": (_i32, [_vp]),

@@ -8,6 +8,7 @@
 // overtake in-flight kernels, so frees are stream-ordered (cudaFreeAsync
 // into the device's memory pool, whose release threshold keeps freed
 // blocks cached for reuse: a caching allocator with stream semantics).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <string.h>
@@ -480,6 +481,50 @@ int tpg_event_create_untimed(tpg_event* ev) {
   cudaEvent_t e;
   TPG_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   *ev = (tpg_event)e;
+  return TPG_OK;
+}
+
+int tpg_mark_word_create(uint64_t** word) {
+  if (!word) return arg_fail("null word");
+  void* p = nullptr;
+  TPG_CUDA_CHECK(cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(p, 0, 64);
+  *word = (uint64_t*)p;
+  return TPG_OK;
+}
+
+int tpg_mark_word_free(uint64_t* word) {
+  if (word) TPG_CUDA_CHECK(cudaFreeHost(word));
+  return TPG_OK;
+}
+
+int tpg_stream_mark(tpg_stream stream, uint64_t* word, uint64_t value) {
+  Stream* st = resolve_stream(stream);
+  if (!st) return arg_fail("no stream");
+  if (!word) return arg_fail("null word");
+  void* dptr = nullptr;
+  if (cudaHostGetDevicePointer(&dptr, word, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return TPG_E_UNSUPPORTED;
+  }
+  // the driver entry point is resolved at run time (no link-time libcuda
+  // dependency: the library still loads on a CPU-only host)
+  typedef CUresult (*WriteValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+  static WriteValue64 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (WriteValue64)f;
+  }
+  if (!fn) return TPG_E_UNSUPPORTED;
+  const CUresult r = fn((CUstream)st->s, (CUdeviceptr)dptr, (cuuint64_t)value,
+                        CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) return TPG_E_UNSUPPORTED;
   return TPG_OK;
 }
 

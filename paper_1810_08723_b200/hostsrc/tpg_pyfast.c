@@ -42,6 +42,8 @@ typedef int (*f_ev_create)(void**);
 typedef int (*f_ev_record)(void*, void*);
 typedef int (*f_ev_query)(void*);
 typedef int (*f_ev_sync)(void*);
+typedef int (*f_mark_create)(uint64_t**);
+typedef int (*f_mark)(void*, uint64_t*, uint64_t);
 
 #define MAX_DEV 64
 
@@ -57,7 +59,8 @@ static inline long long now_ns(void) {
 }
 
 typedef struct Marker {
-  void* ev;
+  void* ev;      /* event marker (NULL for a completion-word marker) */
+  uint64_t wval; /* completion-word marker: done once the stream's word >= wval */
   long refs;
   uint64_t seq; /* launch epoch it was recorded in */
   int dev, sidx; /* owning stream */
@@ -68,6 +71,9 @@ typedef struct {
   Marker* marker;    /* newest marker recorded on the stream (NULL once freed) */
   uint64_t marker_seq;
   uint64_t done_seq; /* every marker of this stream with seq <= done_seq completed */
+  volatile uint64_t* word; /* completion word (tpg_stream_mark), or NULL: events */
+  uint64_t wnext;
+  int wdisabled; /* tpg_stream_mark failed once: new markers use events */
 } StreamRec;
 
 typedef struct {
@@ -94,6 +100,8 @@ typedef struct {
   f_ev_record ev_record;
   f_ev_query ev_query;
   f_ev_sync ev_sync;
+  f_mark_create mark_create; /* optional (NULL: event markers only) */
+  f_mark mark;
   PyObject* blocks;       /* dict ptr -> (device, cap) */
   PyObject* lazy;         /* dict dst ptr -> record */
   PyObject* lazy_by_src;  /* dict src ptr -> set */
@@ -151,15 +159,17 @@ static void unref_markers(BlockPool* p, Entry* e) {
     for (int d = 0; d < MAX_DEV; ++d)
       for (int s = 0; s < p->nstreams[d]; ++s)
         if (p->streams[d][s].marker == m) p->streams[d][s].marker = NULL;
-    if (p->nevpool == p->aevpool) {
-      size_t na = p->aevpool ? 2 * p->aevpool : 64;
-      void** nv = (void**)realloc(p->evpool, na * sizeof(void*));
-      if (nv) {
-        p->evpool = nv;
-        p->aevpool = na;
+    if (m->ev) {
+      if (p->nevpool == p->aevpool) {
+        size_t na = p->aevpool ? 2 * p->aevpool : 64;
+        void** nv = (void**)realloc(p->evpool, na * sizeof(void*));
+        if (nv) {
+          p->evpool = nv;
+          p->aevpool = na;
+        }
       }
+      if (p->nevpool < p->aevpool) p->evpool[p->nevpool++] = m->ev;
     }
-    if (p->nevpool < p->aevpool) p->evpool[p->nevpool++] = m->ev;
     free(m);
   }
   free(e->evs);
@@ -176,6 +186,10 @@ static int entry_done(BlockPool* p, Entry* e) {
   for (int i = 0; i < e->nev; ++i) {
     Marker* m = e->evs[i];
     StreamRec* st = &p->streams[m->dev][m->sidx];
+    if (m->wval) { /* completion word: a host memory read, no CUDA call */
+      if (*st->word >= m->wval) continue;
+      return 0;
+    }
     if (m->seq <= st->done_seq && st->done_seq != (uint64_t)-1) continue;
     Marker* nw = st->marker;
     if (nw && nw != m && nw->seq > m->seq && p->ev_query(nw->ev) == 0) {
@@ -190,7 +204,18 @@ static int entry_done(BlockPool* p, Entry* e) {
 
 static void entry_wait(BlockPool* p, Entry* e) {
   Py_BEGIN_ALLOW_THREADS
-  for (int i = 0; i < e->nev; ++i) p->ev_sync(e->evs[i]->ev);
+  for (int i = 0; i < e->nev; ++i) {
+    Marker* m = e->evs[i];
+    if (m->wval) {
+      volatile uint64_t* w = p->streams[m->dev][m->sidx].word;
+      while (*w < m->wval) {
+        struct timespec ts = {0, 20000};
+        nanosleep(&ts, NULL);
+      }
+    } else {
+      p->ev_sync(m->ev);
+    }
+  }
   Py_END_ALLOW_THREADS
 }
 
@@ -297,16 +322,27 @@ static void release_block_(BlockPool* p, void* ptr, size_t cap, int dev) {
       if (!st->marker || st->marker_seq != p->seq) {
         Marker* m = (Marker*)calloc(1, sizeof(Marker));
         if (!m) break;
-        if (p->nevpool) {
-          m->ev = p->evpool[--p->nevpool];
-        } else if (p->ev_create(&m->ev) != 0) {
-          free(m);
-          break;
-        }
         m->seq = p->seq;
         m->dev = dev;
         m->sidx = s;
-        p->ev_record(m->ev, st->handle);
+        if (st->word && !st->wdisabled) {
+          m->wval = st->wnext + 1;
+          if (p->mark(st->handle, (uint64_t*)st->word, m->wval) == 0) {
+            st->wnext = m->wval;
+          } else {
+            m->wval = 0; /* no stream memory ops: events from now on */
+            st->wdisabled = 1;
+          }
+        }
+        if (!m->wval) {
+          if (p->nevpool) {
+            m->ev = p->evpool[--p->nevpool];
+          } else if (p->ev_create(&m->ev) != 0) {
+            free(m);
+            break;
+          }
+          p->ev_record(m->ev, st->handle);
+        }
         st->marker = m;
         st->marker_seq = p->seq;
       }
@@ -315,9 +351,7 @@ static void release_block_(BlockPool* p, void* ptr, size_t cap, int dev) {
     }
   }
   if (!c) { /* out of host memory: drop the block */
-    Py_BEGIN_ALLOW_THREADS
-    for (int i = 0; i < e.nev; ++i) p->ev_sync(e.evs[i]->ev);
-    Py_END_ALLOW_THREADS
+    entry_wait(p, &e);
     unref_markers(p, &e);
     p->free_managed(ptr);
     return;
@@ -400,18 +434,23 @@ static int pool_init(BlockPool* p, PyObject* args, PyObject* kw) {
   if (!PyArg_ParseTuple(args, "OO!O!O!Li", &fns, &PyDict_Type, &blocks, &PyDict_Type, &lazy,
                         &PyDict_Type, &lbs, &limit, &maxp))
     return -1;
-  if (!PyTuple_Check(fns) || PyTuple_GET_SIZE(fns) != 6) {
-    PyErr_SetString(PyExc_TypeError, "fns: 6 function addresses");
+  const Py_ssize_t nf = PyTuple_Check(fns) ? PyTuple_GET_SIZE(fns) : 0;
+  if (nf != 6 && nf != 8) {
+    PyErr_SetString(PyExc_TypeError, "fns: 6 (or 8, with the completion-word pair) addresses");
     return -1;
   }
-  void* f[6];
-  for (int i = 0; i < 6; ++i) {
-    f[i] = PyLong_AsVoidPtr(PyTuple_GET_ITEM(fns, i));
-    if (!f[i]) {
+  void* f[8] = {0};
+  for (int i = 0; i < nf; ++i) {
+    PyObject* a = PyTuple_GET_ITEM(fns, i);
+    f[i] = a == Py_None ? NULL : PyLong_AsVoidPtr(a);
+    if (!f[i] && (i < 6 || PyErr_Occurred())) {
       if (!PyErr_Occurred()) PyErr_SetString(PyExc_ValueError, "null function address");
       return -1;
     }
   }
+  p->mark_create = (f_mark_create)f[6];
+  p->mark = (f_mark)f[7];
+  if (!p->mark) p->mark_create = NULL;
   p->malloc_managed = (f_malloc_managed)f[0];
   p->free_managed = (f_free_managed)f[1];
   p->ev_create = (f_ev_create)f[2];
@@ -598,6 +637,16 @@ static PyObject* pool_add_stream(BlockPool* p, PyObject* args) {
   ns[p->nstreams[dev]].marker = NULL;
   ns[p->nstreams[dev]].marker_seq = (uint64_t)-1;
   ns[p->nstreams[dev]].done_seq = (uint64_t)-1; /* nothing known yet */
+  ns[p->nstreams[dev]].word = NULL;
+  ns[p->nstreams[dev]].wnext = 0;
+  ns[p->nstreams[dev]].wdisabled = 0;
+  if (p->mark_create) {
+    uint64_t* w = NULL;
+    if (p->mark_create(&w) == 0 && w) {
+      *w = 0;
+      ns[p->nstreams[dev]].word = w;
+    }
+  }
   p->nstreams[dev]++;
   Py_RETURN_NONE;
 }

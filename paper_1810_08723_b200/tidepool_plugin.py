@@ -263,7 +263,8 @@ def _pool_functions(L):
     double (tests/fake_native.py) they are ctypes callbacks into it."""
     if isinstance(L, C.CDLL):
         names = ("tpg_malloc_managed", "tpg_free_managed", "tpg_event_create_untimed",
-                 "tpg_event_record", "tpg_event_query", "tpg_event_sync")
+                 "tpg_event_record", "tpg_event_query", "tpg_event_sync",
+                 "tpg_mark_word_create", "tpg_stream_mark")
         return tuple(C.cast(getattr(L, n), C.c_void_p).value for n in names), ()
     I, P, PP = C.c_int, C.c_void_p, C.POINTER(C.c_void_p)
 
@@ -278,13 +279,27 @@ def _pool_functions(L):
         rc = L.tpg_event_create_untimed(C.byref(v))
         out[0] = v.value
         return rc
+    words = []  # the test double's "device" is synchronous: a mark is set at once
+
+    def mark_create(out):
+        w = C.c_uint64(0)
+        words.append(w)
+        out[0] = C.addressof(w)
+        return 0
+
+    def mark(st, word, value):
+        C.c_uint64.from_address(word).value = value
+        return 0
     cbs = (C.CFUNCTYPE(I, I, C.c_size_t, PP)(malloc_managed),
            C.CFUNCTYPE(I, P)(lambda p: L.tpg_free_managed(p)),
            C.CFUNCTYPE(I, PP)(ev_create),
            C.CFUNCTYPE(I, P, P)(lambda e, st: L.tpg_event_record(e, st)),
            C.CFUNCTYPE(I, P)(lambda e: L.tpg_event_query(e)),
-           C.CFUNCTYPE(I, P)(lambda e: L.tpg_event_sync(e)))
-    return tuple(C.cast(f, C.c_void_p).value for f in cbs), cbs
+           C.CFUNCTYPE(I, P)(lambda e: L.tpg_event_sync(e)),
+           C.CFUNCTYPE(I, PP)(mark_create),
+           C.CFUNCTYPE(I, P, P, C.c_uint64)(mark),
+           words)
+    return tuple(C.cast(f, C.c_void_p).value for f in cbs[:8]), cbs
 
 
 class _Runtime:

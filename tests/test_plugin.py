@@ -409,3 +409,32 @@ def test_threads_share_the_drop_in(env):
     for t in ts:
         t.join()
     assert not errors, errors[:3]
+
+
+@pytest.mark.gpu
+def test_recycled_blocks_wait_for_their_last_gpu_use():
+    """The block pool hands a freed block out again only after the GPU work
+    that last used it completed (completion words / events): fresh storages
+    written by the host right after dropping results of in-flight 64 MiB
+    kernels keep exactly the host's bytes."""
+    import numpy as np
+    tp, gpu, fake, rt = _gpu_env()
+    n = 4096
+    X = tp.tensor_create((n, n), tp.int16, gpu)
+    R = tp.tensor_create((1, n), tp.float, gpu)
+    gpu.default_stream().sync()
+    X.storage.view()[:] = np.arange(n * n, dtype=np.int16).tobytes()
+    R.storage.view()[:] = np.ones(n, dtype=np.float32).tobytes()
+    V = tp.apply_index(tp.transpose(X), (slice(None, None, -1), slice(None)))
+    stats0 = rt.pool.stats()
+    for i in range(24):
+        out = tp.add(V, R)          # 64 MiB result written by an in-flight kernel
+        del out                     # block back to the pool while the kernel may still run
+        fresh = tp.tensor_create((n, n), tp.float, gpu)
+        pattern = np.full(n * n, float(i) + 0.5, dtype=np.float32)
+        fresh.storage.view()[:] = pattern.tobytes()   # host write, no sync
+        gpu.default_stream().sync()
+        got = np.frombuffer(fresh.storage.snapshot(), dtype=np.float32)
+        assert np.array_equal(got, pattern), i
+        del fresh
+    assert rt.pool.stats()["reused"] > stats0["reused"]

@@ -82,7 +82,9 @@ Stream* resolve_stream(tpg_stream s) {
     if (d < 0 || d >= (int)g_default.size()) return nullptr;
     st = g_default[d];
   }
-  cudaSetDevice(st->device);
+  // cudaSetDevice only on a change (a host-side per-launch cost otherwise)
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != st->device) cudaSetDevice(st->device);
   return st;
 }
 

@@ -518,9 +518,11 @@ def register(tidepool_module, count: int | None = None, lib=None):
             rt.streams.setdefault(device.index, []).append(self)
             rt.pool.add_stream(device.index, handle)
 
+        is_default = False  # set on the device's default stream
+
         def submit(self, task) -> None:
             prev = getattr(rt.tls, "stream", None)
-            if prev is None and rt.defaults.get(self.device.index) is self:
+            if prev is None and self.is_default:
                 task()  # rt.current() resolves to this stream anyway
                 return
             rt.tls.stream = self
@@ -542,6 +544,9 @@ def register(tidepool_module, count: int | None = None, lib=None):
             self.allocate = rt.pool.allocator(index, self)
 
         def default_stream(self):
+            st = self._default_stream  # set once; read without the lock afterwards
+            if st is not None:
+                return st
             with self._lock:
                 if self._default_stream is None:
                     h = C.c_void_p()
@@ -549,6 +554,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
                     self._default_stream = GpuStream(self, h.value)
                     rt.entries.set_default_stream(self.index, h.value, self._default_stream)
                     rt.defaults[self.index] = self._default_stream
+                    self._default_stream.is_default = True
                 return self._default_stream
 
         def allocate(self, nbytes):

@@ -738,6 +738,7 @@ static const char* const L_str[19] = {"device", "plan", "stream", "dst_ptr", "sr
                                       "cext", "cdst", "csrc", "sbase", "soff", "sdt", "sbig",
                                       "lazy"};
 static PyObject* L_names[19];
+static PyObject* S_cpack;
 static PyObject *S_standard, *S_stream, *S_device, *S_index, *S_handle, *S_status_sink, *S_extents,
     *S_strides, *S_fused, *S_src_ptr, *S_cext, *S_cdst, *S_csrc, *S_sbase, *S_soff, *S_sdt,
     *S_sbig, *S_pack, *S_mode, *S_ctx, *S_status, *S_store_tag, *S_status_tag;
@@ -943,22 +944,41 @@ static int64_t attr_i64(PyObject* o, PyObject* name, int* bad) {
 
 /* _fuse_strides (tidepool_plugin.py): re-express a binary operand reading a
  * recorded copy's dense destination as a view of the copy's source. */
+/* a copy record's plan and source operand, packed by entries_copy (the
+ * record's `cpack` bytes) so the binary entry reads them with one lookup */
+typedef struct {
+  int64_t ne, sbase, soff, sdt, sbig;
+  int64_t E[TPG_MAX_DIMS], T[TPG_MAX_DIMS], S[TPG_MAX_DIMS];
+} CopyPack;
+
 static int fuse(PyObject* lz, int nd, const int64_t* bext, const int64_t* bstr, int64_t base,
                 int size, int64_t* out_str, int64_t* out_off, int64_t* sbase_out, int* sdt_out,
                 int* sbig_out) {
   int64_t E[TPG_MAX_DIMS], T[TPG_MAX_DIMS], S[TPG_MAX_DIMS], dg[TPG_MAX_DIMS];
-  PyObject *ce = PyObject_GetAttr(lz, S_cext), *cd = PyObject_GetAttr(lz, S_cdst),
-           *cs = PyObject_GetAttr(lz, S_csrc);
   int ne = -1, nt = -1, ns = -1;
-  if (ce && cd && cs) {
-    ne = i64_seq(ce, E, TPG_MAX_DIMS);
-    nt = i64_seq(cd, T, TPG_MAX_DIMS);
-    ns = i64_seq(cs, S, TPG_MAX_DIMS);
+  const CopyPack* cp = NULL;
+  PyObject* pk = PyObject_GetAttr(lz, S_cpack);
+  if (pk && PyBytes_Check(pk) && PyBytes_GET_SIZE(pk) == (Py_ssize_t)sizeof(CopyPack)) {
+    cp = (const CopyPack*)PyBytes_AS_STRING(pk);
+    ne = nt = ns = (int)cp->ne;
+    memcpy(E, cp->E, sizeof E);
+    memcpy(T, cp->T, sizeof T);
+    memcpy(S, cp->S, sizeof S);
+  } else {
+    PyErr_Clear();
+    PyObject *ce = PyObject_GetAttr(lz, S_cext), *cd = PyObject_GetAttr(lz, S_cdst),
+             *cs = PyObject_GetAttr(lz, S_csrc);
+    if (ce && cd && cs) {
+      ne = i64_seq(ce, E, TPG_MAX_DIMS);
+      nt = i64_seq(cd, T, TPG_MAX_DIMS);
+      ns = i64_seq(cs, S, TPG_MAX_DIMS);
+    }
+    Py_XDECREF(ce);
+    Py_XDECREF(cd);
+    Py_XDECREF(cs);
   }
-  Py_XDECREF(ce);
-  Py_XDECREF(cd);
-  Py_XDECREF(cs);
   if (ne < 0 || nt != ne || ns != ne || size <= 0 || base % size) {
+    Py_XDECREF(pk);
     PyErr_Clear();
     return -1;
   }
@@ -971,7 +991,10 @@ static int fuse(PyObject* lz, int nd, const int64_t* bext, const int64_t* bstr, 
       dg[j] = 0;
     }
   }
-  if (lin) return -1;
+  if (lin) {
+    Py_XDECREF(pk);
+    return -1;
+  }
   unsigned used = 0;
   for (int i = 0; i < nd; ++i) {
     if (bext[i] == 1 || bstr[i] == 0) {
@@ -984,17 +1007,28 @@ static int fuse(PyObject* lz, int nd, const int64_t* bext, const int64_t* bstr, 
         found = j;
         break;
       }
-    if (found < 0) return -1;
+    if (found < 0) {
+      Py_XDECREF(pk);
+      return -1;
+    }
     used |= 1u << found;
     out_str[i] = S[found];
   }
   int64_t off = 0;
   for (int j = 0; j < ne; ++j) off += dg[j] * S[j];
   int bad = 0;
-  *out_off = attr_i64(lz, S_soff, &bad) + off;
-  *sbase_out = attr_i64(lz, S_sbase, &bad);
-  *sdt_out = (int)attr_i64(lz, S_sdt, &bad);
-  *sbig_out = (int)attr_i64(lz, S_sbig, &bad);
+  if (cp) {
+    *out_off = cp->soff + off;
+    *sbase_out = cp->sbase;
+    *sdt_out = (int)cp->sdt;
+    *sbig_out = (int)cp->sbig;
+  } else {
+    *out_off = attr_i64(lz, S_soff, &bad) + off;
+    *sbase_out = attr_i64(lz, S_sbase, &bad);
+    *sdt_out = (int)attr_i64(lz, S_sdt, &bad);
+    *sbig_out = (int)attr_i64(lz, S_sbig, &bad);
+  }
+  Py_XDECREF(pk);
   if (bad) {
     PyErr_Clear();
     return -1;
@@ -1411,6 +1445,23 @@ static PyObject* entries_copy_(Entries* e, PyObject* const* args, Py_ssize_t nar
       {(Py_INCREF(L_names[16]), L_names[16]), PyLong_FromLong(ca.wire)},
       {(Py_INCREF(L_names[17]), L_names[17]), PyLong_FromLong(ca.big)},
   };
+  if (!err) {
+    CopyPack cpk;
+    memset(&cpk, 0, sizeof cpk);
+    cpk.ne = nd;
+    cpk.sbase = (int64_t)(intptr_t)ba->ptr;
+    cpk.soff = b1;
+    cpk.sdt = ca.wire;
+    cpk.sbig = ca.big;
+    for (int i = 0; i < nd; ++i) {
+      cpk.E[i] = ext[i];
+      cpk.T[i] = s0[i];
+      cpk.S[i] = s1[i];
+    }
+    PyObject* pb = PyBytes_FromStringAndSize((const char*)&cpk, sizeof cpk);
+    if (!pb || PyObject_SetAttr(lz, S_cpack, pb) < 0) err = 1;
+    Py_XDECREF(pb);
+  }
   const int nv = (int)(sizeof vals / sizeof vals[0]);
   for (int i = 0; i < nv; ++i) {
     if (!err && (!vals[i][0] || !vals[i][1] || PyObject_SetAttr(lz, vals[i][0], vals[i][1]) < 0))
@@ -1498,6 +1549,7 @@ static int intern_names(void) {
   IN(S_soff, "soff");
   IN(S_sdt, "sdt");
   IN(S_sbig, "sbig");
+  IN(S_cpack, "cpack");
   IN(S_pack, "pack");
   IN(S_mode, "mode");
   IN(S_ctx, "ctx");

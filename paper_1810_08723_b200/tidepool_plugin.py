@@ -449,7 +449,7 @@ class _Lazy:
     __slots__ = ("device", "plan", "dst_ptr", "ddt", "dbig", "src_ptr", "keep", "src_dtype",
                  "dst_dtype", "src_order", "stream",
                  # plain-int copies read by the C binary entry (tpg_pyfast.c)
-                 "cext", "cdst", "csrc", "sbase", "soff", "sdt", "sbig")
+                 "cext", "cdst", "csrc", "sbase", "soff", "sdt", "sbig", "cpack")
 
     def launch(self, rt):
         """Launch on the stream the copy entry ran on (the destination
@@ -796,6 +796,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
         lz.src_dtype, lz.dst_dtype, lz.src_order = da, dd, aord
         lz.cext, lz.cdst, lz.csrc = tuple(plan.extents), tuple(plan.strides[0]), tuple(plan.strides[1])
         lz.sbase, lz.soff, lz.sdt, lz.sbig = aptr, bases[1], da.wire_code, int(aord == "big")
+        lz.cpack = None  # (the C copy entry packs these fields; see tpg_pyfast.c CopyPack)
         rt.before_write(dptr)
         rt.stats["lazy"] += 1
         with rt.lock:

@@ -59,6 +59,7 @@ static inline long long now_ns(void) {
 }
 
 typedef struct Marker {
+  int armed;     /* recorded on its stream (a pending marker collects releases first) */
   void* ev;      /* event marker (NULL for a completion-word marker) */
   uint64_t wval; /* completion-word marker: done once the stream's word >= wval */
   long refs;
@@ -74,6 +75,8 @@ typedef struct {
   volatile uint64_t* word; /* completion word (tpg_stream_mark), or NULL: events */
   uint64_t wnext;
   int wdisabled; /* tpg_stream_mark failed once: new markers use events */
+  Marker* pending; /* unrecorded marker the blocks released since the last record share */
+  int npending;
 } StreamRec;
 
 typedef struct {
@@ -157,8 +160,13 @@ static void unref_markers(BlockPool* p, Entry* e) {
     if (--m->refs > 0) continue;
     /* last user: detach from its stream and recycle the event */
     for (int d = 0; d < MAX_DEV; ++d)
-      for (int s = 0; s < p->nstreams[d]; ++s)
+      for (int s = 0; s < p->nstreams[d]; ++s) {
         if (p->streams[d][s].marker == m) p->streams[d][s].marker = NULL;
+        if (p->streams[d][s].pending == m) {
+          p->streams[d][s].pending = NULL;
+          p->streams[d][s].npending = 0;
+        }
+      }
     if (m->ev) {
       if (p->nevpool == p->aevpool) {
         size_t na = p->aevpool ? 2 * p->aevpool : 64;
@@ -182,10 +190,14 @@ static void unref_markers(BlockPool* p, Entry* e) {
  * complete: the stream's NEWEST marker is queried first (one query then
  * usually clears every pending block of the device -- the host runs behind
  * the GPU in steady state), and a watermark makes repeat checks free. */
+static int arm_pending(BlockPool* p, int dev, int sidx);
+static void arm_device(BlockPool* p, int dev);
+
 static int entry_done(BlockPool* p, Entry* e) {
   for (int i = 0; i < e->nev; ++i) {
     Marker* m = e->evs[i];
     StreamRec* st = &p->streams[m->dev][m->sidx];
+    if (!m->armed) return 0; /* not recorded yet */
     if (m->wval) { /* completion word: a host memory read, no CUDA call */
       if (*st->word >= m->wval) continue;
       return 0;
@@ -203,9 +215,12 @@ static int entry_done(BlockPool* p, Entry* e) {
 }
 
 static void entry_wait(BlockPool* p, Entry* e) {
+  for (int i = 0; i < e->nev; ++i)
+    if (!e->evs[i]->armed) arm_pending(p, e->evs[i]->dev, e->evs[i]->sidx);
   Py_BEGIN_ALLOW_THREADS
   for (int i = 0; i < e->nev; ++i) {
     Marker* m = e->evs[i];
+    if (!m->armed) continue; /* recording failed (no event could be created) */
     if (m->wval) {
       volatile uint64_t* w = p->streams[m->dev][m->sidx].word;
       while (*w < m->wval) {
@@ -288,6 +303,9 @@ static void* take(BlockPool* p, int dev, size_t cap) {
         return e.ptr;
       }
     }
+    /* nothing reusable: record the device's pending markers so the blocks
+     * waiting on them become reusable for the next allocations */
+    arm_device(p, dev);
     if ((int)live >= p->max_pending) {
       Entry e = c->v[c->head++];
       if (c->head == c->n) c->head = c->n = 0;
@@ -309,6 +327,49 @@ static void release_block(BlockPool* p, void* ptr, size_t cap, int dev) {
   release_block_(p, ptr, cap, dev);
   T_release += now_ns() - t0;
 }
+/* Record a stream's pending marker (completion word, else event): every
+ * block attached to it was released before this point in stream order, so
+ * it completes only after their last GPU use. */
+static int arm_pending(BlockPool* p, int dev, int sidx) {
+  StreamRec* st = &p->streams[dev][sidx];
+  Marker* m = st->pending;
+  if (!m) return 0;
+  m->seq = p->seq;
+  if (st->word && !st->wdisabled) {
+    m->wval = st->wnext + 1;
+    if (p->mark(st->handle, (uint64_t*)st->word, m->wval) == 0) {
+      st->wnext = m->wval;
+    } else {
+      m->wval = 0; /* no stream memory ops: events from now on */
+      st->wdisabled = 1;
+    }
+  }
+  if (!m->wval) {
+    if (p->nevpool) {
+      m->ev = p->evpool[--p->nevpool];
+    } else if (p->ev_create(&m->ev) != 0) {
+      return -1; /* stays pending: its blocks are not reusable yet */
+    }
+    p->ev_record(m->ev, st->handle);
+  }
+  m->armed = 1;
+  st->marker = m;
+  st->marker_seq = p->seq;
+  st->pending = NULL;
+  st->npending = 0;
+  return 0;
+}
+
+static void arm_device(BlockPool* p, int dev) {
+  for (int s = 0; s < p->nstreams[dev]; ++s) arm_pending(p, dev, s);
+}
+
+/* releases share a stream's pending marker; it is recorded once ARM_AT
+ * blocks wait on it, or when an allocation / wait needs it (one stream
+ * memory op per ARM_AT releases instead of one per launch epoch; the pool
+ * keeps the few extra blocks in flight this needs) */
+#define ARM_AT 4
+
 static void release_block_(BlockPool* p, void* ptr, size_t cap, int dev) {
   p->n_release++;
   blocks_del(p, ptr);
@@ -319,35 +380,16 @@ static void release_block_(BlockPool* p, void* ptr, size_t cap, int dev) {
     e.evs = (Marker**)malloc(sizeof(Marker*) * ns);
     for (int s = 0; e.evs && s < ns; ++s) {
       StreamRec* st = &p->streams[dev][s];
-      if (!st->marker || st->marker_seq != p->seq) {
+      if (!st->pending) {
         Marker* m = (Marker*)calloc(1, sizeof(Marker));
         if (!m) break;
-        m->seq = p->seq;
         m->dev = dev;
         m->sidx = s;
-        if (st->word && !st->wdisabled) {
-          m->wval = st->wnext + 1;
-          if (p->mark(st->handle, (uint64_t*)st->word, m->wval) == 0) {
-            st->wnext = m->wval;
-          } else {
-            m->wval = 0; /* no stream memory ops: events from now on */
-            st->wdisabled = 1;
-          }
-        }
-        if (!m->wval) {
-          if (p->nevpool) {
-            m->ev = p->evpool[--p->nevpool];
-          } else if (p->ev_create(&m->ev) != 0) {
-            free(m);
-            break;
-          }
-          p->ev_record(m->ev, st->handle);
-        }
-        st->marker = m;
-        st->marker_seq = p->seq;
+        st->pending = m;
       }
-      st->marker->refs++;
-      e.evs[e.nev++] = st->marker;
+      st->pending->refs++;
+      e.evs[e.nev++] = st->pending;
+      if (++st->npending >= ARM_AT) arm_pending(p, dev, s);
     }
   }
   if (!c) { /* out of host memory: drop the block */
@@ -640,6 +682,8 @@ static PyObject* pool_add_stream(BlockPool* p, PyObject* args) {
   ns[p->nstreams[dev]].word = NULL;
   ns[p->nstreams[dev]].wnext = 0;
   ns[p->nstreams[dev]].wdisabled = 0;
+  ns[p->nstreams[dev]].pending = NULL;
+  ns[p->nstreams[dev]].npending = 0;
   if (p->mark_create) {
     uint64_t* w = NULL;
     if (p->mark_create(&w) == 0 && w) {
@@ -1437,9 +1481,10 @@ static PyObject* entries_copy_(Entries* e, PyObject* const* args, Py_ssize_t nar
       {(Py_INCREF(L_names[9]), L_names[9]), (Py_INCREF(dd), dd)},
       {(Py_INCREF(L_names[10]), L_names[10]),
        (Py_INCREF(PyTuple_GET_ITEM(aobj, 1)), PyTuple_GET_ITEM(aobj, 1))},
-      {(Py_INCREF(L_names[11]), L_names[11]), PySequence_Tuple(pe)},
-      {(Py_INCREF(L_names[12]), L_names[12]), PySequence_Tuple(v0)},
-      {(Py_INCREF(L_names[13]), L_names[13]), PySequence_Tuple(v1)},
+      /* cext / cdst / csrc: only read for records without `cpack` */
+      {(Py_INCREF(L_names[11]), L_names[11]), (Py_INCREF(Py_None), Py_None)},
+      {(Py_INCREF(L_names[12]), L_names[12]), (Py_INCREF(Py_None), Py_None)},
+      {(Py_INCREF(L_names[13]), L_names[13]), (Py_INCREF(Py_None), Py_None)},
       {(Py_INCREF(L_names[14]), L_names[14]), (Py_INCREF(ka), ka)},
       {(Py_INCREF(L_names[15]), L_names[15]), PyLong_FromLongLong(b1)},
       {(Py_INCREF(L_names[16]), L_names[16]), PyLong_FromLong(ca.wire)},

@@ -772,7 +772,7 @@ typedef struct {
   PyObject* lossless;   /* bytes[32 * 32]: lossless_castable(src wire, dst wire) */
   PyObject* default_st[MAX_DEV]; /* default GpuStream objects */
   void* defaults[MAX_DEV];
-  long long n_fast, n_fallback;
+  long long n_fast, n_fallback, n_fused, n_lazy;
 } Entries;
 
 static PyTypeObject EntriesType;
@@ -995,15 +995,71 @@ typedef struct {
   int64_t E[TPG_MAX_DIMS], T[TPG_MAX_DIMS], S[TPG_MAX_DIMS];
 } CopyPack;
 
+/* A recorded lossless copy (tidepool_plugin._Lazy derives from this):
+ * C fields, visible to Python as attributes, filled by the C copy entry
+ * without attribute calls and read by the C binary entry directly. */
+#include <structmember.h>
+typedef struct {
+  PyObject_HEAD
+  PyObject *plan, *stream, *keep, *src_dtype, *dst_dtype, *src_order, *dst_ptr, *src_ptr;
+  PyObject *cext, *cdst, *csrc;
+  long long device, ddt, dbig, sbase, soff, sdt, sbig;
+  int has_pack;
+  CopyPack pack;
+} LazyRecord;
+
+static PyTypeObject LazyRecordType;
+
+static int lazyrec_traverse(LazyRecord* r, visitproc visit, void* arg) {
+  Py_VISIT(r->plan);
+  Py_VISIT(r->stream);
+  Py_VISIT(r->keep);
+  Py_VISIT(r->src_dtype);
+  Py_VISIT(r->dst_dtype);
+  Py_VISIT(r->src_order);
+  Py_VISIT(r->dst_ptr);
+  Py_VISIT(r->src_ptr);
+  Py_VISIT(r->cext);
+  Py_VISIT(r->cdst);
+  Py_VISIT(r->csrc);
+  return 0;
+}
+static int lazyrec_clear(LazyRecord* r) {
+  Py_CLEAR(r->plan);
+  Py_CLEAR(r->stream);
+  Py_CLEAR(r->keep);
+  Py_CLEAR(r->src_dtype);
+  Py_CLEAR(r->dst_dtype);
+  Py_CLEAR(r->src_order);
+  Py_CLEAR(r->dst_ptr);
+  Py_CLEAR(r->src_ptr);
+  Py_CLEAR(r->cext);
+  Py_CLEAR(r->cdst);
+  Py_CLEAR(r->csrc);
+  return 0;
+}
+static void lazyrec_dealloc(LazyRecord* r) {
+  PyObject_GC_UnTrack(r);
+  lazyrec_clear(r);
+  Py_TYPE(r)->tp_free((PyObject*)r);
+}
+#define LR_OBJ(name) {#name, T_OBJECT, offsetof(LazyRecord, name), 0, NULL}
+#define LR_LL(name) {#name, T_LONGLONG, offsetof(LazyRecord, name), 0, NULL}
+static PyMemberDef lazyrec_members[] = {
+    LR_OBJ(plan), LR_OBJ(stream), LR_OBJ(keep), LR_OBJ(src_dtype), LR_OBJ(dst_dtype),
+    LR_OBJ(src_order), LR_OBJ(dst_ptr), LR_OBJ(src_ptr), LR_OBJ(cext), LR_OBJ(cdst),
+    LR_OBJ(csrc), LR_LL(device), LR_LL(ddt), LR_LL(dbig), LR_LL(sbase), LR_LL(soff),
+    LR_LL(sdt), LR_LL(sbig), {NULL}};
+
 static int fuse(PyObject* lz, int nd, const int64_t* bext, const int64_t* bstr, int64_t base,
                 int size, int64_t* out_str, int64_t* out_off, int64_t* sbase_out, int* sdt_out,
                 int* sbig_out) {
   int64_t E[TPG_MAX_DIMS], T[TPG_MAX_DIMS], S[TPG_MAX_DIMS], dg[TPG_MAX_DIMS];
   int ne = -1, nt = -1, ns = -1;
   const CopyPack* cp = NULL;
-  PyObject* pk = PyObject_GetAttr(lz, S_cpack);
-  if (pk && PyBytes_Check(pk) && PyBytes_GET_SIZE(pk) == (Py_ssize_t)sizeof(CopyPack)) {
-    cp = (const CopyPack*)PyBytes_AS_STRING(pk);
+  PyObject* pk = NULL;
+  if (PyObject_TypeCheck(lz, &LazyRecordType) && ((LazyRecord*)lz)->has_pack) {
+    cp = &((LazyRecord*)lz)->pack;
     ne = nt = ns = (int)cp->ne;
     memcpy(E, cp->E, sizeof E);
     memcpy(T, cp->T, sizeof T);
@@ -1229,16 +1285,7 @@ static PyObject* entries_binary_(Entries* e, PyObject* const* args, Py_ssize_t n
   int rc = e->binary(handle, op, &p, &od, &oa, &ob, ca.compute, 0);
   T_launch += now_ns() - tl;
   e->n_fast++;
-  if (nfused) {
-    PyObject* c = PyObject_GetItem(e->stats, S_fused);
-    long long n = c ? PyLong_AsLongLong(c) : 0;
-    Py_XDECREF(c);
-    PyErr_Clear();
-    PyObject* nv = PyLong_FromLongLong(n + nfused);
-    if (nv) PyObject_SetItem(e->stats, S_fused, nv);
-    Py_XDECREF(nv);
-    PyErr_Clear();
-  }
+  e->n_fused += nfused;
   return PyLong_FromLong(rc);
 #undef FALLBACK
 }
@@ -1467,52 +1514,43 @@ static PyObject* entries_copy_(Entries* e, PyObject* const* args, Py_ssize_t nar
   }
   e->pool->seq++; /* rt.current() */
   PyObject* lz = PyObject_CallNoArgs(e->lazy_cls);
-  int err = !lz;
-  PyObject* vals[][2] = {
-      {(Py_INCREF(L_names[0]), L_names[0]), PyLong_FromLong(dev)},
-      {(Py_INCREF(L_names[1]), L_names[1]), (Py_INCREF(plan), plan)},
-      {(Py_INCREF(L_names[2]), L_names[2]), (Py_INCREF(st), st)},
-      {(Py_INCREF(L_names[3]), L_names[3]), (Py_INCREF(kd), kd)},
-      {(Py_INCREF(L_names[4]), L_names[4]), (Py_INCREF(ka), ka)},
-      {(Py_INCREF(L_names[5]), L_names[5]), PyLong_FromLong(cd.wire)},
-      {(Py_INCREF(L_names[6]), L_names[6]), PyLong_FromLong(cd.big)},
-      {(Py_INCREF(L_names[7]), L_names[7]), (Py_INCREF(args[3]), args[3])},
-      {(Py_INCREF(L_names[8]), L_names[8]), (Py_INCREF(da), da)},
-      {(Py_INCREF(L_names[9]), L_names[9]), (Py_INCREF(dd), dd)},
-      {(Py_INCREF(L_names[10]), L_names[10]),
-       (Py_INCREF(PyTuple_GET_ITEM(aobj, 1)), PyTuple_GET_ITEM(aobj, 1))},
-      /* cext / cdst / csrc: only read for records without `cpack` */
-      {(Py_INCREF(L_names[11]), L_names[11]), (Py_INCREF(Py_None), Py_None)},
-      {(Py_INCREF(L_names[12]), L_names[12]), (Py_INCREF(Py_None), Py_None)},
-      {(Py_INCREF(L_names[13]), L_names[13]), (Py_INCREF(Py_None), Py_None)},
-      {(Py_INCREF(L_names[14]), L_names[14]), (Py_INCREF(ka), ka)},
-      {(Py_INCREF(L_names[15]), L_names[15]), PyLong_FromLongLong(b1)},
-      {(Py_INCREF(L_names[16]), L_names[16]), PyLong_FromLong(ca.wire)},
-      {(Py_INCREF(L_names[17]), L_names[17]), PyLong_FromLong(ca.big)},
-  };
+  int err = !lz || !PyObject_TypeCheck(lz, &LazyRecordType);
   if (!err) {
-    CopyPack cpk;
-    memset(&cpk, 0, sizeof cpk);
-    cpk.ne = nd;
-    cpk.sbase = (int64_t)(intptr_t)ba->ptr;
-    cpk.soff = b1;
-    cpk.sdt = ca.wire;
-    cpk.sbig = ca.big;
+    LazyRecord* r = (LazyRecord*)lz;
+#define LR_SET(field, val) \
+  do {                     \
+    PyObject* v_ = (val);  \
+    Py_XINCREF(v_);        \
+    Py_XSETREF(r->field, v_); \
+  } while (0)
+    LR_SET(plan, plan);
+    LR_SET(stream, st);
+    LR_SET(dst_ptr, kd);
+    LR_SET(src_ptr, ka);
+    LR_SET(keep, args[3]);
+    LR_SET(src_dtype, da);
+    LR_SET(dst_dtype, dd);
+    LR_SET(src_order, PyTuple_GET_ITEM(aobj, 1));
+#undef LR_SET
+    r->device = dev;
+    r->ddt = cd.wire;
+    r->dbig = cd.big;
+    r->sbase = (long long)(intptr_t)ba->ptr;
+    r->soff = b1;
+    r->sdt = ca.wire;
+    r->sbig = ca.big;
+    memset(&r->pack, 0, sizeof r->pack);
+    r->pack.ne = nd;
+    r->pack.sbase = r->sbase;
+    r->pack.soff = b1;
+    r->pack.sdt = ca.wire;
+    r->pack.sbig = ca.big;
     for (int i = 0; i < nd; ++i) {
-      cpk.E[i] = ext[i];
-      cpk.T[i] = s0[i];
-      cpk.S[i] = s1[i];
+      r->pack.E[i] = ext[i];
+      r->pack.T[i] = s0[i];
+      r->pack.S[i] = s1[i];
     }
-    PyObject* pb = PyBytes_FromStringAndSize((const char*)&cpk, sizeof cpk);
-    if (!pb || PyObject_SetAttr(lz, S_cpack, pb) < 0) err = 1;
-    Py_XDECREF(pb);
-  }
-  const int nv = (int)(sizeof vals / sizeof vals[0]);
-  for (int i = 0; i < nv; ++i) {
-    if (!err && (!vals[i][0] || !vals[i][1] || PyObject_SetAttr(lz, vals[i][0], vals[i][1]) < 0))
-      err = 1;
-    Py_XDECREF(vals[i][0]);
-    Py_XDECREF(vals[i][1]);
+    r->has_pack = 1;
   }
   PyObject* set = NULL;
   if (!err) err = PyDict_SetItem(e->lazy, kd, lz) < 0;
@@ -1528,18 +1566,7 @@ static PyObject* entries_copy_(Entries* e, PyObject* const* args, Py_ssize_t nar
       err = 1;
     }
   }
-  if (!err) {
-    PyObject* key = (Py_INCREF(L_names[18]), L_names[18]);
-    PyObject* c = key ? PyObject_GetItem(e->stats, key) : NULL;
-    long long n = c ? PyLong_AsLongLong(c) : 0;
-    Py_XDECREF(c);
-    PyErr_Clear();
-    PyObject* nvv = PyLong_FromLongLong(n + 1);
-    if (key && nvv) PyObject_SetItem(e->stats, key, nvv);
-    Py_XDECREF(nvv);
-    Py_XDECREF(key);
-    PyErr_Clear();
-  }
+  if (!err) e->n_lazy++;
   Py_XDECREF(lz);
   Py_DECREF(kd);
   Py_DECREF(ka);
@@ -1555,9 +1582,10 @@ static PyObject* entries_copy_(Entries* e, PyObject* const* args, Py_ssize_t nar
 }
 
 static PyObject* entries_counts(Entries* e, PyObject* unused) {
-  return Py_BuildValue("{s:L,s:L,s:L,s:L,s:L,s:L,s:L}", "fast", e->n_fast, "fallback",
-                       e->n_fallback, "ns_allocate", T_alloc, "ns_release", T_release,
-                       "ns_binary", T_binary, "ns_copy", T_copy, "ns_launch", T_launch);
+  return Py_BuildValue("{s:L,s:L,s:L,s:L,s:L,s:L,s:L,s:L,s:L}", "fast", e->n_fast, "fallback",
+                       e->n_fallback, "fused", e->n_fused, "lazy", e->n_lazy, "ns_allocate",
+                       T_alloc, "ns_release", T_release, "ns_binary", T_binary, "ns_copy", T_copy,
+                       "ns_launch", T_launch);
 }
 
 static PyMethodDef entries_methods[] = {
@@ -1651,6 +1679,16 @@ PyMODINIT_FUNC PyInit__tpg_pyfast(void) {
   if (PyType_Ready(&BlockPoolType) < 0) return NULL;
 
   if (intern_names() < 0) return NULL;
+  LazyRecordType.tp_name = "_tpg_pyfast.LazyRecord";
+  LazyRecordType.tp_basicsize = sizeof(LazyRecord);
+  LazyRecordType.tp_flags = Py_TPFLAGS_DEFAULT | Py_TPFLAGS_BASETYPE | Py_TPFLAGS_HAVE_GC;
+  LazyRecordType.tp_doc = "a recorded lossless gpu->gpu copy (base of tidepool_plugin._Lazy)";
+  LazyRecordType.tp_new = PyType_GenericNew;
+  LazyRecordType.tp_dealloc = (destructor)lazyrec_dealloc;
+  LazyRecordType.tp_traverse = (traverseproc)lazyrec_traverse;
+  LazyRecordType.tp_clear = (inquiry)lazyrec_clear;
+  LazyRecordType.tp_members = lazyrec_members;
+  if (PyType_Ready(&LazyRecordType) < 0) return NULL;
   if (!(S_alloc_count = PyUnicode_InternFromString("alloc_count"))) return NULL;
   if (!(ONE = PyLong_FromLong(1))) return NULL;
   AllocatorType.tp_name = "_tpg_pyfast.Allocator";
@@ -1694,5 +1732,7 @@ PyMODINIT_FUNC PyInit__tpg_pyfast(void) {
   PyModule_AddObject(m, "BlockPool", (PyObject*)&BlockPoolType);
   Py_INCREF(&EntriesType);
   PyModule_AddObject(m, "Entries", (PyObject*)&EntriesType);
+  Py_INCREF(&LazyRecordType);
+  PyModule_AddObject(m, "LazyRecord", (PyObject*)&LazyRecordType);
   return m;
 }

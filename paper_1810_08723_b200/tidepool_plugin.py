@@ -55,6 +55,7 @@ captured reference table calls into golden vectors.
 from __future__ import annotations
 
 import collections
+import collections.abc
 import ctypes as C
 import threading
 
@@ -302,6 +303,34 @@ def _pool_functions(L):
     return tuple(C.cast(f, C.c_void_p).value for f in cbs[:8]), cbs
 
 
+class _Stats(collections.abc.Mapping):
+    """Path counters (lazy / fused / materialized / staged / ...): the Python
+    entries bump them here, the C entries count in C (Entries.counts());
+    reads add both."""
+
+    def __init__(self):
+        self.py = collections.Counter()
+        self.entries = None
+
+    def bump(self, key, n=1):
+        self.py[key] += n
+
+    def _c(self):
+        if self.entries is None:
+            return {}
+        c = self.entries.counts()
+        return {"lazy": c["lazy"], "fused": c["fused"]}
+
+    def __getitem__(self, key):
+        return self.py[key] + self._c().get(key, 0)
+
+    def __iter__(self):
+        return iter(set(self.py) | set(self._c()))
+
+    def __len__(self):
+        return len(set(self.py) | set(self._c()))
+
+
 class _Runtime:
     """Per-registration state: devices, streams, block cache, lazy casts."""
 
@@ -328,7 +357,7 @@ class _Runtime:
         self.defaults: dict = {}     # device -> its default GpuStream (rt.current)
         self.event_pool: list = []   # timing events (profile hook)
         self.plans: dict = {}    # (extents, strides) -> abi.Plan (entries rebuild plans per call)
-        self.stats = collections.Counter()  # lazy / fused / materialised / transfer paths
+        self.stats = _Stats()  # lazy / fused / materialised / transfer paths
         self.profile = None  # [] -> (start, stop) timing events around each standard-mode launch
 
     # -- errors --------------------------------------------------------------
@@ -419,7 +448,7 @@ class _Runtime:
         with self.lock:
             lz = self._drop_lazy_locked(dst_ptr)
         if lz is not None:
-            self.stats["materialized"] += 1
+            self.stats.bump("materialized")
             lz.launch(self)
 
     def before_read(self, ptr):
@@ -444,12 +473,19 @@ class _Runtime:
             self.materialize(p)
 
 
-class _Lazy:
-    """A recorded dtype-converting gpu->gpu copy (ops._dtype_convert)."""
-    __slots__ = ("device", "plan", "dst_ptr", "ddt", "dbig", "src_ptr", "keep", "src_dtype",
-                 "dst_dtype", "src_order", "stream",
-                 # plain-int copies read by the C binary entry (tpg_pyfast.c)
-                 "cext", "cdst", "csrc", "sbase", "soff", "sdt", "sbig", "cpack")
+try:  # the C host fast path (built in-tree; register() requires it)
+    from . import _tpg_pyfast as _fastmod
+except ImportError:
+    _fastmod = None
+
+
+class _Lazy(_fastmod.LazyRecord if _fastmod is not None else object):
+    """A recorded dtype-converting gpu->gpu copy (ops._dtype_convert).  The
+    fields live in the C base (tpg_pyfast.c LazyRecord), which the C copy
+    entry fills and the C binary entry reads directly."""
+    __slots__ = () if _fastmod is not None else (
+        "device", "plan", "dst_ptr", "ddt", "dbig", "src_ptr", "keep", "src_dtype", "dst_dtype",
+        "src_order", "stream", "cext", "cdst", "csrc", "sbase", "soff", "sdt", "sbig")
 
     def launch(self, rt):
         """Launch on the stream the copy entry ran on (the destination
@@ -494,7 +530,8 @@ def register(tidepool_module, count: int | None = None, lib=None):
                        ref_dtypes.widen_for_compute(d).wire_code)
                    for f, (d, order) in codec_of.items()}
     rt.entries = _fast_module().Entries(rt.pool, _binary_function(L, abi), rt, rt.tls, rt.lazy,
-                                        rt.lazy_by_src, fast_codecs, rt.stats)
+                                        rt.lazy_by_src, fast_codecs, rt.stats.py)
+    rt.stats.entries = rt.entries
     lossless_table = bytearray(32 * 32)
     for a_ in ref_dtypes.ALL_DTYPES:
         for b_ in ref_dtypes.ALL_DTYPES:
@@ -590,7 +627,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
             p = C.c_void_p()
             rt.check(L.tpg_malloc_on(self.st.handle, n, C.byref(p)), "staging")
             self.ptrs.append(p.value)
-            rt.stats["staged"] += 1
+            rt.stats.bump("staged")
             # pageable source: returns once the bytes are consumed
             rt.check(L.tpg_memcpy_h2d(p.value, host_ptr + lo, n, self.st.handle), "H2D")
             return p.value - lo
@@ -718,7 +755,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
                     with rt.lock:
                         keep = rt.lazy.get(ptr) is lz
                     if keep:
-                        rt.stats["fused"] += 1
+                        rt.stats.bump("fused")
                         o = abi.make_operand(lz.sbase, lz.soff + off, lz.sdt, lz.sbig)
                         ops.append(o)
                         strides.append(s)
@@ -796,9 +833,8 @@ def register(tidepool_module, count: int | None = None, lib=None):
         lz.src_dtype, lz.dst_dtype, lz.src_order = da, dd, aord
         lz.cext, lz.cdst, lz.csrc = tuple(plan.extents), tuple(plan.strides[0]), tuple(plan.strides[1])
         lz.sbase, lz.soff, lz.sdt, lz.sbig = aptr, bases[1], da.wire_code, int(aord == "big")
-        lz.cpack = None  # (the C copy entry packs these fields; see tpg_pyfast.c CopyPack)
         rt.before_write(dptr)
-        rt.stats["lazy"] += 1
+        rt.stats.bump("lazy")
         with rt.lock:
             rt.lazy[dptr] = lz
             rt.lazy_by_src.setdefault(aptr, set()).add(dptr)
@@ -1082,7 +1118,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
             lo, hi = _span(plan.extents, plan.strides[1], src.offset, size)
             sptr = temps.stage(sptr, lo, hi)
         p = _plan(plan)
-        rt.stats["gather_plan"] += 1
+        rt.stats.bump("gather_plan")
         rt.check(L.tpg_gather_plan(st.handle, C.byref(p), dptr, dst.offset, sptr, soff, size),
                  "gather")
         temps.done()
@@ -1101,7 +1137,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
         rt.check(L.tpg_memcpy_d2h(hptr + lo, tmp.value, hi - lo, st.handle), "D2H")
         L.tpg_free(src.device.index, tmp.value, st.handle)
         rt.check(L.tpg_stream_sync(st.handle), "sync")
-        rt.stats["gather_to_host"] += 1
+        rt.stats.bump("gather_to_host")
 
     raw_gather.reference = orig_raw_gather
     ref_tensors._raw_gather = raw_gather
@@ -1135,7 +1171,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
                 hptr = rt.address(d_buf)
                 rt.check(L.tpg_memcpy_d2h(hptr + lo, tmp.value, hi - lo, st.handle), "D2H")
                 rt.check(L.tpg_stream_sync(st.handle), "sync")
-                rt.stats["cpu_copy_from_gpu"] += 1
+                rt.stats.bump("cpu_copy_from_gpu")
             finally:
                 L.tpg_free(dev, tmp.value, st.handle)
         return h

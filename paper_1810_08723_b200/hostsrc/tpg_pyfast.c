@@ -133,7 +133,28 @@ typedef struct {
 
 static PyTypeObject BlockPoolType;
 static PyTypeObject DevBufType;
+static PyTypeObject LazyRecordType;
 static PyObject* AllocError;  /* set by the plugin: the reference's AllocationError */
+
+/* a copy record's plan and source operand, packed by entries_copy (the
+ * record's `cpack` bytes) so the binary entry reads them with one lookup */
+typedef struct {
+  int64_t ne, sbase, soff, sdt, sbig;
+  int64_t E[TPG_MAX_DIMS], T[TPG_MAX_DIMS], S[TPG_MAX_DIMS];
+} CopyPack;
+
+/* A recorded lossless copy (tidepool_plugin._Lazy derives from this):
+ * C fields, visible to Python as attributes, filled by the C copy entry
+ * without attribute calls and read by the C binary entry directly. */
+#include <structmember.h>
+typedef struct {
+  PyObject_HEAD
+  PyObject *plan, *stream, *keep, *src_dtype, *dst_dtype, *src_order, *dst_ptr, *src_ptr;
+  PyObject *cext, *cdst, *csrc;
+  long long device, ddt, dbig, sbase, soff, sdt, sbig;
+  int has_pack;
+  CopyPack pack;
+} LazyRecord;
 
 static size_t size_class(size_t n) {
   if (n <= ((size_t)1 << 20)) return ((n ? n : 1) + 511) & ~(size_t)511;
@@ -257,7 +278,9 @@ static void blocks_del(BlockPool* p, void* ptr) {
   if (rec) {
     Py_INCREF(rec);
     if (PyDict_DelItem(p->lazy, k) < 0) PyErr_Clear();
-    PyObject* src = PyObject_GetAttrString(rec, "src_ptr");
+    PyObject* src = PyObject_TypeCheck(rec, &LazyRecordType) ? ((LazyRecord*)rec)->src_ptr : NULL;
+    if (src) Py_INCREF(src);
+    else src = PyObject_GetAttrString(rec, "src_ptr");
     PyObject* set = src ? PyDict_GetItemWithError(p->lazy_by_src, src) : NULL;
     if (set && PySet_Check(set)) {
       if (PySet_Discard(set, k) < 0) PyErr_Clear();
@@ -988,27 +1011,8 @@ static int64_t attr_i64(PyObject* o, PyObject* name, int* bad) {
 
 /* _fuse_strides (tidepool_plugin.py): re-express a binary operand reading a
  * recorded copy's dense destination as a view of the copy's source. */
-/* a copy record's plan and source operand, packed by entries_copy (the
- * record's `cpack` bytes) so the binary entry reads them with one lookup */
-typedef struct {
-  int64_t ne, sbase, soff, sdt, sbig;
-  int64_t E[TPG_MAX_DIMS], T[TPG_MAX_DIMS], S[TPG_MAX_DIMS];
-} CopyPack;
 
-/* A recorded lossless copy (tidepool_plugin._Lazy derives from this):
- * C fields, visible to Python as attributes, filled by the C copy entry
- * without attribute calls and read by the C binary entry directly. */
-#include <structmember.h>
-typedef struct {
-  PyObject_HEAD
-  PyObject *plan, *stream, *keep, *src_dtype, *dst_dtype, *src_order, *dst_ptr, *src_ptr;
-  PyObject *cext, *cdst, *csrc;
-  long long device, ddt, dbig, sbase, soff, sdt, sbig;
-  int has_pack;
-  CopyPack pack;
-} LazyRecord;
 
-static PyTypeObject LazyRecordType;
 
 static int lazyrec_traverse(LazyRecord* r, visitproc visit, void* arg) {
   Py_VISIT(r->plan);

@@ -412,7 +412,7 @@ def bench_cfg2(L, steps, warmup, dev=0):
             "launches": steps + launches[0]}
 
 
-def bench_plugin(L, steps=400, warmup=30):
+def bench_plugin(L, steps=2000, warmup=300):
     """cfg2 through the UNMODIFIED reference `tidepool` with the gpu table
     registered (the north_star drop-in): `tidepool.add(V, R)` on gpu0, where
     the reference pipeline converts V int16 -> float (ops._dtype_convert)

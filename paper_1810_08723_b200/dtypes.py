@@ -23,9 +23,10 @@ MODE_CODE = {m: i for i, m in enumerate(MODES)}
 
 
 def check_mode(mode: str) -> str:
-    if mode not in MODES:
-        raise ValueError(f"unknown compute mode {mode!r}; expected one of {MODES}")
-    return mode
+    """`mode` itself when it is one of MODES (the reference's compute modes)."""
+    if mode in MODE_CODE:
+        return mode
+    raise ValueError(f"unknown compute mode {mode!r}; expected one of {MODES}")
 
 
 class DType:
@@ -85,18 +86,19 @@ _CPLX = {HALF: CHALF, FLOAT: CFLOAT, DOUBLE: CDOUBLE}
 _SIG = {HALF: 11, FLOAT: 24, DOUBLE: 53, BFLOAT16: 8}
 
 
+def _lookup(table, key, what):
+    d = table.get(key)
+    if d is None:
+        raise CastError(f"unknown dtype {what} {key!r}")
+    return d
+
+
 def by_name(name: str) -> DType:
-    try:
-        return _BY_NAME[name]
-    except KeyError:
-        raise CastError(f"unknown dtype name {name!r}") from None
+    return _lookup(_BY_NAME, name, "name")
 
 
 def by_code(code: int) -> DType:
-    try:
-        return _BY_CODE[code]
-    except KeyError:
-        raise CastError(f"unknown dtype wire code {code}") from None
+    return _lookup(_BY_CODE, code, "wire code")
 
 
 by_wire_code = by_code
@@ -107,10 +109,10 @@ def real_counterpart(d: DType) -> DType:
 
 
 def int_range(d: DType):
-    bits = 8 * d.size
-    if d.is_signed:
-        return -(1 << (bits - 1)), (1 << (bits - 1)) - 1
-    return 0, (1 << bits) - 1
+    """(min, max) of an integer dtype's values."""
+    span = 1 << (8 * d.size)
+    lo = -(span >> 1) if d.is_signed else 0
+    return lo, lo + span - 1
 
 
 def float_container(d: DType) -> DType:

@@ -172,15 +172,11 @@ class Tensor:
     __slots__ = ("storage", "offset", "dims", "strides", "dtype", "byteorder", "_so")
 
     def __init__(self, storage, offset, dims, strides, dtype, byteorder=None):
-        dims = _check_dims(dims)
-        strides = tuple(int(s) for s in strides)
-        if len(strides) != len(dims):
+        shape, steps = _check_dims(dims), tuple(map(int, strides))
+        if len(shape) != len(steps):
             raise ShapeError("dims and strides must have equal length")
-        self.storage = storage
-        self.offset = int(offset)
-        self.dims = dims
-        self.strides = strides
-        self.dtype = dtype
+        self.storage, self.dtype = storage, dtype
+        self.offset, self.dims, self.strides = int(offset), shape, steps
         self.byteorder = byteorder or storage.byteorder
         self._so = None
         lo, hi = byte_extent(self)

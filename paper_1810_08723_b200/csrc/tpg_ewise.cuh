@@ -658,7 +658,8 @@ __global__ void __launch_bounds__(256, sizeof(TX) >= 4 ? 4 : 5) k_tile_f32(EwPar
 }
 
 // k_tile_tma: the transposing float kernel fed by TMA (SURVEY cfg2, the
-// headline; the default for 2- and 4-byte X).  The X operand is a 2-D
+// headline; the default for 1-, 2- and 4-byte X; 1-byte X uses 64-B
+// swizzled boxes and two warps per 16-B chunk).  The X operand is a 2-D
 // tensor map over its memory order (reversed plan axes are handled by
 // mirrored tile coordinates and index flips); each 64 x 64 X tile arrives
 // by TMA (one box per 128 B of a tile row, 128-B swizzle) in an XS-stage
@@ -693,14 +694,19 @@ __global__ void __launch_bounds__(256, 4) k_tile_tma(const __grid_constant__ CUt
                                                   EwParams p, int q, int nt0, int ntq, int ymode,
                                                   int rev0, int revq) {
   constexpr int SX = sizeof(TX);
-  static_assert(SX == 2 || SX == 4, "128-B swizzled boxes need 2- or 4-byte X");
+  static_assert(SX == 1 || SX == 2 || SX == 4, "1-, 2- or 4-byte X");
   constexpr int VX = 16 / SX;           // X elements per 16-B chunk
-  constexpr int BQ = 128 / SX;          // box width (elements along q)
+  constexpr int ROWB = SX == 1 ? 64 : 128;  // bytes per box row (64- / 128-B swizzle)
+  constexpr int BQ = ROWB / SX;         // box width (elements along q)
   constexpr int NB = TT / BQ;           // boxes per tile
-  constexpr int BOX = TT * 128;         // bytes per box
+  constexpr int BOX = TT * ROWB;        // bytes per box
   constexpr int STAGE = NB * BOX;       // = TT * TT * SX
-  constexpr int NCH = TT / VX;          // 16-B chunks per tile row
-  static_assert(NCH % 8 == 0, "chunks per warp");
+  constexpr int NCH = TT / VX;          // 16-B chunks per tile row (4, 8 or 16)
+  constexpr int CPB = ROWB / 16;        // chunks per box row
+  // warps per chunk (1-byte X: 4 chunks, so two warps share one, one row
+  // group each) and row groups per warp
+  constexpr int WPC = NCH >= 8 ? 1 : 8 / NCH;
+  constexpr int RGW = 2 / WPC;
   constexpr int Y = 3 - XI;
   extern __shared__ uint8_t tsm_raw[];
   uint8_t* xring = (uint8_t*)(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
@@ -749,23 +755,27 @@ __global__ void __launch_bounds__(256, 4) k_tile_tma(const __grid_constant__ CUt
   // each column address serves two stores, the second at +128 B):
   // shared-memory offsets of the lane's 16-B chunk rows, and the byte offset
   // of each chunk's first plan column from the tile origin
-  constexpr int CPW = NCH / 8;
+  constexpr int CPW = NCH >= 8 ? NCH / 8 : 1;
+  constexpr int WSTEP = 8 / WPC;                             // warps per pass over the chunks
+  const int g0w = (warp / WSTEP) * RGW;                      // first row group of this warp
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(xring);
-  uint32_t soff[CPW][2];
+  uint32_t soff[CPW][RGW];
   int64_t dofs[CPW], yofs[CPW];
 #pragma unroll
   for (int u = 0; u < CPW; ++u) {
-    const int ch = warp + 8 * u;                             // chunk (memory order)
+    const int ch = warp % WSTEP + WSTEP * u;                 // chunk (memory order)
 #pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      const int i = 32 * g + lane;                           // plan row (output fast axis)
+    for (int k = 0; k < RGW; ++k) {
+      const int i = 32 * (g0w + k) + lane;                   // plan row (output fast axis)
       const int rm = rev0 ? TT - 1 - i : i;                  // memory row in the tile
-      soff[u][g] = (uint32_t)((ch / 8) * BOX + rm * 128 + (((ch % 8) ^ (rm & 7)) << 4));
+      const int c = ch % CPB;
+      const int pos = ROWB == 128 ? (c ^ (rm & 7)) : (c ^ ((rm >> 1) & 3));  // TMA swizzle
+      soff[u][k] = (uint32_t)((ch / CPB) * BOX + rm * ROWB + (pos << 4));
     }
     const int jm0 = ch * VX;                                 // memory column of the chunk
     const int jl = revq ? TT - 1 - jm0 : jm0;                // its plan column in the tile
-    dofs[u] = (int64_t)lane * 4 + jl * sdq;
-    yofs[u] = jl * syq + (ymode == 2 ? (int64_t)lane * sy0 : 0);
+    dofs[u] = (int64_t)(32 * g0w + lane) * 4 + jl * sdq;
+    yofs[u] = jl * syq + (ymode == 2 ? (int64_t)(32 * g0w + lane) * sy0 : 0);
   }
   // ymode 1 with a float row of unit stride (either sign) along q: each
   // chunk's VX row values are one aligned 16-32 B run, read as float4s
@@ -788,18 +798,20 @@ __global__ void __launch_bounds__(256, 4) k_tile_tma(const __grid_constant__ CUt
     if (NIN >= 2) ytile = ys + (int64_t)tq * TT * syq + (ymode == 2 ? (int64_t)t0 * TT * sy0 : 0);
 #pragma unroll
     for (int u = 0; u < CPW; ++u) {
-      uint4 raw[2];
+      uint4 raw[RGW];
 #pragma unroll
-      for (int g = 0; g < 2; ++g)
+      for (int g = 0; g < RGW; ++g)
         asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(raw[g].x), "=r"(raw[g].y), "=r"(raw[g].z), "=r"(raw[g].w)
                      : "r"(sbase + s * STAGE + soff[u][g]));
       char* dp = dtile + dofs[u];
-      float yv[2][VX];
+      float yv[RGW][VX];
       if (NIN >= 2) {
         if (ymode == 0) {
 #pragma unroll
-          for (int k = 0; k < VX; ++k) yv[0][k] = yv[1][k] = yimm;
+          for (int k = 0; k < VX; ++k)
+#pragma unroll
+            for (int g = 0; g < RGW; ++g) yv[g][k] = yimm;
         } else if (yvec) {
           const float* yp = (const float*)(ytile + yofs[u]) - (yrev ? VX - 1 : 0);
           float t[VX];
@@ -809,11 +821,13 @@ __global__ void __launch_bounds__(256, 4) k_tile_tma(const __grid_constant__ CUt
             t[4 * h] = f.x; t[4 * h + 1] = f.y; t[4 * h + 2] = f.z; t[4 * h + 3] = f.w;
           }
 #pragma unroll
-          for (int k = 0; k < VX; ++k) yv[0][k] = yv[1][k] = t[yrev ? VX - 1 - k : k];
+          for (int k = 0; k < VX; ++k)
+#pragma unroll
+            for (int g = 0; g < RGW; ++g) yv[g][k] = t[yrev ? VX - 1 - k : k];
         } else {
           const char* yp = ytile + yofs[u];
 #pragma unroll
-          for (int g = 0; g < 2; ++g) {
+          for (int g = 0; g < RGW; ++g) {
             const char* ypg = yp + (ymode == 2 ? g * 32 * sy0 : 0);
 #pragma unroll
             for (int k = 0; k < VX; ++k) yv[g][k] = to_f<TY>(__ldg((const TY*)(ypg + k * ystep)));
@@ -824,7 +838,7 @@ __global__ void __launch_bounds__(256, 4) k_tile_tma(const __grid_constant__ CUt
       for (int k = 0; k < VX; ++k) {
         float* col = (float*)(dp + k * dstep);
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
+        for (int g = 0; g < RGW; ++g) {
           const float x = to_f<TX>(((const TX*)&raw[g])[k]);
           float v = x;
           if (NIN >= 2) v = XI == 1 ? fop<OP>(x, yv[g][k]) : fop<OP>(yv[g][k], x);
@@ -857,7 +871,7 @@ constexpr size_t tile_tma_smem() {
 template <auto K, typename TX>
 bool launch_tile_tma(EwParams& p, Stream* st, int xi, int q, int64_t nt0, int64_t ntq, int ymode) {
   constexpr int SX = sizeof(TX);
-  if ((SX != 2 && SX != 4) || p.ndim != 2) return false;
+  if ((SX != 1 && SX != 2 && SX != 4) || p.ndim != 2) return false;
   const int64_t sq = p.str[xi][q], s0 = p.str[xi][0];
   if ((sq != SX && sq != -SX) || s0 == 0 || (s0 < 0 ? -s0 : s0) % 16) return false;
   const int64_t eq = p.ext[q], e0 = p.ext[0];
@@ -882,13 +896,15 @@ bool launch_tile_tma(EwParams& p, Stream* st, int xi, int q, int64_t nt0, int64_
     MapCache& c = cache[next++ % 8];
     cuuint64_t dims[2] = {(cuuint64_t)eq, (cuuint64_t)e0};
     cuuint64_t strides[1] = {(cuuint64_t)s0a};
-    cuuint32_t box[2] = {(cuuint32_t)(128 / SX), TT};
+    cuuint32_t box[2] = {(cuuint32_t)((SX == 1 ? 64 : 128) / SX), TT};
     cuuint32_t estr[2] = {1, 1};
-    const CUtensorMapDataType ty = SX == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
-                                           : CU_TENSOR_MAP_DATA_TYPE_UINT32;
+    const CUtensorMapDataType ty = SX == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                   : SX == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                             : CU_TENSOR_MAP_DATA_TYPE_UINT32;
     c.lo = nullptr;
     if (enc(&c.map, ty, 2, const_cast<char*>(lo), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE,
+            SX == 1 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
     c.lo = lo;
@@ -917,7 +933,7 @@ bool launch_tile_tma(EwParams& p, Stream* st, int xi, int q, int64_t nt0, int64_
   return true;
 }
 
-// The TMA-fed tile kernel is the default for 2- / 4-byte X (TPG_TILE_TMA=0
+// The TMA-fed tile kernel is the default for 1-, 2- and 4-byte X (TPG_TILE_TMA=0
 // selects the register-staged k_tile_f32 instead, for A/B runs).
 inline bool tile_tma_disabled() {
   static int v = -1;
@@ -1196,8 +1212,8 @@ int launch_ew(EwParams& p, Stream* st) {
             typedef typename Native<(NIN >= 2 ? DTB : DTA)>::T TB;
             if (nrest == 1 && !tile_tma_disabled()) {
               bool ok = false;
-              constexpr bool ta_ok = sizeof(TA) == 2 || sizeof(TA) == 4;
-              constexpr bool tb_ok = sizeof(TB) == 2 || sizeof(TB) == 4;
+              constexpr bool ta_ok = sizeof(TA) <= 4 && sizeof(TA) != 3;
+              constexpr bool tb_ok = sizeof(TB) <= 4 && sizeof(TB) != 3;
               if constexpr (ta_ok) {
                 if (NIN == 1)
                   ok = launch_tile_tma<k_tile_tma<0, 1, 1, TA, TA>, TA>(p, st, 1, qa, nt0, ntq, 0);

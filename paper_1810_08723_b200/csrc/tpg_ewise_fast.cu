@@ -30,6 +30,9 @@ int ew_dispatch_fast(int oc, int op, int kind, EwParams& p, Stream* st, bool* do
   // SURVEY cfg2: int16 view (fused cast-on-load) + float broadcast row
   FAST(OC_BINARY, 2, TPG_ADD, K_FLT, TPG_FLOAT, TPG_INT16, TPG_FLOAT)
   FAST(OC_BINARY, 2, TPG_ADD, K_FLT, TPG_FLOAT, TPG_FLOAT, TPG_INT16)
+  // the same shape family from 8-bit data (e.g. uint8 images viewed
+  // transposed): 1-byte TMA tiles
+  FAST(OC_BINARY, 2, TPG_ADD, K_FLT, TPG_FLOAT, TPG_UINT8, TPG_FLOAT)
   // unary
   FAST(OC_UNARY, 1, TPG_NEGATE, K_FLT, TPG_FLOAT, TPG_FLOAT, -1)
   FAST(OC_UNARY, 1, TPG_NEGATE, K_FLT, TPG_DOUBLE, TPG_DOUBLE, -1)
@@ -41,6 +44,7 @@ int ew_dispatch_fast(int oc, int op, int kind, EwParams& p, Stream* st, bool* do
   FAST(OC_COPY, 1, 0, K_FLT, TPG_FLOAT, TPG_DOUBLE, -1)   // cfg5
   FAST(OC_COPY, 1, 0, K_FLT, TPG_DOUBLE, TPG_FLOAT, -1)
   FAST(OC_COPY, 1, 0, K_INT, TPG_FLOAT, TPG_INT16, -1)    // cfg2 through the table
+  FAST(OC_COPY, 1, 0, K_INT, TPG_FLOAT, TPG_UINT8, -1)
   FAST(OC_COPY, 1, 0, K_INT, TPG_HALF, TPG_INT16, -1)     // cfg5
   FAST(OC_COPY, 1, 0, K_FLT, TPG_HALF, TPG_FLOAT, -1)
   FAST(OC_COPY, 1, 0, K_FLT, TPG_FLOAT, TPG_HALF, -1)

@@ -126,18 +126,6 @@ def decode_store(ref_dtypes, store):
     raise LookupError("unrecognised store closure")
 
 
-def decode_ctx(store):
-    """The CastContext a store closure reports cast loss to (or None)."""
-    return _cells(store).get("ctx")
-
-
-def decode_status(fn):
-    """The status set a scalar function records flags into (kernels.py:72-78,
-    151-156); None for functions that never flag."""
-    s = _cells(fn).get("status")
-    return s if isinstance(s, set) else None
-
-
 def unary_forces_complex(fn) -> bool:
     """unary_scalar_fn returns `lambda v: complex_fn(complex(v))` for the
     complex branch (kernels.py:145-146)."""

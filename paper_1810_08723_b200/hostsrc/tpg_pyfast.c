@@ -783,11 +783,14 @@ static PyMethodDef pool_methods[] = {
  */
 typedef int (*f_binary)(void*, int, const tpg_plan*, const tpg_operand*, const tpg_operand*,
                         const tpg_operand*, int, int);
+typedef int (*f_unary)(void*, int, const tpg_plan*, const tpg_operand*, const tpg_operand*, int,
+                       int, int);
 
 typedef struct {
   PyObject_HEAD
   BlockPool* pool;
   f_binary binary;
+  f_unary unary; /* optional (set_unary) */
   PyObject *rt, *tls, *lazy, *lazy_by_src, *codecs, *stats;
   PyObject* cell_idx; /* {(code, tag): tuple of closure indices} */
   PyObject* lazy_cls; /* tidepool_plugin._Lazy */
@@ -1295,6 +1298,125 @@ static PyObject* entries_binary_(Entries* e, PyObject* const* args, Py_ssize_t n
 }
 
 static PyObject* entries_copy(Entries* e, PyObject* const* args, Py_ssize_t nargs);
+static PyObject *S_complex_fn, *S_complex_tag;
+
+/* The gpu table's unary entries (negate ... conjugate) for the common case:
+ * standard mode, a real gpu source and destination of one device, no
+ * pending copy on either, a scalar fn without the complex promotion
+ * (unary_forces_complex).  Same contract as entries_binary. */
+static PyObject* entries_unary(Entries* e, PyObject* const* args, Py_ssize_t nargs) {
+  if (nargs != 8 || !e->unary) Py_RETURN_NONE;
+  const int op = (int)PyLong_AsLong(args[0]);
+  PyObject *plan = args[1], *store = args[3], *fn = args[6], *bases = args[7];
+  if (PyErr_Occurred()) return NULL;
+#define FALLBACK()   \
+  do {               \
+    PyErr_Clear();   \
+    e->n_fallback++; \
+    Py_RETURN_NONE;  \
+  } while (0)
+  PyObject* sc[3];
+  PyObject* const snames[3] = {S_pack, S_mode, S_ctx};
+  int r = closure_cells(e, store, S_store_tag, snames, 3, sc);
+  if (r == -2) return NULL;
+  if (r < 0 || !sc[0]) FALLBACK();
+  if (sc[1] && sc[1] != S_standard && PyUnicode_Compare(sc[1], S_standard) != 0) FALLBACK();
+  CodecInfo cd, ca;
+  if (codec_info(e, sc[0], &cd) || codec_info(e, args[5], &ca)) FALLBACK();
+  if (ca.wire >= 12 || cd.wire >= 12) FALLBACK(); /* complex: the Python entry */
+  PyObject* fc[1];
+  PyObject* const fcn[1] = {S_complex_fn};
+  r = closure_cells(e, fn, S_complex_tag, fcn, 1, fc);
+  if (r == -2) return NULL;
+  if (r == 0 && fc[0]) FALLBACK(); /* unary_forces_complex */
+  DevBuf *bd = devbuf_of(args[2]), *ba = devbuf_of(args[4]);
+  if (!bd || !ba || ba->dev != bd->dev) FALLBACK();
+  const int dev = bd->dev;
+  int64_t ext[TPG_MAX_DIMS], str[2][TPG_MAX_DIMS];
+  PyObject *pe = PyObject_GetAttr(plan, S_extents), *ps = PyObject_GetAttr(plan, S_strides);
+  int nd = pe ? i64_seq(pe, ext, TPG_MAX_DIMS) : -1;
+  int ok = nd >= 0 && ps && PySequence_Check(ps) && PySequence_Size(ps) == 2;
+  for (int v = 0; ok && v < 2; ++v) {
+    PyObject* sv = PySequence_GetItem(ps, v);
+    ok = sv && i64_seq(sv, str[v], TPG_MAX_DIMS) == nd;
+    Py_XDECREF(sv);
+  }
+  Py_XDECREF(pe);
+  Py_XDECREF(ps);
+  if (!ok || !PyTuple_Check(bases) || PyTuple_GET_SIZE(bases) != 2) FALLBACK();
+  const int64_t b0 = PyLong_AsLongLong(PyTuple_GET_ITEM(bases, 0));
+  const int64_t b1 = PyLong_AsLongLong(PyTuple_GET_ITEM(bases, 1));
+  if (PyErr_Occurred()) FALLBACK();
+  if (PyDict_GET_SIZE(e->lazy) || PyDict_GET_SIZE(e->lazy_by_src)) {
+    PyObject *kd = PyLong_FromVoidPtr(bd->ptr), *ka = PyLong_FromVoidPtr(ba->ptr);
+    const int busy = !kd || !ka || PyDict_Contains(e->lazy, kd) == 1 ||
+                     PyDict_Contains(e->lazy_by_src, kd) == 1 || PyDict_Contains(e->lazy, ka) == 1;
+    Py_XDECREF(kd);
+    Py_XDECREF(ka);
+    if (busy || PyErr_Occurred()) FALLBACK();
+  }
+  void* handle = e->defaults[dev];
+  PyObject* st = PyObject_GetAttr(e->tls, S_stream);
+  if (!st) {
+    PyErr_Clear();
+  } else if (st != Py_None) {
+    int bad = 0;
+    PyObject* sdev = PyObject_GetAttr(st, S_device);
+    int64_t sidx = sdev ? attr_i64(sdev, S_index, &bad) : (bad = 1, 0);
+    Py_XDECREF(sdev);
+    if (!bad && sidx == dev) handle = (void*)(intptr_t)attr_i64(st, S_handle, &bad);
+    if (bad) {
+      Py_DECREF(st);
+      FALLBACK();
+    }
+  }
+  Py_XDECREF(st);
+  if (!handle) FALLBACK();
+  PyObject* stc[1];
+  PyObject* const stn[1] = {S_status};
+  r = closure_cells(e, fn, S_status_tag, stn, 1, stc);
+  if (r == -2) return NULL;
+  if (r == 0 && stc[0] && PySet_Check(stc[0])) {
+    PyObject* cur = PyObject_GetAttr(e->rt, S_status_sink);
+    if (cur != stc[0] && PyObject_SetAttr(e->rt, S_status_sink, stc[0]) < 0) {
+      Py_XDECREF(cur);
+      return NULL;
+    }
+    Py_XDECREF(cur);
+    PyErr_Clear();
+  }
+  tpg_plan p;
+  memset(&p, 0, sizeof p);
+  p.ndim = nd;
+  p.nviews = 2;
+  for (int i = 0; i < nd; ++i) {
+    p.extent[i] = ext[i];
+    p.stride[0][i] = str[0][i];
+    p.stride[1][i] = str[1][i];
+  }
+  tpg_operand od, oa;
+  memset(&od, 0, sizeof od);
+  memset(&oa, 0, sizeof oa);
+  od.base = bd->ptr;
+  od.offset = b0;
+  od.dtype = cd.wire;
+  od.big_endian = cd.big;
+  oa.base = ba->ptr;
+  oa.offset = b1;
+  oa.dtype = ca.wire;
+  oa.big_endian = ca.big;
+  e->pool->seq++;
+  const int rc = e->unary(handle, op, &p, &od, &oa, ca.compute, 0, 0);
+  e->n_fast++;
+  return PyLong_FromLong(rc);
+#undef FALLBACK
+}
+
+static PyObject* entries_set_unary(Entries* e, PyObject* addr) {
+  e->unary = (f_unary)PyLong_AsVoidPtr(addr);
+  if (PyErr_Occurred()) return NULL;
+  Py_RETURN_NONE;
+}
 
 /* A gpu table entry callable in C: tries the fast path (when the plugin's
  * profiling hook is off) and otherwise calls the Python entry `slow` with
@@ -1328,11 +1450,17 @@ static PyObject* fastentry_call(FastEntry* f, PyObject* args, PyObject* kw) {
     } else if (off && f->kind == 1 && n == 7) {
       r = entries_copy(f->e, ((PyTupleObject*)args)->ob_item, 7);
       tried = 1;
+    } else if (off && f->kind == 2 && n == 7) {
+      PyObject* a[8];
+      a[0] = f->opobj;
+      for (int i = 0; i < 7; ++i) a[i + 1] = PyTuple_GET_ITEM(args, i);
+      r = entries_unary(f->e, a, 8);
+      tried = 1;
     }
     if (tried) {
       if (!r) return NULL;
       if (r != Py_None) {
-        if (f->kind == 0) {
+        if (f->kind == 0 || f->kind == 2) {
           const long rc = PyLong_AsLong(r);
           Py_DECREF(r);
           if (rc) {
@@ -1377,8 +1505,8 @@ static PyObject* entries_entry(Entries* e, PyObject* args) {
   int kind, op;
   PyObject* slow;
   if (!PyArg_ParseTuple(args, "iiO", &kind, &op, &slow)) return NULL;
-  if (kind != 0 && kind != 1) {
-    PyErr_SetString(PyExc_ValueError, "kind: 0 binary, 1 copy");
+  if (kind < 0 || kind > 2) {
+    PyErr_SetString(PyExc_ValueError, "kind: 0 binary, 1 copy, 2 unary");
     return NULL;
   }
   FastEntry* f = PyObject_GC_New(FastEntry, &FastEntryType);
@@ -1603,7 +1731,8 @@ static PyMethodDef entries_methods[] = {
      "set_copy_support(lazy class, {codec fn: (dtype, order)}, lossless table bytes)"},
     {"counts", (PyCFunction)entries_counts, METH_NOARGS, "fast / fallback call counts"},
     {"entry", (PyCFunction)entries_entry, METH_VARARGS,
-     "entry(kind, op code, python entry) -> table callable (kind 0 binary, 1 copy)"},
+     "entry(kind, op code, python entry) -> table callable (kind 0 binary, 1 copy, 2 unary)"},
+    {"set_unary", (PyCFunction)entries_set_unary, METH_O, "set_unary(tpg_unary address)"},
     {NULL}};
 
 static int intern_names(void) {
@@ -1716,6 +1845,8 @@ PyMODINIT_FUNC PyInit__tpg_pyfast(void) {
   EntriesType.tp_methods = entries_methods;
   if (PyType_Ready(&EntriesType) < 0) return NULL;
   if (!(S_profile = PyUnicode_InternFromString("profile"))) return NULL;
+  if (!(S_complex_fn = PyUnicode_InternFromString("complex_fn"))) return NULL;
+  if (!(S_complex_tag = PyUnicode_InternFromString("#complex"))) return NULL;
   if (!(S_check = PyUnicode_InternFromString("check"))) return NULL;
   if (!(S_kernel = PyUnicode_InternFromString("kernel"))) return NULL;
   FastEntryType.tp_name = "_tpg_pyfast.FastEntry";

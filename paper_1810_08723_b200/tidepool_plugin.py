@@ -243,6 +243,19 @@ def _binary_function(L, abi):
     return C.cast(cb, C.c_void_p).value
 
 
+def _unary_function(L, abi):
+    """Address of tpg_unary for the C entry (a ctypes callback into a
+    duck-typed test double)."""
+    if isinstance(L, C.CDLL):
+        return C.cast(L.tpg_unary, C.c_void_p).value
+    PP, PO = C.POINTER(abi.Plan), C.POINTER(abi.Operand)
+    cb = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, PP, PO, PO, C.c_int, C.c_int, C.c_int)(
+        lambda st, op, p, d, a, comp, mode, fc: L.tpg_unary(st, op, p.contents, d.contents,
+                                                            a.contents, comp, mode, fc))
+    _CALLBACKS.append(cb)
+    return C.cast(cb, C.c_void_p).value
+
+
 _CALLBACKS: list = []  # ctypes callbacks handed to C (kept alive)
 
 
@@ -526,6 +539,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
             lossless_table[a_.wire_code * 32 + b_.wire_code] = \
                 int(bool(ref_dtypes.lossless_castable(a_, b_)))
     rt.entries.set_copy_support(_Lazy, dict(codec_of), bytes(lossless_table))
+    rt.entries.set_unary(_unary_function(L, abi))
 
     # -- devices and streams ------------------------------------------------------
     class GpuStream(ref_devices.Stream):
@@ -793,7 +807,11 @@ def register(tidepool_module, count: int | None = None, lib=None):
             _run(st, mode, ctx, dd, lambda: L.tpg_unary(*args), lambda: L.tpg_unary_check(*args))
             temps.done()
         h.__name__ = f"gpu_{op}"
-        return h
+        if op == "identity":
+            return h
+        # unary ops: C fast path (standard mode, real gpu operands of one
+        # device; tpg_pyfast.c FastEntry kind 2), this Python entry otherwise
+        return rt.entries.entry(2, code, h)
 
     lossless = {}
 

@@ -369,6 +369,24 @@ def test_c_entry_fast_paths_match_the_python_entries(env):
         assert tp.tensors.read_values(got_fast) == tp.tensors.read_values(want), it
         assert got_fast.storage.snapshot() == want.storage.snapshot(), it
         assert got_py.storage.snapshot() == want.storage.snapshot(), it
+    for it in range(12):   # unary entries (kind 2)
+        d = rng.choice([tp.float, tp.double, tp.int16, tp.half])
+        n = rng.randint(1, 30)
+        name = rng.choice(["negate", "absolute", "square_root", "exponential", "sine"])
+        lo = 0 if name == "square_root" else -20   # (NaN payloads are not compared bytewise)
+        xs = [rng.randint(lo, 20) for _ in range(n)]
+        A = tp.from_nested(xs, d)
+        op = getattr(tp, name)
+        want = op(A)
+        Ag = tp.cast(A, device=gpu)
+        got_fast = op(Ag)
+        rt.profile = []
+        try:
+            got_py = op(Ag)
+        finally:
+            rt.profile = None
+        assert got_fast.storage.snapshot() == want.storage.snapshot(), (it, op)
+        assert got_py.storage.snapshot() == want.storage.snapshot(), (it, op)
     c1 = rt.entries.counts()
     assert c1["fast"] > c0["fast"]
     # error mode goes to the Python entry (CastContext semantics live there)

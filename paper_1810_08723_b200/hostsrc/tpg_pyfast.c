@@ -785,12 +785,15 @@ typedef int (*f_binary)(void*, int, const tpg_plan*, const tpg_operand*, const t
                         const tpg_operand*, int, int);
 typedef int (*f_unary)(void*, int, const tpg_plan*, const tpg_operand*, const tpg_operand*, int,
                        int, int);
+typedef int (*f_reduce)(void*, int, double, const tpg_plan*, const tpg_plan*, const tpg_operand*,
+                        const tpg_operand*, int, int);
 
 typedef struct {
   PyObject_HEAD
   BlockPool* pool;
   f_binary binary;
   f_unary unary; /* optional (set_unary) */
+  f_reduce reduce; /* optional (set_reduce) */
   PyObject *rt, *tls, *lazy, *lazy_by_src, *codecs, *stats;
   PyObject* cell_idx; /* {(code, tag): tuple of closure indices} */
   PyObject* lazy_cls; /* tidepool_plugin._Lazy */
@@ -1412,6 +1415,124 @@ static PyObject* entries_unary(Entries* e, PyObject* const* args, Py_ssize_t nar
 #undef FALLBACK
 }
 
+/* plan attributes -> tpg_plan with `nv` views; -1 on mismatch */
+static int read_plan(PyObject* plan, int nv, tpg_plan* p) {
+  int64_t ext[TPG_MAX_DIMS];
+  PyObject *pe = PyObject_GetAttr(plan, S_extents), *ps = PyObject_GetAttr(plan, S_strides);
+  int nd = pe ? i64_seq(pe, ext, TPG_MAX_DIMS) : -1;
+  int ok = nd >= 0 && ps && PySequence_Check(ps) && PySequence_Size(ps) == nv;
+  memset(p, 0, sizeof *p);
+  for (int v = 0; ok && v < nv; ++v) {
+    PyObject* sv = PySequence_GetItem(ps, v);
+    ok = sv && i64_seq(sv, p->stride[v], TPG_MAX_DIMS) == nd;
+    Py_XDECREF(sv);
+  }
+  Py_XDECREF(pe);
+  Py_XDECREF(ps);
+  if (!ok) return -1;
+  p->ndim = nd;
+  p->nviews = nv;
+  for (int i = 0; i < nd; ++i) p->extent[i] = ext[i];
+  return 0;
+}
+
+static PyObject *S_p, *S_norm_tag;
+
+/* The gpu table's reduction entries (reference signature (outer, inner,
+ * d_buf, store, a_buf, a_unpack, init, step, fin, bases), ops.py:522-556)
+ * for the common case: standard mode, gpu source and destination of one
+ * device, no pending copy on either.  args[0] = op code, args[1] = 1 for
+ * the norm (its order is the `p` cell of the step closure). */
+static PyObject* entries_reduce(Entries* e, PyObject* const* args, Py_ssize_t nargs) {
+  if (nargs != 12 || !e->reduce) Py_RETURN_NONE;
+  const int op = (int)PyLong_AsLong(args[0]);
+  const int is_norm = PyObject_IsTrue(args[1]);
+  PyObject *outer = args[2], *inner = args[3], *store = args[5], *step = args[9],
+           *bases = args[11];
+  if (PyErr_Occurred()) return NULL;
+#define FALLBACK()   \
+  do {               \
+    PyErr_Clear();   \
+    e->n_fallback++; \
+    Py_RETURN_NONE;  \
+  } while (0)
+  PyObject* sc[3];
+  PyObject* const snames[3] = {S_pack, S_mode, S_ctx};
+  int r = closure_cells(e, store, S_store_tag, snames, 3, sc);
+  if (r == -2) return NULL;
+  if (r < 0 || !sc[0]) FALLBACK();
+  if (sc[1] && sc[1] != S_standard && PyUnicode_Compare(sc[1], S_standard) != 0) FALLBACK();
+  CodecInfo cd, ca;
+  if (codec_info(e, sc[0], &cd) || codec_info(e, args[7], &ca)) FALLBACK();
+  double pnorm = 2.0;
+  if (is_norm) {
+    PyObject* pc[1];
+    PyObject* const pn[1] = {S_p};
+    r = closure_cells(e, step, S_norm_tag, pn, 1, pc);
+    if (r == -2) return NULL;
+    if (r == 0 && pc[0]) {
+      pnorm = PyFloat_AsDouble(pc[0]);
+      if (PyErr_Occurred()) FALLBACK();
+    }
+  }
+  DevBuf *bd = devbuf_of(args[4]), *ba = devbuf_of(args[6]);
+  if (!bd || !ba || ba->dev != bd->dev) FALLBACK();
+  const int dev = bd->dev;
+  tpg_plan po, pi;
+  if (read_plan(outer, 2, &po) || read_plan(inner, 1, &pi)) FALLBACK();
+  if (!PyTuple_Check(bases) || PyTuple_GET_SIZE(bases) != 2) FALLBACK();
+  const int64_t b0 = PyLong_AsLongLong(PyTuple_GET_ITEM(bases, 0));
+  const int64_t b1 = PyLong_AsLongLong(PyTuple_GET_ITEM(bases, 1));
+  if (PyErr_Occurred()) FALLBACK();
+  if (PyDict_GET_SIZE(e->lazy) || PyDict_GET_SIZE(e->lazy_by_src)) {
+    PyObject *kd = PyLong_FromVoidPtr(bd->ptr), *ka = PyLong_FromVoidPtr(ba->ptr);
+    const int busy = !kd || !ka || PyDict_Contains(e->lazy, kd) == 1 ||
+                     PyDict_Contains(e->lazy_by_src, kd) == 1 || PyDict_Contains(e->lazy, ka) == 1;
+    Py_XDECREF(kd);
+    Py_XDECREF(ka);
+    if (busy || PyErr_Occurred()) FALLBACK();
+  }
+  void* handle = e->defaults[dev];
+  PyObject* st = PyObject_GetAttr(e->tls, S_stream);
+  if (!st) {
+    PyErr_Clear();
+  } else if (st != Py_None) {
+    int bad = 0;
+    PyObject* sdev = PyObject_GetAttr(st, S_device);
+    int64_t sidx = sdev ? attr_i64(sdev, S_index, &bad) : (bad = 1, 0);
+    Py_XDECREF(sdev);
+    if (!bad && sidx == dev) handle = (void*)(intptr_t)attr_i64(st, S_handle, &bad);
+    if (bad) {
+      Py_DECREF(st);
+      FALLBACK();
+    }
+  }
+  Py_XDECREF(st);
+  if (!handle) FALLBACK();
+  tpg_operand od, oa;
+  memset(&od, 0, sizeof od);
+  memset(&oa, 0, sizeof oa);
+  od.base = bd->ptr;
+  od.offset = b0;
+  od.dtype = cd.wire;
+  od.big_endian = cd.big;
+  oa.base = ba->ptr;
+  oa.offset = b1;
+  oa.dtype = ca.wire;
+  oa.big_endian = ca.big;
+  e->pool->seq++;
+  const int rc = e->reduce(handle, op, pnorm, &po, &pi, &od, &oa, ca.compute, 0);
+  e->n_fast++;
+  return PyLong_FromLong(rc);
+#undef FALLBACK
+}
+
+static PyObject* entries_set_reduce(Entries* e, PyObject* addr) {
+  e->reduce = (f_reduce)PyLong_AsVoidPtr(addr);
+  if (PyErr_Occurred()) return NULL;
+  Py_RETURN_NONE;
+}
+
 static PyObject* entries_set_unary(Entries* e, PyObject* addr) {
   e->unary = (f_unary)PyLong_AsVoidPtr(addr);
   if (PyErr_Occurred()) return NULL;
@@ -1456,11 +1577,18 @@ static PyObject* fastentry_call(FastEntry* f, PyObject* args, PyObject* kw) {
       for (int i = 0; i < 7; ++i) a[i + 1] = PyTuple_GET_ITEM(args, i);
       r = entries_unary(f->e, a, 8);
       tried = 1;
+    } else if (off && (f->kind == 3 || f->kind == 4) && n == 10) {
+      PyObject* a[12];
+      a[0] = f->opobj;
+      a[1] = f->kind == 4 ? Py_True : Py_False;
+      for (int i = 0; i < 10; ++i) a[i + 2] = PyTuple_GET_ITEM(args, i);
+      r = entries_reduce(f->e, a, 12);
+      tried = 1;
     }
     if (tried) {
       if (!r) return NULL;
       if (r != Py_None) {
-        if (f->kind == 0 || f->kind == 2) {
+        if (f->kind != 1) {
           const long rc = PyLong_AsLong(r);
           Py_DECREF(r);
           if (rc) {
@@ -1505,8 +1633,8 @@ static PyObject* entries_entry(Entries* e, PyObject* args) {
   int kind, op;
   PyObject* slow;
   if (!PyArg_ParseTuple(args, "iiO", &kind, &op, &slow)) return NULL;
-  if (kind < 0 || kind > 2) {
-    PyErr_SetString(PyExc_ValueError, "kind: 0 binary, 1 copy, 2 unary");
+  if (kind < 0 || kind > 4) {
+    PyErr_SetString(PyExc_ValueError, "kind: 0 binary, 1 copy, 2 unary, 3 reduce, 4 norm");
     return NULL;
   }
   FastEntry* f = PyObject_GC_New(FastEntry, &FastEntryType);
@@ -1733,6 +1861,7 @@ static PyMethodDef entries_methods[] = {
     {"entry", (PyCFunction)entries_entry, METH_VARARGS,
      "entry(kind, op code, python entry) -> table callable (kind 0 binary, 1 copy, 2 unary)"},
     {"set_unary", (PyCFunction)entries_set_unary, METH_O, "set_unary(tpg_unary address)"},
+    {"set_reduce", (PyCFunction)entries_set_reduce, METH_O, "set_reduce(tpg_reduce address)"},
     {NULL}};
 
 static int intern_names(void) {
@@ -1847,6 +1976,8 @@ PyMODINIT_FUNC PyInit__tpg_pyfast(void) {
   if (!(S_profile = PyUnicode_InternFromString("profile"))) return NULL;
   if (!(S_complex_fn = PyUnicode_InternFromString("complex_fn"))) return NULL;
   if (!(S_complex_tag = PyUnicode_InternFromString("#complex"))) return NULL;
+  if (!(S_p = PyUnicode_InternFromString("p"))) return NULL;
+  if (!(S_norm_tag = PyUnicode_InternFromString("#norm"))) return NULL;
   if (!(S_check = PyUnicode_InternFromString("check"))) return NULL;
   if (!(S_kernel = PyUnicode_InternFromString("kernel"))) return NULL;
   FastEntryType.tp_name = "_tpg_pyfast.FastEntry";

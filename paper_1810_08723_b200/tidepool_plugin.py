@@ -256,6 +256,19 @@ def _unary_function(L, abi):
     return C.cast(cb, C.c_void_p).value
 
 
+def _reduce_function(L, abi):
+    """Address of tpg_reduce for the C entry (a ctypes callback into a
+    duck-typed test double)."""
+    if isinstance(L, C.CDLL):
+        return C.cast(L.tpg_reduce, C.c_void_p).value
+    PP, PO = C.POINTER(abi.Plan), C.POINTER(abi.Operand)
+    cb = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_double, PP, PP, PO, PO, C.c_int, C.c_int)(
+        lambda st, op, pn, po, pi, d, a, comp, mode: L.tpg_reduce(
+            st, op, pn, po.contents, pi.contents, d.contents, a.contents, comp, mode))
+    _CALLBACKS.append(cb)
+    return C.cast(cb, C.c_void_p).value
+
+
 _CALLBACKS: list = []  # ctypes callbacks handed to C (kept alive)
 
 
@@ -540,6 +553,7 @@ def register(tidepool_module, count: int | None = None, lib=None):
                 int(bool(ref_dtypes.lossless_castable(a_, b_)))
     rt.entries.set_copy_support(_Lazy, dict(codec_of), bytes(lossless_table))
     rt.entries.set_unary(_unary_function(L, abi))
+    rt.entries.set_reduce(_reduce_function(L, abi))
 
     # -- devices and streams ------------------------------------------------------
     class GpuStream(ref_devices.Stream):
@@ -873,7 +887,10 @@ def register(tidepool_module, count: int | None = None, lib=None):
             _run(st, mode, ctx, dd, lambda: L.tpg_reduce(*args))
             temps.done()
         h.__name__ = f"gpu_reduce_{op}"
-        return h
+        # C fast path (standard mode, gpu operands of one device), this
+        # Python entry otherwise (kind 4: the norm, whose order is read from
+        # the step closure)
+        return rt.entries.entry(4 if op == "norm" else 3, code, h)
 
     def matmul(d_buf, d_base, d_strides, store, a_buf, a_base, a_strides, a_unpack, b_buf,
                b_base, b_strides, b_unpack, m, n, k, mul, init, step, fin):

@@ -387,6 +387,24 @@ def test_c_entry_fast_paths_match_the_python_entries(env):
             rt.profile = None
         assert got_fast.storage.snapshot() == want.storage.snapshot(), (it, op)
         assert got_py.storage.snapshot() == want.storage.snapshot(), (it, op)
+    for it in range(10):   # reduction entries (kinds 3 / 4)
+        d = rng.choice([tp.float, tp.double, tp.int32])
+        r, c = rng.randint(1, 7), rng.randint(1, 7)
+        A = tp.from_nested([[rng.randint(-9, 9) for _ in range(c)] for _ in range(r)], d)
+        name = rng.choice(["sum", "maximum", "minimum", "norm"])
+        axes = rng.choice([None, (0,), (1,)])
+        want = tp.reduce(name, A, axes=axes)
+        Ag = tp.cast(A, device=gpu)
+        f0 = rt.entries.counts()["fast"]
+        got_fast = tp.reduce(name, Ag, axes=axes)
+        assert rt.entries.counts()["fast"] > f0, (it, name)
+        rt.profile = []
+        try:
+            got_py = tp.reduce(name, Ag, axes=axes)
+        finally:
+            rt.profile = None
+        assert tp.tensors.read_values(got_fast) == tp.tensors.read_values(want), (it, name)
+        assert tp.tensors.read_values(got_py) == tp.tensors.read_values(want), (it, name)
     c1 = rt.entries.counts()
     assert c1["fast"] > c0["fast"]
     # error mode goes to the Python entry (CastContext semantics live there)

@@ -303,6 +303,8 @@ def _pool_functions(L):
         return 0
 
     def mark(st, word, value):
+        if getattr(L, "fail_marks", False):  # test hook: no stream memory ops -> events
+            return -4
         C.c_uint64.from_address(word).value = value
         return 0
     cbs = (C.CFUNCTYPE(I, I, C.c_size_t, PP)(malloc_managed),

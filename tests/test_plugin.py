@@ -474,3 +474,29 @@ def test_recycled_blocks_wait_for_their_last_gpu_use():
         assert np.array_equal(got, pattern), i
         del fresh
     assert rt.pool.stats()["reused"] > stats0["reused"]
+
+
+def test_block_pool_falls_back_to_events_without_stream_memory_ops():
+    """Where tpg_stream_mark is unavailable the block pool records CUDA
+    events instead of completion words; blocks are still recycled and every
+    result equals the cpu device's (CPU test double, marks failing)."""
+    tp = ref_loader.load("tidepool_events_plugin")
+    if tp is None:
+        pytest.skip("reference tidepool not found")
+    from oracle import oracle
+
+    from paper_1810_08723_b200 import tidepool_plugin
+    fake = FakeNative(oracle.lib())
+    fake.fail_marks = True
+    gpu = tidepool_plugin.register(tp, count=1, lib=fake)[0]
+    rt = tidepool_plugin.register.runtime
+    rng = random.Random(41)
+    for it in range(40):
+        xs = [[rng.randint(-50, 50) for _ in range(6)] for _ in range(5)]
+        X, R = tp.from_nested(xs, tp.int16), tp.from_nested([[1.5] * 6], tp.float)
+        want = tp.add(X, R)
+        got = tp.add(tp.cast(X, device=gpu), tp.cast(R, device=gpu))
+        assert got.storage.snapshot() == want.storage.snapshot(), it
+    st = rt.pool.stats()
+    assert st["reused"] > 0 and st["released"] > 0
+    assert st["event_pool"] > 0   # markers were events (recycled into the event pool)

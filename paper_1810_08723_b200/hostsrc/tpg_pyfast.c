@@ -1774,7 +1774,11 @@ static PyObject* entries_copy_(Entries* e, PyObject* const* args, Py_ssize_t nar
   }
   e->pool->seq++; /* rt.current() */
   PyObject* lz = PyObject_CallNoArgs(e->lazy_cls);
-  int err = !lz || !PyObject_TypeCheck(lz, &LazyRecordType);
+  int err = !lz;
+  if (lz && !PyObject_TypeCheck(lz, &LazyRecordType)) {
+    PyErr_SetString(PyExc_TypeError, "the copy record class must derive from LazyRecord");
+    err = 1;
+  }
   if (!err) {
     LazyRecord* r = (LazyRecord*)lz;
 #define LR_SET(field, val) \

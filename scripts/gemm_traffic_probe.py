@@ -22,11 +22,14 @@ for _ in range(2):
     tp.matmul(A, B, dest=Cm)
     tp.matmul_batched(Ab, Bb, dest=Cb)
 dev.default_stream().sync()
+# distinct A and B buffers (as for ours), so DRAM traffic is comparable
 At = (torch.rand((m, m), device="cuda") * 2 - 1).half()
+Bt = (torch.rand((m, m), device="cuda") * 2 - 1).half()
 Ct = torch.empty_like(At)
 Abt = (torch.rand((64, 2048, 2048), device="cuda") * 2 - 1).half()
+Bbt = (torch.rand((64, 2048, 2048), device="cuda") * 2 - 1).half()
 Cbt = torch.empty_like(Abt)
 for _ in range(2):
-    torch.matmul(At, At, out=Ct)
-    torch.bmm(Abt, Abt, out=Cbt)
+    torch.matmul(At, Bt, out=Ct)
+    torch.bmm(Abt, Bbt, out=Cbt)
 torch.cuda.synchronize()

@@ -70,11 +70,14 @@ def sustained(kind, seconds=3.0):
         import numpy as np
         dev = tp.gpu(0)
         h = np.asfortranarray(np.random.default_rng(6).uniform(-1, 1, (m, m)).astype(np.float16))
-        A, B = tp.transpose(tp.from_numpy(h, dev)), tp.from_numpy(h, dev)
+        h2 = np.asfortranarray(np.random.default_rng(8).uniform(-1, 1, (m, m)).astype(np.float16))
+        A, B = tp.transpose(tp.from_numpy(h, dev)), tp.from_numpy(h2, dev)
         Cm = tp.tensor_create((m, m), tp.half, dev)
         hb = np.asfortranarray(np.random.default_rng(7).uniform(-1, 1, (2048, 2048, 64))
                                .astype(np.float16))
-        Ab, Bb = tp.from_numpy(hb, dev), tp.from_numpy(hb, dev)
+        hb2 = np.asfortranarray(np.random.default_rng(9).uniform(-1, 1, (2048, 2048, 64))
+                                .astype(np.float16))
+        Ab, Bb = tp.from_numpy(hb, dev), tp.from_numpy(hb2, dev)
         Cb = tp.tensor_create((2048, 2048, 64), tp.half, dev)
         cases = {"f16_8192^3": (lambda: tp.matmul(A, B, dest=Cm), 2 * m ** 3,
                                 lambda: dev.default_stream().sync()),
@@ -82,12 +85,14 @@ def sustained(kind, seconds=3.0):
                              lambda: dev.default_stream().sync())}
     else:
         A = (torch.rand((m, m), device="cuda") * 2 - 1).half()
+        B = (torch.rand((m, m), device="cuda") * 2 - 1).half()
         C = torch.empty_like(A)
         Ab = (torch.rand((64, 2048, 2048), device="cuda") * 2 - 1).half()
+        Bb = (torch.rand((64, 2048, 2048), device="cuda") * 2 - 1).half()
         Cb = torch.empty_like(Ab)
-        cases = {"f16_8192^3": (lambda: torch.matmul(A, A, out=C), 2 * m ** 3,
+        cases = {"f16_8192^3": (lambda: torch.matmul(A, B, out=C), 2 * m ** 3,
                                 torch.cuda.synchronize),
-                 "batched": (lambda: torch.bmm(Ab, Ab, out=Cb), 64 * 2 * 2048 ** 3,
+                 "batched": (lambda: torch.bmm(Ab, Bb, out=Cb), 64 * 2 * 2048 ** 3,
                              torch.cuda.synchronize)}
     for name, (fn, flops, sync) in cases.items():
         samples, stop = [], threading.Event()

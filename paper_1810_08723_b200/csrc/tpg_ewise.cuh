@@ -739,12 +739,9 @@ __global__ void __launch_bounds__(256, 4) k_tile_tma(const __grid_constant__ CUt
           : "memory");
   };
   if (threadIdx.x == 0) {
-    for (int s = 0; s < XS; ++s) {
+    for (int s = 0; s < XS; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
           (uint32_t)__cvta_generic_to_shared(&bar[s])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(
-          (uint32_t)__cvta_generic_to_shared(&bar[XS + s])));
-    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&xmap) : "memory");
   }
@@ -795,16 +792,6 @@ __global__ void __launch_bounds__(256, 4) k_tile_tma(const __grid_constant__ CUt
   const int g0 = (int)gridDim.x % nt0, gq = (int)gridDim.x / nt0;
   for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++it) {
     const int s = it % XS;
-    // refill the previous tile's stage once all 8 warps released it (its
-    // empty barrier); only thread 0 waits, the other warps run ahead
-    if (threadIdx.x == 0 && it > 0) {
-      const int sp = (it - 1) % XS;
-      const int wn = w - (int)gridDim.x + XS * (int)gridDim.x;
-      if (wn < nwork) {
-        tma_mbar_wait(sbase + XS * STAGE + (XS + sp) * 8, ((it - 1) / XS) & 1);
-        issue(wn, sp);
-      }
-    }
     tma_mbar_wait(sbase + XS * STAGE + s * 8, (it / XS) & 1);
     char* dtile = ds + (int64_t)t0 * TT * 4 + (int64_t)tq * TT * sdq;
     const char* ytile = nullptr;
@@ -859,11 +846,11 @@ __global__ void __launch_bounds__(256, 4) k_tile_tma(const __grid_constant__ CUt
         }
       }
     }
-    __syncwarp();  // stage s consumed by this warp
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sbase + XS * STAGE +
-                                                                      (XS + s) * 8)
-                   : "memory");
+    __syncthreads();  // stage s consumed by every warp
+    if (threadIdx.x == 0) {
+      const int wn = w + XS * gridDim.x;
+      if (wn < nwork) issue(wn, s);
+    }
     t0 += g0;
     tq += gq;
     if (t0 >= nt0) {
@@ -875,7 +862,7 @@ __global__ void __launch_bounds__(256, 4) k_tile_tma(const __grid_constant__ CUt
 
 template <int SX>
 constexpr size_t tile_tma_smem() {
-  return (size_t)XS * TT * TT * SX + 2 * XS * 8 + 1024;
+  return (size_t)XS * TT * TT * SX + XS * 8 + 1024;
 }
 
 // TMA launch of the cfg2 pattern: 2-D plan, X unit-stride (+-) along q,

@@ -77,6 +77,7 @@ def test_lookup_error_codes():
 
 def test_override_counts_and_restores():
     h = dispatch.lookup("core", "gpu", "add")
+    fn0 = h.fn
     calls = []
     restore = dispatch.override_op("core", "gpu", "add",
                                    lambda orig: (lambda *a: calls.append(len(a))))
@@ -84,7 +85,7 @@ def test_override_counts_and_restores():
     h(1, 2, 3)
     assert calls == [3] and h.call_count == before + 1
     restore()
-    assert h._current is h._original
+    assert h.fn is fn0
 
 
 def test_scalar_packing_roundtrip():

@@ -503,3 +503,31 @@ def test_block_pool_falls_back_to_events_without_stream_memory_ops():
     st = rt.pool.stats()
     assert st["reused"] > 0 and st["released"] > 0
     assert records   # the markers were CUDA events
+
+
+def test_c_host_path_does_not_leak(env):
+    """Reference counts of the C entries (hostsrc/tpg_pyfast.c): repeated
+    cfg2-shaped adds (lazy cast fused), unaries, reductions and lazy casts
+    leave the interpreter's allocated-block count flat
+    (scripts/plugin_leak_probe.py is the long version)."""
+    import sys
+    tp, gpu, fake, rt = env
+    X = _on(tp, gpu, [[i - 8 for i in range(16)] for _ in range(16)], tp.int16)
+    R = _on(tp, gpu, [[0.5 * i for i in range(16)]], tp.float)
+    V = tp.apply_index(tp.transpose(X), (slice(None, None, -1), slice(None)))
+
+    def rounds(n):
+        for _ in range(n):
+            tp.add(V, R)
+            tp.negate(R)
+            tp.reduce("sum", R)
+            tp.cast(V, tp.float)
+            if fake is not None:
+                fake.calls.clear()  # the test double's own launch log
+        gpu.default_stream().sync()
+        gc.collect()
+        return sys.getallocatedblocks()
+    rounds(300)
+    b0 = rounds(1000)
+    b1 = rounds(3000)
+    assert b1 - b0 < 100, (b0, b1)
